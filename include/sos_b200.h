@@ -1,0 +1,139 @@
+/*
+ * sos_b200.h -- C ABI of the B200 (sm_100a) SOS loss-and-gradient path.
+ *
+ * The method (PAPER.md = arxiv 2410.19844 text, cited by line):
+ *   A form p of degree 2d in n variables is fitted by p ~ sum_k q_k^2 with
+ *   q_k = m_d . v_k, i.e. p = m_d V V^T m_d^T (PAPER.md:45-48,
+ *   Eq. 1 with B = V V^T), by minimising the squared coefficient distance
+ *   L(V) = || coef(m_d V V^T m_d^T) - p ||^2            (Eq. 2)
+ *   with a first-order method ("basic ADAM approach").
+ *   m_d holds the N = C(n+d-1, d) degree-d monomials; the
+ *   target has M = C(n+2d-1, 2d) coefficients.
+ *
+ * Conventions (all entry points):
+ *   - Monomial order: colex order of the sorted variable-index multiset,
+ *     i.e. the combinatorial number system: the multiset m_1<=...<=m_D has
+ *     rank sum_k C(m_k + k - 1, k).  For n=d=2 this is (x1^2, x1x2, x2^2),
+ *     the order of PAPER.md:53.
+ *   - V is N x r, fp32, row-major (row i = monomial alpha_i, column k = square k).
+ *   - Coefficient vectors (coef, p, residual) are length M, fp32, in the
+ *     degree-2d colex order.
+ *   - Pointers named *_dev are CUDA device pointers; *_host are host pointers.
+ *     The library never takes ownership of caller buffers.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Calls are asynchronous on that stream unless stated otherwise.
+ *   - Every call returns SOS_OK (0) or an error code; sos_last_error() gives a
+ *     thread-local message.  On error no output is guaranteed to be written.
+ *   - Requires a compute-capability 10.0 device (B200); there is no CPU path:
+ *     without one every compute call returns SOS_ERR_DEVICE.
+ */
+#ifndef SOS_B200_H
+#define SOS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SOS_OK 0
+#define SOS_ERR_ARG 1    /* invalid argument (sizes, null pointers, n/d out of range) */
+#define SOS_ERR_CUDA 2   /* CUDA runtime error; message in sos_last_error() */
+#define SOS_ERR_NOMEM 3  /* device allocation failed */
+#define SOS_ERR_DEVICE 4 /* no sm_100 device visible */
+
+typedef struct sos_index sos_index; /* monomial tables + pair-rank table (device) */
+typedef struct sos_plan sos_plan;   /* per-(index, r) workspaces and optimiser state */
+
+/* Thread-local description of the last error ("" if none). */
+const char *sos_last_error(void);
+
+/* ABI version (increments on incompatible change). */
+int sos_version(void);
+
+/* ------------------------------------------------------------------------
+ * Index (the degree-d basis m_d and the degree-2d basis).
+ * ------------------------------------------------------------------------ */
+
+/* Build the index for n variables and half-degree d on the current device:
+ * the colex-ordered exponent table of the N degree-d monomials, and the table
+ * rank(alpha_i + alpha_j) in the degree-2d basis for every ordered pair (i,j),
+ * computed by the combinatorial number system.  Synchronous.
+ * Limits: 1 <= n, 1 <= d, n + 2d <= 64, M < 2^32 - 1, N <= 65536.
+ * Device memory: about 4*Np^2 bytes (Np = N rounded up to 256). */
+int sos_build_index(int n, int d, sos_index **out);
+int sos_index_destroy(sos_index *idx);
+
+/* N (degree-d monomials) and M (degree-2d coefficients). */
+int sos_index_dims(const sos_index *idx, int64_t *N, int64_t *M);
+
+/* Copy the degree-d exponent table (N x n, uint8, row-major) to alpha_dev. */
+int sos_index_alpha(const sos_index *idx, uint8_t *alpha_dev, void *stream);
+
+/* Write the degree-2d exponent table (M x n, uint8, row-major) to beta_dev
+ * (computed on the device by colex unranking). */
+int sos_index_beta(const sos_index *idx, uint8_t *beta_dev, void *stream);
+
+/* out_dev[t] = rank(alpha_{i_dev[t]} + alpha_{j_dev[t]}) read from the stored
+ * pair-rank table, t < count; 0 <= i,j < N (else SOS_ERR_ARG is NOT detected on
+ * device: out-of-range pairs yield 0xFFFFFFFF). */
+int sos_index_pair_ranks(const sos_index *idx, const int64_t *i_dev, const int64_t *j_dev,
+                         int64_t count, uint32_t *out_dev, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Plan: workspaces for one (index, r).  Device memory ~ 4*Np*(2*r + Np) bytes
+ * plus 8*N*r for the gradient scratch (and 8*N*r more once Adam is enabled).
+ * ------------------------------------------------------------------------ */
+int sos_plan_create(const sos_index *idx, int64_t r, sos_plan **out);
+int sos_plan_destroy(sos_plan *plan);
+
+/* Number of kernels this library launched through `plan` so far. */
+int64_t sos_plan_launch_count(const sos_plan *plan);
+
+/* coef_dev[M] = coefficients of m_d V V^T m_d^T (PAPER.md:45-48 with B = V V^T):
+ * coef_beta = sum over ordered pairs (i,j) with alpha_i + alpha_j = beta of
+ * <V_i, V_j>.  Computed on tensor cores (fp16 hi/lo split, 3 products, fp32
+ * accumulate: fp32-class accuracy), reduced into coef in the GEMM epilogue. */
+int sos_forward(sos_plan *plan, const float *V_dev, float *coef_dev, void *stream);
+
+/* grad_dev[N x r] = 4 R V with R_ij = res[rank(alpha_i + alpha_j)]: the
+ * gradient of Eq. 2 for residual res = coef - p (length M). */
+int sos_backward(sos_plan *plan, const float *V_dev, const float *res_dev, float *grad_dev,
+                 void *stream);
+
+/* loss_dev[0] = ||coef(V) - p||^2 (fp64), grad_dev = dL/dV = 4 R V.
+ * grad_dev may be NULL (loss only).  res_dev, if not NULL, receives coef - p. */
+int sos_loss_grad(sos_plan *plan, const float *V_dev, const float *p_dev, double *loss_dev,
+                  float *grad_dev, float *res_dev, void *stream);
+
+/* ------------------------------------------------------------------------
+ * First-order optimiser ("basic ADAM approach"; plain GD).
+ * ------------------------------------------------------------------------ */
+#define SOS_OPT_GD 0
+#define SOS_OPT_ADAM 1
+typedef struct {
+    int kind;     /* SOS_OPT_GD or SOS_OPT_ADAM */
+    float lr;     /* step size */
+    float beta1;  /* Adam only */
+    float beta2;  /* Adam only */
+    float eps;    /* Adam only */
+} sos_opt_params;
+
+/* Reset the optimiser: zero the Adam moments, step counter t = 0. */
+int sos_opt_init(sos_plan *plan, const sos_opt_params *params, void *stream);
+
+/* One descent step, in place on V_dev:  loss_dev[0] = L(V) (before the update),
+ * then V <- V - lr*g (GD) or the bias-corrected Adam update with t += 1. */
+int sos_step(sos_plan *plan, float *V_dev, const float *p_dev, double *loss_dev, void *stream);
+
+/* Host-buffer entry point: copies p_host (M) and V_host (N x r) to the device,
+ * runs `steps` sos_step calls, copies V back to V_host and the per-step losses
+ * (steps values, fp64) to losses_host.  Synchronous.  Uses the plan's
+ * optimiser settings (sos_opt_init must have been called). */
+int sos_solve_host(sos_plan *plan, float *V_host, const float *p_host, int64_t steps,
+                   double *losses_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOS_B200_H */

@@ -1,0 +1,357 @@
+// sos_api.cu -- the C ABI declared in include/sos_b200.h (host side).
+// Argument checking, device memory ownership, launch sequencing.  Every
+// arithmetic step of the path runs in the kernels of sos_index.cu,
+// sos_pointwise.cu and sos_gemm.cu; there is no host or CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/sos_b200.h"
+#include "sos_internal.cuh"
+
+using namespace sos;
+
+struct sos_index {
+    Index ix;
+};
+struct sos_plan {
+    Plan P;
+};
+
+static thread_local char g_err[512] = "";
+
+static int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) return fail(SOS_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+static int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SOS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return SOS_OK;
+}
+
+static int require_device(int* num_sms) {
+    int dev = 0, count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(SOS_ERR_DEVICE, "no CUDA device");
+    }
+    CK(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10) return fail(SOS_ERR_DEVICE, "device %s is sm_%d%d, need sm_100", prop.name, prop.major, prop.minor);
+    if (num_sms) *num_sms = prop.multiProcessorCount;
+    return SOS_OK;
+}
+
+static uint64_t binom_u64(int x, int k) {
+    if (k < 0 || k > x) return 0;
+    unsigned __int128 c = 1;
+    for (int t = 1; t <= k; ++t) {
+        c = c * (unsigned)(x - k + t) / (unsigned)t;
+        if (c > (unsigned __int128)UINT64_MAX) return UINT64_MAX;
+    }
+    return (uint64_t)c;
+}
+
+template <class T>
+static int dalloc(T** p, size_t bytes) {
+    if (cudaMalloc(reinterpret_cast<void**>(p), bytes) != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return fail(SOS_ERR_NOMEM, "cudaMalloc(%zu) failed", bytes);
+    }
+    return SOS_OK;
+}
+
+extern "C" {
+
+const char* sos_last_error(void) { return g_err; }
+int sos_version(void) { return 1; }
+
+// ------------------------------------------------------------------ index --
+int sos_build_index(int n, int d, sos_index** out) {
+    if (!out) return fail(SOS_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (n < 1 || d < 1 || n + 2 * d > kMaxVars) return fail(SOS_ERR_ARG, "need n>=1, d>=1, n+2d<=%d", kMaxVars);
+    const uint64_t N = binom_u64(n + d - 1, d), M = binom_u64(n + 2 * d - 1, 2 * d);
+    if (N > 65536) return fail(SOS_ERR_ARG, "N=%llu > 65536", (unsigned long long)N);
+    if (M >= 0xFFFFFFFFull) return fail(SOS_ERR_ARG, "M=%llu does not fit uint32 ranks", (unsigned long long)M);
+    int sms = 0;
+    int rc = require_device(&sms);
+    if (rc) return rc;
+
+    sos_index* h = new sos_index();
+    Index& ix = h->ix;
+    ix.n = n;
+    ix.d = d;
+    ix.N = (int64_t)N;
+    ix.M = (int64_t)M;
+    ix.Np = ((ix.N + kPad - 1) / kPad) * kPad;
+    ix.nb = n + 2 * d;
+    const int bstride = 2 * d + 1;
+    std::vector<uint32_t> hb((size_t)ix.nb * bstride);
+    for (int x = 0; x < ix.nb; ++x)
+        for (int k = 0; k < bstride; ++k) {
+            uint64_t c = binom_u64(x, k);
+            hb[(size_t)x * bstride + k] = c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
+        }
+    if ((rc = dalloc(&ix.d_binom, hb.size() * 4)) || (rc = dalloc(&ix.d_ms, (size_t)ix.N * d)) ||
+        (rc = dalloc(&ix.d_alpha, (size_t)ix.N * n)) ||
+        (rc = dalloc(&ix.d_pt, (size_t)ix.Np * ix.Np * 4))) {
+        sos_index_destroy(h);
+        return rc;
+    }
+    if (cudaMemcpy(ix.d_binom, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        sos_index_destroy(h);
+        return fail(SOS_ERR_CUDA, "copy binomial table");
+    }
+    launch_index_build(ix, 0);
+    if ((rc = check_launch("index build")) || (cudaDeviceSynchronize() != cudaSuccess)) {
+        if (!rc) rc = fail(SOS_ERR_CUDA, "index build: %s", cudaGetErrorString(cudaGetLastError()));
+        sos_index_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return SOS_OK;
+}
+
+int sos_index_destroy(sos_index* h) {
+    if (!h) return SOS_OK;
+    cudaFree(h->ix.d_binom);
+    cudaFree(h->ix.d_ms);
+    cudaFree(h->ix.d_alpha);
+    cudaFree(h->ix.d_pt);
+    delete h;
+    return SOS_OK;
+}
+
+int sos_index_dims(const sos_index* h, int64_t* N, int64_t* M) {
+    if (!h) return fail(SOS_ERR_ARG, "index is NULL");
+    if (N) *N = h->ix.N;
+    if (M) *M = h->ix.M;
+    return SOS_OK;
+}
+
+int sos_index_alpha(const sos_index* h, uint8_t* alpha_dev, void* stream) {
+    if (!h || !alpha_dev) return fail(SOS_ERR_ARG, "NULL argument");
+    CK(cudaMemcpyAsync(alpha_dev, h->ix.d_alpha, (size_t)h->ix.N * h->ix.n, cudaMemcpyDeviceToDevice,
+                       (cudaStream_t)stream));
+    return SOS_OK;
+}
+
+int sos_index_beta(const sos_index* h, uint8_t* beta_dev, void* stream) {
+    if (!h || !beta_dev) return fail(SOS_ERR_ARG, "NULL argument");
+    launch_beta_table(h->ix, beta_dev, (cudaStream_t)stream);
+    return check_launch("beta table");
+}
+
+int sos_index_pair_ranks(const sos_index* h, const int64_t* i_dev, const int64_t* j_dev, int64_t count,
+                         uint32_t* out_dev, void* stream) {
+    if (!h || count < 0 || (count > 0 && (!i_dev || !j_dev || !out_dev))) return fail(SOS_ERR_ARG, "bad argument");
+    launch_pair_lookup(h->ix, i_dev, j_dev, count, out_dev, (cudaStream_t)stream);
+    return check_launch("pair lookup");
+}
+
+// ------------------------------------------------------------------- plan --
+static void build_tiles(int64_t Np, int64_t ncols_blocks, bool upper, std::vector<TileCoord>& out) {
+    // grouped raster: 16 consecutive 128-row blocks share the B panels of a wave
+    const int64_t na = Np / kBlockM;
+    const int64_t GA = 16;
+    for (int64_t g0 = 0; g0 < na; g0 += GA) {
+        const int64_t g1 = std::min(na, g0 + GA);
+        for (int64_t b = 0; b < ncols_blocks; ++b)
+            for (int64_t a = g0; a < g1; ++a) {
+                if (upper && b * kBlockN + kBlockN - 1 < a * kBlockM) continue;  // entirely below diagonal
+                out.push_back(TileCoord{(int)a, (int)b});
+            }
+    }
+}
+
+int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
+    if (!h || !out || r < 1) return fail(SOS_ERR_ARG, "bad argument");
+    *out = nullptr;
+    int sms = 0;
+    int rc = require_device(&sms);
+    if (rc) return rc;
+    sos_plan* pl = new sos_plan();
+    Plan& P = pl->P;
+    P.idx = &h->ix;
+    P.r = r;
+    P.rK = ((r + kBlockK - 1) / kBlockK) * kBlockK;
+    P.rN = ((r + kBlockN - 1) / kBlockN) * kBlockN;
+    P.num_sms = sms;
+    const int64_t Np = h->ix.Np, N = h->ix.N, M = h->ix.M;
+    std::vector<TileCoord> tf, tb;
+    build_tiles(Np, Np / kBlockN, true, tf);
+    build_tiles(Np, P.rN / kBlockN, false, tb);
+    P.ntiles_fwd = (int)tf.size();
+    P.ntiles_bwd = (int)tb.size();
+    if ((rc = dalloc(&P.d_vs, (size_t)(P.rK / 32) * Np * 128)) || (rc = dalloc(&P.d_vts, (size_t)(Np / 32) * P.rN * 128)) ||
+        (rc = dalloc(&P.d_rs, (size_t)(Np / 32) * Np * 128)) || (rc = dalloc(&P.d_coef, (size_t)M * 4)) ||
+        (rc = dalloc(&P.d_res, (size_t)M * 4)) || (rc = dalloc(&P.d_grad, (size_t)N * r * 4)) ||
+        (rc = dalloc(&P.d_scal, sizeof(Scalars))) || (rc = dalloc(&P.d_tiles_fwd, tf.size() * sizeof(TileCoord))) ||
+        (rc = dalloc(&P.d_tiles_bwd, tb.size() * sizeof(TileCoord)))) {
+        sos_plan_destroy(pl);
+        return rc;
+    }
+    if (cudaMemcpy(P.d_tiles_fwd, tf.data(), tf.size() * sizeof(TileCoord), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(P.d_tiles_bwd, tb.data(), tb.size() * sizeof(TileCoord), cudaMemcpyHostToDevice) != cudaSuccess) {
+        sos_plan_destroy(pl);
+        return fail(SOS_ERR_CUDA, "tile list upload");
+    }
+    P.opt_kind = SOS_OPT_GD;
+    P.lr = 0.f;
+    P.opt_ready = false;
+    *out = pl;
+    return SOS_OK;
+}
+
+int sos_plan_destroy(sos_plan* pl) {
+    if (!pl) return SOS_OK;
+    Plan& P = pl->P;
+    cudaFree(P.d_vs);
+    cudaFree(P.d_vts);
+    cudaFree(P.d_rs);
+    cudaFree(P.d_coef);
+    cudaFree(P.d_res);
+    cudaFree(P.d_grad);
+    cudaFree(P.d_m);
+    cudaFree(P.d_v);
+    cudaFree(P.d_scal);
+    cudaFree(P.d_tiles_fwd);
+    cudaFree(P.d_tiles_bwd);
+    delete pl;
+    return SOS_OK;
+}
+
+int64_t sos_plan_launch_count(const sos_plan* pl) { return pl ? pl->P.launches : -1; }
+
+// --------------------------------------------------------------- compute --
+static int do_forward(Plan& P, const float* V, float* coef, cudaStream_t st) {
+    CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
+    CK(cudaMemsetAsync(coef, 0, (size_t)P.idx->M * 4, st));
+    launch_absmax_v(P, V, st);
+    launch_pack_v(P, V, st);
+    launch_gemm_fwd(P, coef, st);
+    return check_launch("forward");
+}
+
+int sos_forward(sos_plan* pl, const float* V_dev, float* coef_dev, void* stream) {
+    if (!pl || !V_dev || !coef_dev) return fail(SOS_ERR_ARG, "NULL argument");
+    return do_forward(pl->P, V_dev, coef_dev, (cudaStream_t)stream);
+}
+
+int sos_backward(sos_plan* pl, const float* V_dev, const float* res_dev, float* grad_dev, void* stream) {
+    if (!pl || !V_dev || !res_dev || !grad_dev) return fail(SOS_ERR_ARG, "NULL argument");
+    Plan& P = pl->P;
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
+    launch_absmax_v(P, V_dev, st);
+    launch_pack_v(P, V_dev, st);
+    launch_absmax_res(P, res_dev, st);
+    launch_pack_r(P, res_dev, st);
+    launch_gemm_bwd(P, grad_dev, st);
+    return check_launch("backward");
+}
+
+static int do_loss_grad(Plan& P, const float* V, const float* p, double* loss, float* grad, float* res,
+                        cudaStream_t st) {
+    int rc = do_forward(P, V, P.d_coef, st);
+    if (rc) return rc;
+    float* r = res ? res : P.d_res;
+    launch_residual(P, P.d_coef, p, r, st);
+    if (grad) {
+        launch_pack_r(P, r, st);
+        launch_gemm_bwd(P, grad, st);
+    }
+    if (loss) CK(cudaMemcpyAsync(loss, &P.d_scal->loss, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return check_launch("loss_grad");
+}
+
+int sos_loss_grad(sos_plan* pl, const float* V_dev, const float* p_dev, double* loss_dev, float* grad_dev,
+                  float* res_dev, void* stream) {
+    if (!pl || !V_dev || !p_dev) return fail(SOS_ERR_ARG, "NULL argument");
+    return do_loss_grad(pl->P, V_dev, p_dev, loss_dev, grad_dev, res_dev, (cudaStream_t)stream);
+}
+
+int sos_opt_init(sos_plan* pl, const sos_opt_params* prm, void* stream) {
+    if (!pl || !prm) return fail(SOS_ERR_ARG, "NULL argument");
+    if (prm->kind != SOS_OPT_GD && prm->kind != SOS_OPT_ADAM) return fail(SOS_ERR_ARG, "unknown optimiser %d", prm->kind);
+    if (!(prm->lr > 0.f)) return fail(SOS_ERR_ARG, "lr must be > 0");
+    Plan& P = pl->P;
+    P.opt_kind = prm->kind;
+    P.lr = prm->lr;
+    P.b1 = prm->beta1;
+    P.b2 = prm->beta2;
+    P.eps = prm->eps;
+    P.t = 0;
+    if (prm->kind == SOS_OPT_ADAM) {
+        if (!(prm->beta1 >= 0.f && prm->beta1 < 1.f && prm->beta2 >= 0.f && prm->beta2 < 1.f))
+            return fail(SOS_ERR_ARG, "betas must be in [0,1)");
+        const size_t bytes = (size_t)P.idx->N * P.r * 4;
+        int rc;
+        if (!P.d_m && ((rc = dalloc(&P.d_m, bytes)) || (rc = dalloc(&P.d_v, bytes)))) return rc;
+        CK(cudaMemsetAsync(P.d_m, 0, bytes, (cudaStream_t)stream));
+        CK(cudaMemsetAsync(P.d_v, 0, bytes, (cudaStream_t)stream));
+    }
+    P.opt_ready = true;
+    return SOS_OK;
+}
+
+int sos_step(sos_plan* pl, float* V_dev, const float* p_dev, double* loss_dev, void* stream) {
+    if (!pl || !V_dev || !p_dev) return fail(SOS_ERR_ARG, "NULL argument");
+    Plan& P = pl->P;
+    if (!P.opt_ready) return fail(SOS_ERR_ARG, "sos_opt_init not called");
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = do_loss_grad(P, V_dev, p_dev, loss_dev, P.d_grad, nullptr, st);
+    if (rc) return rc;
+    P.t += 1;
+    launch_update(P, V_dev, P.d_grad, st);
+    return check_launch("step update");
+}
+
+int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t steps, double* losses_host) {
+    if (!pl || !V_host || !p_host || steps < 0 || (steps > 0 && !losses_host)) return fail(SOS_ERR_ARG, "bad argument");
+    Plan& P = pl->P;
+    const size_t vb = (size_t)P.idx->N * P.r * 4, pb = (size_t)P.idx->M * 4;
+    float *dV = nullptr, *dp = nullptr;
+    double* dl = nullptr;
+    int rc;
+    if ((rc = dalloc(&dV, vb)) || (rc = dalloc(&dp, pb)) || (rc = dalloc(&dl, sizeof(double) * (steps > 0 ? steps : 1)))) {
+        cudaFree(dV);
+        cudaFree(dp);
+        return rc;
+    }
+    cudaStream_t st = 0;
+    rc = SOS_OK;
+    if (cudaMemcpyAsync(dV, V_host, vb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(dp, p_host, pb, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        rc = fail(SOS_ERR_CUDA, "H2D copy");
+    for (int64_t t = 0; !rc && t < steps; ++t) rc = sos_step(pl, dV, dp, dl + t, st);
+    if (!rc && (cudaMemcpyAsync(V_host, dV, vb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                (steps > 0 && cudaMemcpyAsync(losses_host, dl, sizeof(double) * steps, cudaMemcpyDeviceToHost, st) != cudaSuccess) ||
+                cudaStreamSynchronize(st) != cudaSuccess))
+        rc = fail(SOS_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
+    cudaFree(dV);
+    cudaFree(dp);
+    cudaFree(dl);
+    return rc;
+}
+
+}  // extern "C"

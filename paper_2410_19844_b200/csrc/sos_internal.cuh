@@ -1,0 +1,91 @@
+// sos_internal.cuh -- shared definitions of the CUDA path (not part of the ABI).
+//
+// HBM layouts:
+//   * split operand tiles "S-layout": an fp32 matrix X[rows][K] is stored as
+//     fp16 hi/lo pairs scaled by a power of two s (x*s = hi + lo + O(2^-22 |x*s|)),
+//     in K-blocks of 32:   byte offset of row `row`, K-block kb =
+//         (kb * rows_total + row) * 128
+//     and inside that 128-byte row the 16-byte chunk c (c<4: hi of k=8c..8c+7,
+//     c>=4: lo of k=8(c-4)..) lives at physical chunk c ^ (row & 7) -- exactly
+//     the UMMA K-major SWIZZLE_128B image, so a 128-row x 32-K tile is one
+//     contiguous 16 KB block copied to shared memory by one bulk copy.
+//       VS  = V   as [rK/32][Np][128B]   (forward A and B operands, K = column of V)
+//       VTS = V^T as [Np/32][rN][128B]   (backward B operand, K = row of V)
+//       RS  = R   as [Np/32][Np][128B]   (backward A operand, K = column j of R)
+//   * pair-rank table PT[jb][i][32] (uint32): PT[((j/32)*Np + i)*32 + j%32] =
+//     rank(alpha_i + alpha_j), 0xFFFFFFFF for padding (i >= N or j >= N).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace sos {
+
+constexpr int kBlockM = 128;   // tile rows  (UMMA M)
+constexpr int kBlockN = 256;   // tile cols  (UMMA N)
+constexpr int kBlockK = 32;    // fp32-equivalent K per stage (hi+lo = 128 B rows)
+constexpr int kPad = 256;      // Np = N rounded up to kPad
+constexpr int kStages = 4;
+constexpr uint32_t kTileABytes = kBlockM * 128;  // 16 KB
+constexpr uint32_t kTileBBytes = kBlockN * 128;  // 32 KB
+constexpr uint32_t kStageBytes = kTileABytes + kTileBBytes;
+constexpr int kGemmThreads = 192;  // warp0 producer, warp1 MMA, warps2-5 epilogue
+constexpr uint32_t kInvalidRank = 0xFFFFFFFFu;
+constexpr int kMaxVars = 64;       // n + 2d <= 64
+constexpr int kMaxDeg2 = 64;
+
+struct Scalars {           // device-resident per-step scalars
+    unsigned int absmax_v; // float bits of max |V|
+    unsigned int absmax_r; // float bits of max |res|
+    float s_v;             // power-of-two scale for the V split
+    float s_r;             // power-of-two scale for the R split
+    double loss;           // sum res^2
+    double pnorm2;         // sum p^2
+};
+
+struct Index {
+    int n, d;
+    int64_t N, M, Np;
+    int nb;                    // rows of the binomial table = n + 2d
+    uint32_t* d_binom;         // [nb][2d+1] C(x,k), x < nb, k <= 2d   (device)
+    uint8_t* d_ms;             // [N][d] sorted variable indices of alpha_i
+    uint8_t* d_alpha;          // [N][n] exponents of alpha_i
+    uint32_t* d_pt;            // pair-rank table PT (Np*Np)
+};
+
+struct TileCoord { int a; int b; };  // a: 128-row block, b: 256-col block
+
+struct Plan {
+    const Index* idx;
+    int64_t r, rK, rN;
+    uint8_t* d_vs;    // VS
+    uint8_t* d_vts;   // VTS
+    uint8_t* d_rs;    // RS
+    float* d_coef;    // M
+    float* d_res;     // M
+    float* d_grad;    // N*r (scratch for sos_step)
+    float* d_m;       // Adam moments (lazy)
+    float* d_v;
+    Scalars* d_scal;
+    TileCoord* d_tiles_fwd; int ntiles_fwd;
+    TileCoord* d_tiles_bwd; int ntiles_bwd;
+    int opt_kind; float lr, b1, b2, eps; int64_t t; bool opt_ready;
+    int64_t launches;
+    int num_sms;
+};
+
+// ---- kernels (defined in the .cu files) ----
+void launch_index_build(Index& ix, cudaStream_t st);
+void launch_beta_table(const Index& ix, uint8_t* beta, cudaStream_t st);
+void launch_pair_lookup(const Index& ix, const int64_t* i, const int64_t* j, int64_t cnt, uint32_t* out,
+                        cudaStream_t st);
+
+void launch_absmax_v(Plan& P, const float* V, cudaStream_t st);
+void launch_pack_v(Plan& P, const float* V, cudaStream_t st);
+void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
+void launch_absmax_res(Plan& P, const float* res, cudaStream_t st);
+void launch_pack_r(Plan& P, const float* res, cudaStream_t st);
+void launch_gemm_fwd(Plan& P, float* coef, cudaStream_t st);
+void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st);
+void launch_update(Plan& P, float* V, const float* grad, cudaStream_t st);
+
+}  // namespace sos

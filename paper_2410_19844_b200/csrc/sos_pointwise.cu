@@ -1,0 +1,286 @@
+// sos_pointwise.cu -- HBM-bound kernels of the step: operand split/pack of V
+// and of the residual matrix R, the fused residual + loss reduction, and the
+// optimiser update.  All are coalesced, vectorised where the
+// layout allows, and sized as a multiple of the SM count (grid-stride).
+#include <cuda_fp16.h>
+
+#include "sos_internal.cuh"
+
+namespace sos {
+
+// power-of-two scale s with max|x| * s < 2^14 (fp16 hi/lo split headroom)
+__device__ __forceinline__ float split_scale(unsigned int absmax_bits) {
+    float a = __uint_as_float(absmax_bits);
+    if (!(a > 0.f) || !isfinite(a)) return 1.f;
+    int e;
+    frexpf(a, &e);  // a = f * 2^e, f in [0.5, 1)  =>  a < 2^e
+    return ldexpf(1.f, 14 - e);
+}
+
+// x*s = hi + lo with hi = fp16(x*s), lo = fp16(x*s - hi): ~22 significant bits
+__device__ __forceinline__ void split8(const float* x, uint4& hi, uint4& lo) {
+    __half h[8], l[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        h[t] = __float2half_rn(x[t]);
+        l[t] = __float2half_rn(x[t] - __half2float(h[t]));
+    }
+    hi = *reinterpret_cast<uint4*>(h);
+    lo = *reinterpret_cast<uint4*>(l);
+}
+
+__device__ __forceinline__ void store_split_row(uint8_t* row128, int64_t row, int q, const float* x8) {
+    uint4 hi, lo;
+    split8(x8, hi, lo);
+    const int sw = (int)(row & 7);
+    reinterpret_cast<uint4*>(row128)[q ^ sw] = hi;
+    reinterpret_cast<uint4*>(row128)[(4 + q) ^ sw] = lo;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ---------------------------------------------------------------- absmax ---
+__global__ void k_absmax(const float* __restrict__ x, int64_t len, unsigned int* __restrict__ out) {
+    float m = 0.f;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        const int64_t n4 = len >> 2;
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        for (int64_t t = tid; t < n4; t += stride) {
+            float4 v = __ldg(x4 + t);
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+        for (int64_t t = (n4 << 2) + tid; t < len; t += stride) m = fmaxf(m, fabsf(x[t]));
+    } else {
+        for (int64_t t = tid; t < len; t += stride) m = fmaxf(m, fabsf(x[t]));
+    }
+    m = warp_max(m);
+    __shared__ float s[32];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = (threadIdx.x < (blockDim.x >> 5)) ? s[threadIdx.x] : 0.f;
+        m = warp_max(m);
+        if (threadIdx.x == 0) atomicMax(out, __float_as_uint(m));
+    }
+}
+
+// --------------------------------------------------------------- pack V ----
+// One block = 32 rows (j) x 64 columns (c) of V.  Writes the VS tile rows
+// (K = column) and the VTS tile rows (K = row) of the S-layout.
+__global__ void __launch_bounds__(256) k_pack_v(const float* __restrict__ V, int64_t N, int64_t r, int64_t Np,
+                                                int64_t rK, int64_t rN, Scalars* __restrict__ sc,
+                                                uint8_t* __restrict__ VS, uint8_t* __restrict__ VTS) {
+    __shared__ float tile[32][65];
+    const int tid = threadIdx.x;
+    const int64_t j0 = (int64_t)blockIdx.y * 32;
+    const int64_t c0 = (int64_t)blockIdx.x * 64;
+    const float s = split_scale(sc->absmax_v);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) sc->s_v = s;
+    for (int e = tid; e < 32 * 64; e += 256) {
+        const int jj = e >> 6, cc = e & 63;
+        const int64_t j = j0 + jj, c = c0 + cc;
+        tile[jj][cc] = (j < N && c < r) ? V[j * r + c] * s : 0.f;
+    }
+    __syncthreads();
+    {  // VS: 32 rows x 2 K-blocks x 4 chunks
+        const int jj = tid >> 3, h = (tid >> 2) & 1, q = tid & 3;
+        const int64_t kb = (c0 >> 5) + h;
+        if (kb < (rK >> 5)) {
+            float x[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) x[t] = tile[jj][h * 32 + q * 8 + t];
+            const int64_t row = j0 + jj;
+            store_split_row(VS + (kb * Np + row) * 128, row, q, x);
+        }
+    }
+    {  // VTS: 64 rows (c) x 4 chunks, K-block jb = j0/32
+        const int cc = tid >> 2, q = tid & 3;
+        const int64_t c = c0 + cc;
+        if (c < rN) {
+            float x[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) x[t] = tile[q * 8 + t][cc];
+            store_split_row(VTS + ((j0 >> 5) * rN + c) * 128, c, q, x);
+        }
+    }
+}
+
+// ------------------------------------------------------------- residual ----
+// res = coef - p ; loss += res^2 ; pnorm2 += p^2 ; absmax_r = max |res|
+__global__ void k_residual(const float* __restrict__ coef, const float* __restrict__ p, float* __restrict__ res,
+                           int64_t M, Scalars* __restrict__ sc) {
+    double l = 0.0, pn = 0.0;
+    float m = 0.f;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M; t += stride) {
+        const float pv = p[t];
+        const float rv = coef[t] - pv;
+        res[t] = rv;
+        l += (double)rv * rv;
+        pn += (double)pv * pv;
+        m = fmaxf(m, fabsf(rv));
+    }
+    l = warp_sum(l);
+    pn = warp_sum(pn);
+    m = warp_max(m);
+    __shared__ double s_l[32], s_p[32];
+    __shared__ float s_m[32];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { s_l[w] = l; s_p[w] = pn; s_m[w] = m; }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        l = lane < nw ? s_l[lane] : 0.0;
+        pn = lane < nw ? s_p[lane] : 0.0;
+        m = lane < nw ? s_m[lane] : 0.f;
+        l = warp_sum(l);
+        pn = warp_sum(pn);
+        m = warp_max(m);
+        if (lane == 0) {
+            atomicAdd(&sc->loss, l);
+            atomicAdd(&sc->pnorm2, pn);
+            atomicMax(&sc->absmax_r, __float_as_uint(m));
+        }
+    }
+}
+
+// --------------------------------------------------------------- pack R ----
+// R_ij = res[rank(alpha_i + alpha_j)] gathered through the pair-rank table,
+// written as the RS S-layout (same [jb][i][32] row structure as PT).
+__global__ void __launch_bounds__(256) k_pack_r(const uint32_t* __restrict__ pt, const float* __restrict__ res,
+                                                int64_t rows8, Scalars* __restrict__ sc, uint8_t* __restrict__ RS) {
+    const float s = split_scale(sc->absmax_r);
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->s_r = s;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows8; t += stride) {
+        const uint4* p4 = reinterpret_cast<const uint4*>(pt + t * 8);
+        const uint4 k0 = __ldg(p4), k1 = __ldg(p4 + 1);
+        const uint32_t k[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+        float x[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = (k[e] != kInvalidRank) ? __ldg(res + k[e]) * s : 0.f;
+        const int64_t row = t >> 2;  // = jb*Np + i ; i & 7 == row & 7 since Np % 8 == 0
+        store_split_row(RS + row * 128, row, (int)(t & 3), x);
+    }
+}
+
+// --------------------------------------------------------------- update ----
+__global__ void k_update_gd(float* __restrict__ V, const float* __restrict__ g, int64_t len, float lr) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(V) | reinterpret_cast<uintptr_t>(g)) & 15) == 0;
+    int64_t done = 0;
+    if (vec) {
+        const int64_t n4 = len >> 2;
+        float4* V4 = reinterpret_cast<float4*>(V);
+        const float4* g4 = reinterpret_cast<const float4*>(g);
+        for (int64_t t = tid; t < n4; t += stride) {
+            float4 v = V4[t];
+            const float4 d = __ldg(g4 + t);
+            v.x -= lr * d.x; v.y -= lr * d.y; v.z -= lr * d.z; v.w -= lr * d.w;
+            V4[t] = v;
+        }
+        done = n4 << 2;
+    }
+    for (int64_t t = done + tid; t < len; t += stride) V[t] -= lr * g[t];
+}
+
+__device__ __forceinline__ float adam_one(float& m, float& v, float g, float b1, float b2, float lr_c1, float inv_sqrt_c2,
+                                          float eps) {
+    m = b1 * m + (1.f - b1) * g;
+    v = b2 * v + (1.f - b2) * g * g;
+    return lr_c1 * m / (sqrtf(v) * inv_sqrt_c2 + eps);
+}
+
+// Adam: m <- b1 m + (1-b1) g ; v <- b2 v + (1-b2) g^2 ;
+// V <- V - lr (m/c1) / (sqrt(v/c2) + eps),  c1 = 1-b1^t, c2 = 1-b2^t
+__global__ void k_update_adam(float* __restrict__ V, const float* __restrict__ g, float* __restrict__ m,
+                              float* __restrict__ v, int64_t len, float lr_c1, float inv_sqrt_c2, float b1, float b2,
+                              float eps) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(V) | reinterpret_cast<uintptr_t>(g)) & 15) == 0;
+    int64_t done = 0;
+    if (vec) {
+        const int64_t n4 = len >> 2;
+        float4* V4 = reinterpret_cast<float4*>(V);
+        float4* m4 = reinterpret_cast<float4*>(m);
+        float4* v4 = reinterpret_cast<float4*>(v);
+        const float4* g4 = reinterpret_cast<const float4*>(g);
+        for (int64_t t = tid; t < n4; t += stride) {
+            float4 x = V4[t], mm = m4[t], vv = v4[t];
+            const float4 d = __ldg(g4 + t);
+            x.x -= adam_one(mm.x, vv.x, d.x, b1, b2, lr_c1, inv_sqrt_c2, eps);
+            x.y -= adam_one(mm.y, vv.y, d.y, b1, b2, lr_c1, inv_sqrt_c2, eps);
+            x.z -= adam_one(mm.z, vv.z, d.z, b1, b2, lr_c1, inv_sqrt_c2, eps);
+            x.w -= adam_one(mm.w, vv.w, d.w, b1, b2, lr_c1, inv_sqrt_c2, eps);
+            V4[t] = x; m4[t] = mm; v4[t] = vv;
+        }
+        done = n4 << 2;
+    }
+    for (int64_t t = done + tid; t < len; t += stride)
+        V[t] -= adam_one(m[t], v[t], g[t], b1, b2, lr_c1, inv_sqrt_c2, eps);
+}
+
+// -------------------------------------------------------------- launches ---
+static int grid_for(const Plan& P, int64_t work, int threads, int per_sm = 8) {
+    int64_t b = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)P.num_sms * per_sm;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+void launch_absmax_v(Plan& P, const float* V, cudaStream_t st) {
+    const int64_t len = P.idx->N * P.r;
+    k_absmax<<<grid_for(P, len / 4, 256), 256, 0, st>>>(V, len, &P.d_scal->absmax_v);
+    P.launches++;
+}
+
+void launch_absmax_res(Plan& P, const float* res, cudaStream_t st) {
+    k_absmax<<<grid_for(P, P.idx->M / 4, 256), 256, 0, st>>>(res, P.idx->M, &P.d_scal->absmax_r);
+    P.launches++;
+}
+
+void launch_pack_v(Plan& P, const float* V, cudaStream_t st) {
+    dim3 grid((unsigned)(P.rN / 64), (unsigned)(P.idx->Np / 32));
+    k_pack_v<<<grid, 256, 0, st>>>(V, P.idx->N, P.r, P.idx->Np, P.rK, P.rN, P.d_scal, P.d_vs, P.d_vts);
+    P.launches++;
+}
+
+void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st) {
+    k_residual<<<grid_for(P, P.idx->M, 256, 4), 256, 0, st>>>(coef, p, res, P.idx->M, P.d_scal);
+    P.launches++;
+}
+
+void launch_pack_r(Plan& P, const float* res, cudaStream_t st) {
+    const int64_t rows8 = P.idx->Np * P.idx->Np / 8;
+    k_pack_r<<<grid_for(P, rows8, 256), 256, 0, st>>>(P.idx->d_pt, res, rows8, P.d_scal, P.d_rs);
+    P.launches++;
+}
+
+void launch_update(Plan& P, float* V, const float* grad, cudaStream_t st) {
+    const int64_t len = P.idx->N * P.r;
+    if (P.opt_kind == 0) {
+        k_update_gd<<<grid_for(P, len / 4, 256), 256, 0, st>>>(V, grad, len, P.lr);
+    } else {
+        const double c1 = 1.0 - pow((double)P.b1, (double)P.t);
+        const double c2 = 1.0 - pow((double)P.b2, (double)P.t);
+        k_update_adam<<<grid_for(P, len / 4, 256), 256, 0, st>>>(V, grad, P.d_m, P.d_v, len, (float)(P.lr / c1),
+                                                                (float)(1.0 / sqrt(c2)), P.b1, P.b2, P.eps);
+    }
+    P.launches++;
+}
+
+}  // namespace sos

@@ -1,0 +1,232 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bars (BASELINE.json north_star): monomial tables and pair ranks bit-exact;
+coefficients, loss and gradient within relative L2 error 1e-5 of the oracle;
+descent on a planted-SOS target reaches relative residual <= 1e-8.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import seeded_inputs as si
+from oracle import OracleIndex
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-5
+
+
+def rel_l2(got, want):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    den = np.linalg.norm(want)
+    return np.linalg.norm(got - want) / (den if den > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def sos():
+    import paper_2410_19844_b200 as m
+    m.load()
+    return m
+
+
+_ORACLES = {}
+
+
+def oracle(n, d):
+    if (n, d) not in _ORACLES:
+        _ORACLES[(n, d)] = OracleIndex(n, d)
+    return _ORACLES[(n, d)]
+
+
+# (n, d, r): small / ragged / several tiles; includes BASELINE configs 0 and 1
+SHAPES = [
+    (1, 3, 2),      # univariate: N = 1, M = 1
+    (5, 1, 3),      # quadratic forms: N = n
+    (2, 2, 1),      # paper example basis, one square
+    (4, 3, 20),     # config 0
+    (5, 3, 37),     # ragged N = 35, r = 37
+    (7, 4, 64),     # N = 210
+    (8, 4, 330),    # config 1: N = 330 -> 3 row blocks x 2 col blocks, K ragged
+    (9, 4, 300),    # N = 495: 4 x 2 blocks, diagonal straddling tiles
+    (3, 9, 33),     # N = 55, high degree
+]
+
+
+@pytest.mark.parametrize("n,d,r", SHAPES)
+def test_index_tables_bit_exact(sos, n, d, r):
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    assert (ix.N, ix.M) == (o.N, o.M)
+    np.testing.assert_array_equal(ix.alpha().cpu().numpy(), o.alpha())
+    np.testing.assert_array_equal(ix.beta().cpu().numpy(), o.beta())
+    I, J = np.meshgrid(np.arange(o.N), np.arange(o.N), indexing="ij")
+    got = ix.pair_ranks(torch.from_numpy(I.ravel()), torch.from_numpy(J.ravel())).cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(got.reshape(o.N, o.N), o.pair_ranks())
+
+
+@pytest.mark.parametrize("n,d,r", SHAPES)
+def test_forward_parity(sos, n, d, r):
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    V = si.v0(o.N, r, seed=n * 1000 + d * 10 + r)
+    coef = plan.forward(torch.from_numpy(V).cuda()).cpu().numpy()
+    want = o.forward(V)
+    assert rel_l2(coef, want) <= REL_TOL
+
+
+@pytest.mark.parametrize("n,d,r", SHAPES)
+def test_backward_parity(sos, n, d, r):
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    V = si.v0(o.N, r, seed=7 + r)
+    res = si.residual_probe(o.M, seed=5 + n)
+    g = plan.backward(torch.from_numpy(V).cuda(), torch.from_numpy(res).cuda()).cpu().numpy()
+    want = o.grad_rows(V, res, np.arange(o.N))
+    assert rel_l2(g, want) <= REL_TOL
+
+
+@pytest.mark.parametrize("n,d,r", [(4, 3, 20), (8, 4, 330), (9, 4, 300)])
+def test_loss_grad_parity_planted(sos, n, d, r):
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    W = si.planted_w(o.N, max(1, r // 2), seed=1)
+    V = si.v0(o.N, r, seed=2)
+    p = o.forward(W)
+    loss_o, g_o, coef_o, res_o = o.loss_grad(V, p)
+    loss, g, res = plan.loss_grad(torch.from_numpy(V).cuda(), torch.from_numpy(p.astype(np.float32)).cuda(),
+                                  want_res=True)
+    # the GPU sees p rounded to fp32; compare against the oracle on that same p
+    loss_o, g_o, coef_o, res_o = o.loss_grad(V, p.astype(np.float32))
+    assert abs(loss.item() - loss_o) <= REL_TOL * loss_o
+    assert rel_l2(res.cpu().numpy(), res_o) <= REL_TOL
+    assert rel_l2(g.cpu().numpy(), g_o) <= REL_TOL
+
+
+def test_forward_parity_config2(sos):
+    """BASELINE config 2 (n=10, 2d=10, N=2002, r=2002): full coefficient vector."""
+    c = si.CONFIGS["c2_n10_2d10"]
+    o = oracle(c.n, c.d)
+    ix = sos.SosIndex(c.n, c.d)
+    plan = sos.SosPlan(ix, c.r)
+    V = si.v0(o.N, c.r, seed=0)
+    coef = plan.forward(torch.from_numpy(V).cuda()).cpu().numpy()
+    assert rel_l2(coef, o.forward(V)) <= REL_TOL
+
+
+def test_adam_and_gd_step_parity(sos):
+    n, d, r = 5, 3, 37
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    W = si.planted_w(o.N, 10, seed=3)
+    p = o.forward(W).astype(np.float32)
+    V0 = si.v0(o.N, r, seed=4)
+    for kind, lr in (("gd", 1e-3), ("adam", 1e-3)):
+        plan.opt_init(kind, lr)
+        Vd = torch.from_numpy(V0.copy()).cuda()
+        for _ in range(3):
+            plan.step(Vd, torch.from_numpy(p).cuda())
+        Vo, _ = o.descent(V0, p, kind, 3, lr)
+        # compare the parameter change (the update), relative to its own size
+        assert rel_l2(Vd.cpu().numpy() - V0, Vo - V0) <= 1e-4
+
+
+@pytest.mark.parametrize("kind,lr,steps", [("gd", 0.02, 2000)])
+def test_descent_config0_planted(sos, kind, lr, steps):
+    """BASELINE config 0: 2000 GD steps from V0 ~ N(0,1/N) on p = coef(W W^T),
+    r* = 10.  The final V is checked with the oracle (fp64): relative residual
+    ||coef(V) - p||^2 / ||p||^2 <= 1e-8 (reading R2)."""
+    c = si.CONFIGS["c0_n4_2d6"]
+    o = oracle(c.n, c.d)
+    ix = sos.SosIndex(c.n, c.d)
+    plan = sos.SosPlan(ix, c.r)
+    p = o.forward(si.planted_w(o.N, c.r_star, 0)).astype(np.float32)
+    V = torch.from_numpy(si.v0(o.N, c.r, 0)).cuda()
+    pd = torch.from_numpy(p).cuda()
+    plan.opt_init(kind, lr)
+    losses = torch.empty(steps, dtype=torch.float64, device="cuda")
+    for t in range(steps):
+        plan.step(V, pd, losses[t:t + 1])
+    loss_final, _, _, _ = o.loss_grad(V.cpu().numpy(), p, want_grad=False)
+    pn = float(np.dot(p.astype(np.float64), p))
+    assert loss_final / pn <= 1e-8
+    assert losses[-1].item() / pn <= 1e-7
+
+
+def test_solve_host_matches_device_steps(sos):
+    n, d, r = 4, 3, 20
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    p = o.forward(si.planted_w(o.N, 10, 0)).astype(np.float32)
+    V0 = si.v0(o.N, r, 0)
+    plan.opt_init("gd", 0.02)
+    Vh = V0.copy()
+    losses = plan.solve_host(Vh, p, 50)
+    plan.opt_init("gd", 0.02)
+    Vd = torch.from_numpy(V0.copy()).cuda()
+    for _ in range(50):
+        plan.step(Vd, torch.from_numpy(p).cuda())
+    assert rel_l2(Vh, Vd.cpu().numpy()) <= 1e-5
+    assert np.all(np.isfinite(losses)) and losses[-1] < losses[0]
+
+
+# ---------------------------------------------------------------- full size --
+
+@pytest.fixture(scope="module")
+def big(sos):
+    c = si.CONFIGS[si.BENCH_CONFIG]
+    ix = sos.SosIndex(c.n, c.d)
+    plan = sos.SosPlan(ix, c.r)
+    V = si.v0(ix.N, c.r, seed=0)
+    return c, ix, plan, V
+
+
+def test_full_size_index_sampled(sos, big):
+    c, ix, plan, V = big
+    o = oracle(c.n, c.d)
+    np.testing.assert_array_equal(ix.alpha().cpu().numpy(), o.alpha())
+    np.testing.assert_array_equal(ix.beta().cpu().numpy(), o.beta())
+    rows = np.array([0, 1, 777, o.N // 2, o.N - 1], dtype=np.int64)
+    I = np.repeat(rows, o.N)
+    J = np.tile(np.arange(o.N, dtype=np.int64), rows.size)
+    got = ix.pair_ranks(torch.from_numpy(I), torch.from_numpy(J)).cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(got.reshape(rows.size, o.N), o.pair_ranks(rows))
+
+
+def test_full_size_forward_sampled(sos, big):
+    """BASELINE config 4 (5.3M coefficients): sampled coefficients vs the
+    oracle, plus the point-evaluation identity on the whole vector."""
+    c, ix, plan, V = big
+    o = oracle(c.n, c.d)
+    coef = plan.forward(torch.from_numpy(V).cuda()).cpu().numpy().astype(np.float64)
+    rng = np.random.default_rng(0)
+    betas = np.concatenate([np.arange(8), rng.integers(0, o.M, 56), [o.M - 1]])
+    want = o.coef_sample(V, betas)
+    assert rel_l2(coef[betas], want) <= REL_TOL
+    # sum_beta coef_beta x^beta == sum_k (m_d(x) . v_k)^2 at random points
+    B = o.beta().astype(np.float64)
+    A = o.alpha().astype(np.float64)
+    Vd = V.astype(np.float64)
+    for x in si.points(2, c.n, seed=1) * 0.5:
+        lhs = coef @ np.prod(x[None, :] ** B, axis=1)
+        rhs = np.sum((np.prod(x[None, :] ** A, axis=1) @ Vd) ** 2)
+        assert abs(lhs - rhs) <= REL_TOL * abs(rhs)
+
+
+def test_full_size_backward_sampled(sos, big):
+    c, ix, plan, V = big
+    o = oracle(c.n, c.d)
+    res = si.residual_probe(o.M, seed=9)
+    g = plan.backward(torch.from_numpy(V).cuda(), torch.from_numpy(res).cuda())
+    rows = np.array([0, 5, o.N // 3, o.N - 1], dtype=np.int64)
+    got = g[torch.from_numpy(rows).cuda()].cpu().numpy()
+    want = o.grad_rows(V, res, rows)
+    assert rel_l2(got, want) <= REL_TOL

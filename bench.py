@@ -1,0 +1,347 @@
+#!/usr/bin/env python3
+"""Benchmark of the SOS descent step (loss + gradient + optimiser update) on B200.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE
+JSON line on rank 0.  A "step" is one pass of the whole hot path over the
+BASELINE.json config named in config.workload (default: n=17, 2d=10,
+N=20349 monomials, M=5,311,735 coefficients, r=20349 squares, planted target):
+    pack V -> forward Gram tiles + coefficient scatter (tcgen05) -> residual+loss
+    -> pack R -> backward 4RV (tcgen05) -> Adam update.
+Multi-GPU: the path does not shard (BASELINE.json north_star: one GPU, no
+collectives), so N ranks run N independent replicas ("replicas only",
+scaling "weak"); time = max over ranks of the device-timed region.
+
+`--impl reference` times the fp64 CPU oracle (the only reference this paper
+has) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import seeded_inputs as si  # noqa: E402
+
+METRIC = "SOS grad steps/sec and effective TFLOP/s (% tensor roofline) at N monomials, r squares"
+N_PRODUCTS = 3  # fp16 hi/lo split: A_hi B_hi + A_hi B_lo + A_lo B_hi
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default=si.BENCH_CONFIG, choices=sorted(si.CONFIGS))
+    ap.add_argument("--opt", choices=["adam", "gd"], default="adam")
+    ap.add_argument("--lr", type=float, default=1e-4)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def step_flops(N: int, r: int) -> dict:
+    """Algorithmic fp32-equivalent flops of one step."""
+    fwd = N * (N + 1) * r          # N(N+1)/2 Gram entries (upper triangle) x 2r
+    bwd = 2 * N * N * r            # 4 R V: N x N times N x r
+    return {"fwd": fwd, "bwd": bwd, "step": fwd + bwd}
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            pk = json.load(f)
+        return pk, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks --
+REASON_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 5:
+                    continue
+                try:
+                    s, m = float(parts[1]), float(parts[2])
+                    bits = int(parts[4], 16)
+                except ValueError:
+                    continue
+                if bits & 0x1:  # idle sample (before / after the kernels)
+                    continue
+                sm.append(s)
+                smax.append(m)
+                for b, name in REASON_BITS.items():
+                    if bits & b:
+                        reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- cpu oracle --
+def oracle_rows_sample(cfg, V, target_s: float, seed: int):
+    """Time the fp64 oracle's gradient rows (grad_rows, plain C, 1 thread) on
+    config `cfg`; the oracle's full step = forward pair loop (N^2 r MACs) +
+    gradient (N rows of N r MACs) ~ 2 N x (time per gradient row)."""
+    from oracle import OracleIndex
+    o = OracleIndex(cfg.n, cfg.d)
+    res = si.residual_probe(o.M, seed=seed)
+    Vd = np.ascontiguousarray(V, dtype=np.float64)
+    rows_done, t_total = 0, 0.0
+    row = 0
+    while t_total < target_s and rows_done < o.N:
+        t0 = time.perf_counter()
+        o.grad_rows(Vd, res, [row])
+        t_total += time.perf_counter() - t0
+        rows_done += 1
+        row = (row + 7919) % o.N
+    t_row = t_total / rows_done
+    return {"t_row_s": t_row, "rows": rows_done, "t_total_s": t_total, "step_s": 2 * o.N * t_row}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    cfg = si.CONFIGS[args.workload]
+    V = si.v0(cfg.N, cfg.r, seed=args.seed)
+    per_step = []
+    for t in range(args.warmup + args.steps):
+        s = oracle_rows_sample(cfg, V, target_s=3.0, seed=args.seed + t)
+        if t >= args.warmup:
+            per_step.append(s)
+    step_s = float(np.mean([s["step_s"] for s in per_step]))
+    value = 1.0 / step_s
+    rows = sum(s["rows"] for s in per_step)
+    sample = (f"fp64 C oracle (oracle/sos_oracle.c, 1 thread) gradient rows of {args.workload}: "
+              f"{rows} rows over {args.steps} timed samples; step time extrapolated as 2N x row time "
+              f"(forward pair loop and gradient each do N^2 r multiply-adds)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(cfg, args, 1),
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(cfg, args, world):
+    return {
+        "workload": f"{cfg.name}: n={cfg.n}, 2d={2 * cfg.d}, N={cfg.N} monomials, M={cfg.M} coefficients, "
+                    f"r={cfg.r} squares, planted r*={cfg.r_star}",
+        "n": cfg.n, "degree": 2 * cfg.d, "N": cfg.N, "M": cfg.M, "r": cfg.r,
+        "optimizer": args.opt, "lr": args.lr,
+        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+        "l2": "inputs larger than L2 (V 1.66 GB fp32, R split tiles 1.68 GB, pair-rank table 1.68 GB)",
+    }
+
+
+# -------------------------------------------------------------------- ours --
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_19844_b200 as sos
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = si.CONFIGS[args.workload]
+    seed = args.seed + 1000 * rank
+
+    ix = sos.SosIndex(cfg.n, cfg.d)
+    N, M, r = ix.N, ix.M, cfg.r
+    # planted target p = coef(W W^T), computed on the device by the same path
+    W = torch.from_numpy(si.planted_w(N, cfg.r_star, seed=seed)).to(dev)
+    plan_w = sos.SosPlan(ix, cfg.r_star)
+    p = plan_w.forward(W)
+    torch.cuda.synchronize()
+    plan_w.close()
+    del W, plan_w
+    V0 = si.v0(N, r, seed=seed)
+    V = torch.from_numpy(V0).to(dev)
+    plan = sos.SosPlan(ix, r)
+    plan.opt_init(args.opt, args.lr)
+    losses = torch.zeros(args.warmup + args.steps, dtype=torch.float64, device=dev)
+    pnorm2 = float(torch.dot(p.double(), p.double()).item())
+
+    for t in range(args.warmup):
+        plan.step(V, p, losses[t:t + 1])
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    plan.timing(True)
+    l0 = plan.launch_count
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record()
+    for t in range(args.warmup, args.warmup + args.steps):
+        plan.step(V, p, losses[t:t + 1])
+    ev1.record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = plan.launch_count - l0
+    plan.timing(False)
+    kt = plan.timing_read()
+    clk = clocks.stop()
+    if ws > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    loss_hist = losses.cpu().numpy()
+
+    # ---- end to end through the host-buffer C-ABI call (copies inside) ----
+    e2e = None
+    if not args.no_e2e:
+        Vh = torch.from_numpy(V0).pin_memory()
+        ph = p.cpu().pin_memory()
+        plan.opt_init(args.opt, args.lr)
+        Vn, pn = Vh.numpy(), ph.numpy()
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        plan.solve_host(Vn, pn, args.steps)
+        e2e_s = time.perf_counter() - t0
+        if ws > 1:
+            tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        e2e = {"value": ws * args.steps / e2e_s, "unit": "steps/s",
+               "h2d_bytes_per_step": int((N * r * 4 + M * 4) / args.steps),
+               "d2h_bytes_per_step": int((N * r * 4 + args.steps * 8) / args.steps),
+               "api": "sos_solve_host (host V and p, K steps per call, copies inside the timed region)"}
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return 0
+
+    flops = step_flops(N, r)
+    peaks, peak_src = load_peaks()
+    step_s = ms / 1e3 / args.steps
+    value = ws * args.steps / (ms / 1e3)
+    bwd_ms, bwd_n = kt["gemm_bwd"]
+    fwd_ms, fwd_n = kt["gemm_fwd"]
+    total_kernel_ms = sum(v[0] for v in kt.values())
+    peak_tensor = peaks["bf16_tflops_sustained"] / N_PRODUCTS  # fp16 rate == bf16 rate (nominal ratio 1)
+    achieved_bwd = flops["bwd"] / (bwd_ms / bwd_n / 1e3) / 1e12
+    achieved_fwd = flops["fwd"] / (fwd_ms / fwd_n / 1e3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("gemm_bwd_dram_bytes_per_launch")
+    eff_tflops = flops["step"] / step_s / 1e12
+
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        s = oracle_rows_sample(cfg, V0, target_s=12.0, seed=args.seed)
+        cpu = {"value": 1.0 / s["step_s"], "unit": "steps/s", "cores": 1, "kind": "oracle",
+               "sample": f"fp64 C oracle gradient rows of {cfg.name}: {s['rows']} rows in {s['t_total_s']:.1f} s "
+                         f"(1 thread); step time extrapolated as 2N x row time = {s['step_s']:.3g} s"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16x3 split (fp32-class), fp32 accumulate, fp32 state",
+        "data": "synthetic (seeded Gaussian V0 and planted W, BASELINE.json recipe)",
+        "config": config_block(cfg, args, ws),
+        "effective_tflops": eff_tflops,
+        "tensor_roofline_frac_step": eff_tflops / peak_tensor,
+        "roofline": {"bound": "tensor", "kernel": "k_gemm<bwd> (4RV)", "achieved": achieved_bwd,
+                     "peak": peak_tensor, "unit": "TFLOP/s", "frac": achieved_bwd / peak_tensor,
+                     "traffic": traffic,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained {peaks['bf16_tflops_sustained']} / "
+                                    f"{N_PRODUCTS} fp16 products per fp32-equivalent flop",
+                     "flops_per_launch": flops["bwd"]},
+        "kernels": {k: {"ms_per_launch": (v[0] / v[1] if v[1] else None), "launches": v[1],
+                        "share": (v[0] / total_kernel_ms if total_kernel_ms else None)} for k, v in kt.items()},
+        "fwd_gemm_tflops": achieved_fwd,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "loss_rel": {"first": float(loss_hist[0] / pnorm2), "last": float(loss_hist[-1] / pnorm2)},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

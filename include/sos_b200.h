@@ -90,6 +90,24 @@ int sos_plan_destroy(sos_plan *plan);
 /* Number of kernels this library launched through `plan` so far. */
 int64_t sos_plan_launch_count(const sos_plan *plan);
 
+/* Per-kernel device timing of the launches made through `plan`: when enabled,
+ * every kernel is bracketed by CUDA events recorded on its launch stream.
+ * sos_plan_timing(plan, 1) clears previous records and starts recording;
+ * sos_plan_timing(plan, 0) stops.  sos_plan_timing_read synchronises on the
+ * recorded events and returns the summed duration (ms) and launch count of
+ * kernel kind `kernel` (SOS_KERNEL_*). */
+#define SOS_KERNEL_ABSMAX_V 0
+#define SOS_KERNEL_PACK_V 1
+#define SOS_KERNEL_GEMM_FWD 2
+#define SOS_KERNEL_RESIDUAL 3
+#define SOS_KERNEL_ABSMAX_R 4
+#define SOS_KERNEL_PACK_R 5
+#define SOS_KERNEL_GEMM_BWD 6
+#define SOS_KERNEL_UPDATE 7
+#define SOS_KERNEL_COUNT 8
+int sos_plan_timing(sos_plan *plan, int enable);
+int sos_plan_timing_read(sos_plan *plan, int kernel, double *total_ms, int64_t *launches);
+
 /* coef_dev[M] = coefficients of m_d V V^T m_d^T (PAPER.md:45-48 with B = V V^T):
  * coef_beta = sum over ordered pairs (i,j) with alpha_i + alpha_j = beta of
  * <V_i, V_j>.  Computed on tensor cores (fp16 hi/lo split, 3 products, fp32

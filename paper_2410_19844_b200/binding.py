@@ -47,6 +47,8 @@ SIGNATURES = {
     "sos_plan_create": [_vp, _i64, ctypes.POINTER(_vp)],
     "sos_plan_destroy": [_vp],
     "sos_plan_launch_count": [_vp],
+    "sos_plan_timing": [_vp, ctypes.c_int],
+    "sos_plan_timing_read": [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)],
     "sos_forward": [_vp, _vp, _vp, _vp],
     "sos_backward": [_vp, _vp, _vp, _vp, _vp],
     "sos_loss_grad": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
@@ -154,6 +156,21 @@ class SosPlan:
     @property
     def launch_count(self) -> int:
         return int(load().sos_plan_launch_count(self._h))
+
+    KERNELS = ("absmax_v", "pack_v", "gemm_fwd", "residual", "absmax_r", "pack_r", "gemm_bwd", "update")
+
+    def timing(self, enable: bool):
+        """Start (clears old records) / stop per-kernel CUDA-event timing."""
+        _check(load().sos_plan_timing(self._h, 1 if enable else 0))
+
+    def timing_read(self) -> dict:
+        """{kernel name: (total ms, launches)} over the recorded launches."""
+        out = {}
+        for k, name in enumerate(self.KERNELS):
+            ms, cnt = ctypes.c_double(), _i64()
+            _check(load().sos_plan_timing_read(self._h, k, ctypes.byref(ms), ctypes.byref(cnt)))
+            out[name] = (ms.value, cnt.value)
+        return out
 
     def _V(self, V):
         _dev_f32(V, "V")

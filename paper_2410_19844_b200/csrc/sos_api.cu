@@ -215,6 +215,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         sos_plan_destroy(pl);
         return fail(SOS_ERR_CUDA, "tile list upload");
     }
+    P.timing = new Timing();
     P.opt_kind = SOS_OPT_GD;
     P.lr = 0.f;
     P.opt_ready = false;
@@ -236,11 +237,43 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_scal);
     cudaFree(P.d_tiles_fwd);
     cudaFree(P.d_tiles_bwd);
+    if (P.timing) {
+        for (cudaEvent_t e : P.timing->pool) cudaEventDestroy(e);
+        delete P.timing;
+    }
     delete pl;
     return SOS_OK;
 }
 
 int64_t sos_plan_launch_count(const sos_plan* pl) { return pl ? pl->P.launches : -1; }
+
+int sos_plan_timing(sos_plan* pl, int enable) {
+    if (!pl || !pl->P.timing) return fail(SOS_ERR_ARG, "plan is NULL");
+    Timing& T = *pl->P.timing;
+    if (enable) {
+        T.used = 0;
+        T.recs.clear();
+    }
+    T.on = enable != 0;
+    return SOS_OK;
+}
+
+int sos_plan_timing_read(sos_plan* pl, int kernel, double* total_ms, int64_t* launches) {
+    if (!pl || !pl->P.timing || kernel < 0 || kernel >= KK_COUNT) return fail(SOS_ERR_ARG, "bad argument");
+    double sum = 0.0;
+    int64_t cnt = 0;
+    for (const TimingRec& r : pl->P.timing->recs) {
+        if (r.kind != kernel) continue;
+        CK(cudaEventSynchronize(r.b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, r.a, r.b));
+        sum += ms;
+        cnt++;
+    }
+    if (total_ms) *total_ms = sum;
+    if (launches) *launches = cnt;
+    return SOS_OK;
+}
 
 // --------------------------------------------------------------- compute --
 static int do_forward(Plan& P, const float* V, float* coef, cudaStream_t st) {

@@ -14,12 +14,13 @@
 // and the epilogue divides the scales out.  The dropped A_lo B_lo^T term is
 // O(2^-22) relative.
 //
-// Warp roles (192 threads, 1 CTA per SM, persistent over a static tile list):
+// Warp roles (320 threads, 1 CTA per SM, persistent over a static tile list):
 //   warp 0      one lane issues the bulk copies (A 16 KB + B 32 KB per stage)
 //   warp 1      allocates 512 TMEM columns; one lane issues tcgen05.mma
-//   warps 2..5  epilogue: tcgen05.ld 32 columns at a time, scatter / store;
-//               TMEM is double-buffered (2 x 256 columns) so the epilogue of
-//               tile t overlaps the MMAs of tile t+1.
+//   warps 2..9  epilogue: drain each K-segment accumulator (tcgen05.ld) into
+//               fp32 register sums, then scatter / store the finished tile.
+//               TMEM is double-buffered (2 x 256 columns) so draining segment
+//               s overlaps the MMAs of segment s+1.
 #include "sm100_ptx.cuh"
 #include "sos_internal.cuh"
 
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+            mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
         }
         fence_mbar_init();
     }
@@ -97,6 +98,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer --
+        // The K loop of a tile is cut into segments of kSegKB K-blocks; each
+        // segment accumulates into one of the two TMEM buffers from zero and is
+        // drained by the epilogue into fp32 registers (round-to-nearest adds),
+        // bounding the number of in-TMEM accumulations per value.
         if (lane == 0) {
             constexpr uint32_t idesc = umma_idesc_f16_f32(kBlockM, kBlockN);
             int stage = 0;
@@ -104,35 +109,42 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int tile = blockIdx.x; tile < args.ntiles; tile += gridDim.x) {
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                tc_fence_after();
-                const uint32_t d = tbase + acc * kBlockN;
-                for (int kb = 0; kb < args.num_kb; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                for (int kb0 = 0; kb0 < args.num_kb; kb0 += kSegKB) {
+                    const int kb1 = min(args.num_kb, kb0 + kSegKB);
+                    mbar_wait(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(smem + stage * kStageBytes);
-                    const uint32_t b0 = a0 + kTileABytes;
+                    const uint32_t d = tbase + acc * kBlockN;
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(smem + stage * kStageBytes);
+                        const uint32_t b0 = a0 + kTileABytes;
 #pragma unroll
-                    for (int s = 0; s < 2; ++s) {
-                        const uint64_t ah = umma_desc_sw128(a0 + s * 32);
-                        const uint64_t al = umma_desc_sw128(a0 + 64 + s * 32);
-                        const uint64_t bh = umma_desc_sw128(b0 + s * 32);
-                        const uint64_t bl = umma_desc_sw128(b0 + 64 + s * 32);
-                        umma_f16(d, ah, bh, idesc, (kb | s) != 0);
-                        umma_f16(d, ah, bl, idesc, 1u);
-                        umma_f16(d, al, bh, idesc, 1u);
+                        for (int s = 0; s < 2; ++s) {
+                            const uint64_t ah = umma_desc_sw128(a0 + s * 32);
+                            const uint64_t al = umma_desc_sw128(a0 + 64 + s * 32);
+                            const uint64_t bh = umma_desc_sw128(b0 + s * 32);
+                            const uint64_t bl = umma_desc_sw128(b0 + 64 + s * 32);
+                            umma_f16(d, ah, bh, idesc, (kb != kb0 || s != 0) ? 1u : 0u);
+                            umma_f16(d, ah, bl, idesc, 1u);
+                            umma_f16(d, al, bh, idesc, 1u);
+                        }
+                        umma_commit(&empty[stage]);  // smem slot free once these MMAs finish
+                        if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
-                    umma_commit(&empty[stage]);  // smem slot free once these MMAs finish
-                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                    umma_commit(&tfull[acc]);  // segment accumulator ready for the epilogue
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
                 }
-                umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
             }
         }
     } else {
         // -------------------------------------------------------- epilogue --
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        // 8 warps: warp w reads TMEM lane quarter q = w % 4 (rows 32q..32q+31 of
+        // the tile) and column half h (128 columns); each thread keeps its
+        // 128 running sums in registers.
+        const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
         float scale;
         if (kFwd) {
             const float s = args.scal->s_v;
@@ -145,17 +157,33 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
         for (int tile = blockIdx.x; tile < args.ntiles; tile += gridDim.x) {
             const TileCoord tc = args.tiles[tile];
             const int64_t i = (int64_t)tc.a * kBlockM + q * 32 + lane;
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
-            const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + acc * kBlockN;
-            const bool strictly_upper = (int64_t)tc.a * kBlockM + kBlockM - 1 < (int64_t)tc.b * kBlockN;
-#pragma unroll 1
-            for (int ch = 0; ch < kBlockN / 32; ++ch) {
-                uint32_t v[32];
-                tmem_ld32(tq + ch * 32, v);
-                tmem_ld_wait();
-                const int64_t c0 = (int64_t)tc.b * kBlockN + ch * 32;
-                if (kFwd) {
+            float sum[kEpiCols];
+#pragma unroll
+            for (int t = 0; t < kEpiCols; ++t) sum[t] = 0.f;
+            for (int kb0 = 0; kb0 < args.num_kb; kb0 += kSegKB) {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + acc * kBlockN + h * kEpiCols;
+#pragma unroll
+                for (int ch = 0; ch < kEpiCols / 32; ++ch) {
+                    uint32_t v[32];
+                    tmem_ld32(tq + ch * 32, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int t = 0; t < 32; ++t) sum[ch * 32 + t] += __uint_as_float(v[t]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+            const int64_t cbase = (int64_t)tc.b * kBlockN + h * kEpiCols;
+            if (kFwd) {
+                const bool strictly_upper = (int64_t)tc.a * kBlockM + kBlockM - 1 < (int64_t)tc.b * kBlockN;
+#pragma unroll
+                for (int ch = 0; ch < kEpiCols / 32; ++ch) {
+                    const int64_t c0 = cbase + ch * 32;
                     const uint4* prow = reinterpret_cast<const uint4*>(args.pt + (((c0 >> 5) * args.Np + i) << 5));
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
@@ -167,35 +195,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
                             if (rr[e] == kInvalidRank) continue;
                             const int64_t j = c0 + t;
                             const float w = strictly_upper ? 2.f : (i < j ? 2.f : (i == j ? 1.f : 0.f));
-                            if (w != 0.f) red_add_f32(args.coef + rr[e], w * scale * __uint_as_float(v[t]));
-                        }
-                    }
-                } else {
-                    if (i < args.N) {
-                        float* g = args.grad + i * args.r + c0;
-                        if (c0 + 32 <= args.r && ((reinterpret_cast<uintptr_t>(g) & 15) == 0)) {
-#pragma unroll
-                            for (int u = 0; u < 8; ++u) {
-                                float4 o;
-                                o.x = scale * __uint_as_float(v[4 * u + 0]);
-                                o.y = scale * __uint_as_float(v[4 * u + 1]);
-                                o.z = scale * __uint_as_float(v[4 * u + 2]);
-                                o.w = scale * __uint_as_float(v[4 * u + 3]);
-                                reinterpret_cast<float4*>(g)[u] = o;
-                            }
-                        } else {
-#pragma unroll
-                            for (int t = 0; t < 32; ++t)
-                                if (c0 + t < args.r) g[t] = scale * __uint_as_float(v[t]);
+                            if (w != 0.f) red_add_f32(args.coef + rr[e], w * scale * sum[ch * 32 + t]);
                         }
                     }
                 }
+            } else if (i < args.N) {
+#pragma unroll
+                for (int ch = 0; ch < kEpiCols / 32; ++ch) {
+                    const int64_t c0 = cbase + ch * 32;
+                    float* g = args.grad + i * args.r + c0;
+                    if (c0 + 32 <= args.r && ((reinterpret_cast<uintptr_t>(g) & 15) == 0)) {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            float4 o;
+                            o.x = scale * sum[ch * 32 + 4 * u + 0];
+                            o.y = scale * sum[ch * 32 + 4 * u + 1];
+                            o.z = scale * sum[ch * 32 + 4 * u + 2];
+                            o.w = scale * sum[ch * 32 + 4 * u + 3];
+                            reinterpret_cast<float4*>(g)[u] = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 32; ++t)
+                            if (c0 + t < args.r) g[t] = scale * sum[ch * 32 + t];
+                    }
+                }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
         }
     }
 
@@ -234,8 +259,8 @@ void launch_gemm_fwd(Plan& P, float* coef, cudaStream_t st) {
     a.Np = P.idx->Np;
     a.pt = P.idx->d_pt;
     a.coef = coef;
+    LaunchScope ls(P, KK_GEMM_FWD, st);
     launch(P, a, true, st);
-    P.launches++;
 }
 
 void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st) {
@@ -252,8 +277,8 @@ void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st) {
     a.Np = P.idx->Np;
     a.grad = grad;
     a.r = P.r;
+    LaunchScope ls(P, KK_GEMM_BWD, st);
     launch(P, a, false, st);
-    P.launches++;
 }
 
 }  // namespace sos

@@ -17,8 +17,29 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <vector>
 
 namespace sos {
+
+// kernel kinds for per-launch event timing (sos_plan_timing_read)
+enum KernelKind { KK_ABSMAX_V = 0, KK_PACK_V, KK_GEMM_FWD, KK_RESIDUAL, KK_ABSMAX_R, KK_PACK_R, KK_GEMM_BWD,
+                  KK_UPDATE, KK_COUNT };
+
+struct TimingRec { int kind; cudaEvent_t a, b; };
+struct Timing {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<TimingRec> recs;
+    cudaEvent_t get() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+};
 
 constexpr int kBlockM = 128;   // tile rows  (UMMA M)
 constexpr int kBlockN = 256;   // tile cols  (UMMA N)
@@ -28,7 +49,13 @@ constexpr int kStages = 4;
 constexpr uint32_t kTileABytes = kBlockM * 128;  // 16 KB
 constexpr uint32_t kTileBBytes = kBlockN * 128;  // 32 KB
 constexpr uint32_t kStageBytes = kTileABytes + kTileBBytes;
-constexpr int kGemmThreads = 192;  // warp0 producer, warp1 MMA, warps2-5 epilogue
+constexpr int kEpiWarps = 8;       // 4 TMEM lane quarters x 2 column halves
+constexpr int kEpiCols = kBlockN / 2;
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // warp0 producer, warp1 MMA, warps 2..9 epilogue
+// K-blocks accumulated in TMEM before the epilogue drains them into fp32
+// registers: tcgen05 fp32 accumulation truncates, so the number of in-TMEM
+// adds per value is bounded.
+constexpr int kSegKB = 16;
 constexpr uint32_t kInvalidRank = 0xFFFFFFFFu;
 constexpr int kMaxVars = 64;       // n + 2d <= 64
 constexpr int kMaxDeg2 = 64;
@@ -71,6 +98,30 @@ struct Plan {
     int opt_kind; float lr, b1, b2, eps; int64_t t; bool opt_ready;
     int64_t launches;
     int num_sms;
+    Timing* timing;
+};
+
+// counts every kernel launch of a plan and, when timing is on, brackets it
+// with CUDA events recorded on the launch stream
+struct LaunchScope {
+    Plan& P;
+    int kind;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    LaunchScope(Plan& p, int k, cudaStream_t s) : P(p), kind(k), st(s) {
+        if (P.timing && P.timing->on) {
+            a = P.timing->get();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~LaunchScope() {
+        P.launches++;
+        if (a) {
+            cudaEvent_t b = P.timing->get();
+            cudaEventRecord(b, st);
+            P.timing->recs.push_back(TimingRec{kind, a, b});
+        }
+    }
 };
 
 // ---- kernels (defined in the .cu files) ----

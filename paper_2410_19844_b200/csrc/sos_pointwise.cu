@@ -244,34 +244,35 @@ static int grid_for(const Plan& P, int64_t work, int threads, int per_sm = 8) {
 
 void launch_absmax_v(Plan& P, const float* V, cudaStream_t st) {
     const int64_t len = P.idx->N * P.r;
+    LaunchScope ls(P, KK_ABSMAX_V, st);
     k_absmax<<<grid_for(P, len / 4, 256), 256, 0, st>>>(V, len, &P.d_scal->absmax_v);
-    P.launches++;
 }
 
 void launch_absmax_res(Plan& P, const float* res, cudaStream_t st) {
+    LaunchScope ls(P, KK_ABSMAX_R, st);
     k_absmax<<<grid_for(P, P.idx->M / 4, 256), 256, 0, st>>>(res, P.idx->M, &P.d_scal->absmax_r);
-    P.launches++;
 }
 
 void launch_pack_v(Plan& P, const float* V, cudaStream_t st) {
     dim3 grid((unsigned)(P.rN / 64), (unsigned)(P.idx->Np / 32));
+    LaunchScope ls(P, KK_PACK_V, st);
     k_pack_v<<<grid, 256, 0, st>>>(V, P.idx->N, P.r, P.idx->Np, P.rK, P.rN, P.d_scal, P.d_vs, P.d_vts);
-    P.launches++;
 }
 
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st) {
+    LaunchScope ls(P, KK_RESIDUAL, st);
     k_residual<<<grid_for(P, P.idx->M, 256, 4), 256, 0, st>>>(coef, p, res, P.idx->M, P.d_scal);
-    P.launches++;
 }
 
 void launch_pack_r(Plan& P, const float* res, cudaStream_t st) {
     const int64_t rows8 = P.idx->Np * P.idx->Np / 8;
+    LaunchScope ls(P, KK_PACK_R, st);
     k_pack_r<<<grid_for(P, rows8, 256), 256, 0, st>>>(P.idx->d_pt, res, rows8, P.d_scal, P.d_rs);
-    P.launches++;
 }
 
 void launch_update(Plan& P, float* V, const float* grad, cudaStream_t st) {
     const int64_t len = P.idx->N * P.r;
+    LaunchScope ls(P, KK_UPDATE, st);
     if (P.opt_kind == 0) {
         k_update_gd<<<grid_for(P, len / 4, 256), 256, 0, st>>>(V, grad, len, P.lr);
     } else {
@@ -280,7 +281,6 @@ void launch_update(Plan& P, float* V, const float* grad, cudaStream_t st) {
         k_update_adam<<<grid_for(P, len / 4, 256), 256, 0, st>>>(V, grad, P.d_m, P.d_v, len, (float)(P.lr / c1),
                                                                 (float)(1.0 / sqrt(c2)), P.b1, P.b2, P.eps);
     }
-    P.launches++;
 }
 
 }  // namespace sos

@@ -109,6 +109,26 @@ def test_loss_grad_parity_planted(sos, n, d, r):
     assert rel_l2(g.cpu().numpy(), g_o) <= REL_TOL
 
 
+@pytest.mark.parametrize("r", [20349, 40000])
+def test_forward_long_k_nonnegative(sos, r):
+    """Worst case for fp32 accumulation: every product V_ik V_jk >= 0, so every
+    partial sum grows monotonically over a long K (r up to 40000)."""
+    n, d = 6, 3
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    V = np.abs(si.v0(o.N, r, seed=11))
+    coef = plan.forward(torch.from_numpy(V).cuda()).cpu().numpy()
+    err = rel_l2(coef, o.forward(V))
+    print(f"long-K nonnegative forward rel err {err:.2e}")
+    assert err <= REL_TOL
+    res = si.residual_probe(o.M, seed=1)
+    g = plan.backward(torch.from_numpy(V).cuda(), torch.from_numpy(np.abs(res)).cuda()).cpu().numpy()
+    err = rel_l2(g, o.grad_rows(V, np.abs(res), np.arange(o.N)))
+    print(f"long-K nonnegative backward rel err {err:.2e}")
+    assert err <= REL_TOL
+
+
 def test_forward_parity_config2(sos):
     """BASELINE config 2 (n=10, 2d=10, N=2002, r=2002): full coefficient vector."""
     c = si.CONFIGS["c2_n10_2d10"]
@@ -210,7 +230,9 @@ def test_full_size_forward_sampled(sos, big):
     rng = np.random.default_rng(0)
     betas = np.concatenate([np.arange(8), rng.integers(0, o.M, 56), [o.M - 1]])
     want = o.coef_sample(V, betas)
-    assert rel_l2(coef[betas], want) <= REL_TOL
+    err = rel_l2(coef[betas], want)
+    print(f"full-size forward sampled rel err {err:.2e}")
+    assert err <= REL_TOL
     # sum_beta coef_beta x^beta == sum_k (m_d(x) . v_k)^2 at random points
     B = o.beta().astype(np.float64)
     A = o.alpha().astype(np.float64)
@@ -221,12 +243,19 @@ def test_full_size_forward_sampled(sos, big):
         assert abs(lhs - rhs) <= REL_TOL * abs(rhs)
 
 
-def test_full_size_backward_sampled(sos, big):
+@pytest.mark.parametrize("nonneg", [False, True])
+def test_full_size_backward_sampled(sos, big, nonneg):
+    """Config 4 backward (K = N = 20349): sampled rows of 4RV vs the oracle;
+    nonneg=True makes every product R_ij V_jk >= 0 (monotone partial sums)."""
     c, ix, plan, V = big
     o = oracle(c.n, c.d)
     res = si.residual_probe(o.M, seed=9)
+    if nonneg:
+        res, V = np.abs(res), np.abs(V)
     g = plan.backward(torch.from_numpy(V).cuda(), torch.from_numpy(res).cuda())
     rows = np.array([0, 5, o.N // 3, o.N - 1], dtype=np.int64)
     got = g[torch.from_numpy(rows).cuda()].cpu().numpy()
     want = o.grad_rows(V, res, rows)
-    assert rel_l2(got, want) <= REL_TOL
+    err = rel_l2(got, want)
+    print(f"full-size backward (nonneg={nonneg}) sampled rel err {err:.2e}")
+    assert err <= REL_TOL

@@ -205,7 +205,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     if ((rc = dalloc(&P.d_vs, (size_t)(P.rK / 32) * Np * 128)) || (rc = dalloc(&P.d_vts, (size_t)(Np / 32) * P.rN * 128)) ||
         (rc = dalloc(&P.d_rs, (size_t)(Np / 32) * Np * 128)) || (rc = dalloc(&P.d_coef, (size_t)M * 4)) ||
         (rc = dalloc(&P.d_res, (size_t)M * 4)) || (rc = dalloc(&P.d_grad, (size_t)N * r * 4)) ||
-        (rc = dalloc(&P.d_scal, sizeof(Scalars))) || (rc = dalloc(&P.d_tiles_fwd, tf.size() * sizeof(TileCoord))) ||
+        (rc = dalloc(&P.d_scal, sizeof(Scalars))) || (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) || (rc = dalloc(&P.d_tiles_fwd, tf.size() * sizeof(TileCoord))) ||
         (rc = dalloc(&P.d_tiles_bwd, tb.size() * sizeof(TileCoord)))) {
         sos_plan_destroy(pl);
         return rc;
@@ -235,6 +235,7 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_m);
     cudaFree(P.d_v);
     cudaFree(P.d_scal);
+    cudaFree(P.d_progress);
     cudaFree(P.d_tiles_fwd);
     cudaFree(P.d_tiles_bwd);
     if (P.timing) {

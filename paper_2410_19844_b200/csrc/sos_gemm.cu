@@ -41,6 +41,7 @@ struct GemmArgs {
     float* coef;         // forward: output coefficients
     float* grad;         // backward: output N x r
     int64_t r;           // backward: columns of grad
+    unsigned long long* progress;  // K-skew counter (zeroed before the launch)
 };
 
 constexpr uint32_t kSmemBytes = kStages * kStageBytes + 256 + 1024;
@@ -80,13 +81,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
     if (warp == 0) {
         // ------------------------------------------------------- producer --
         if (lane == 0) {
+            // Bounded K-skew: every kSkewEpoch K-blocks the producer publishes its
+            // progress and does not run more than kSkewLag epochs ahead of the grid,
+            // so the CTAs of a wave stream the same K-slabs of their shared panels
+            // through L2 instead of whole panels (cooperative launch: all resident).
             int stage = 0;
             uint32_t phase = 0;
+            int64_t g = 0;  // K-blocks issued by this CTA
+            const unsigned long long G = gridDim.x;
             for (int tile = blockIdx.x; tile < args.ntiles; tile += gridDim.x) {
                 const TileCoord tc = args.tiles[tile];
                 const uint8_t* srcA = args.A + (int64_t)tc.a * kBlockM * 128;
                 const uint8_t* srcB = args.B + (int64_t)tc.b * kBlockN * 128;
-                for (int kb = 0; kb < args.num_kb; ++kb) {
+                for (int kb = 0; kb < args.num_kb; ++kb, ++g) {
+                    if (g % kSkewEpoch == 0 && g > 0) {
+                        const int64_t e = g / kSkewEpoch;  // epochs completed by this CTA
+                        atomicAdd(args.progress, 1ull);
+                        if (e >= kSkewLag) {
+                            const unsigned long long need = G * (unsigned long long)(e - kSkewLag + 1);
+                            while (ld_acquire_u64(args.progress) < need) __nanosleep(256);
+                        }
+                    }
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * kStageBytes;
                     mbar_arrive_expect_tx(&full[stage], kStageBytes);
@@ -95,6 +110,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
+            atomicAdd(args.progress, 1ull << 32);  // done: never hold back the others
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer --
@@ -241,8 +257,19 @@ static void launch(const Plan& P, const GemmArgs& a, bool fwd, cudaStream_t st) 
     }
     const int grid = a.ntiles < P.num_sms ? a.ntiles : P.num_sms;
     if (grid <= 0) return;
-    if (fwd) k_gemm<true><<<grid, kGemmThreads, kSmemBytes, st>>>(a);
-    else k_gemm<false><<<grid, kGemmThreads, kSmemBytes, st>>>(a);
+    cudaMemsetAsync(a.progress, 0, sizeof(unsigned long long), st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (skew waits)
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (fwd) cudaLaunchKernelEx(&cfg, k_gemm<true>, a);
+    else cudaLaunchKernelEx(&cfg, k_gemm<false>, a);
 }
 
 void launch_gemm_fwd(Plan& P, float* coef, cudaStream_t st) {
@@ -259,6 +286,7 @@ void launch_gemm_fwd(Plan& P, float* coef, cudaStream_t st) {
     a.Np = P.idx->Np;
     a.pt = P.idx->d_pt;
     a.coef = coef;
+    a.progress = P.d_progress;
     LaunchScope ls(P, KK_GEMM_FWD, st);
     launch(P, a, true, st);
 }
@@ -277,6 +305,7 @@ void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st) {
     a.Np = P.idx->Np;
     a.grad = grad;
     a.r = P.r;
+    a.progress = P.d_progress + 1;
     LaunchScope ls(P, KK_GEMM_BWD, st);
     launch(P, a, false, st);
 }

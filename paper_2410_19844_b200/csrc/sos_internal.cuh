@@ -56,6 +56,9 @@ constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // warp0 producer, warp1 MMA,
 // registers: tcgen05 fp32 accumulation truncates, so the number of in-TMEM
 // adds per value is bounded.
 constexpr int kSegKB = 16;
+// bounded K-skew between the CTAs of a GEMM (see the producer in sos_gemm.cu)
+constexpr int kSkewEpoch = 16;  // K-blocks per progress epoch
+constexpr int kSkewLag = 2;     // epochs a CTA may run ahead of the slowest
 constexpr uint32_t kInvalidRank = 0xFFFFFFFFu;
 constexpr int kMaxVars = 64;       // n + 2d <= 64
 constexpr int kMaxDeg2 = 64;
@@ -93,6 +96,7 @@ struct Plan {
     float* d_m;       // Adam moments (lazy)
     float* d_v;
     Scalars* d_scal;
+    unsigned long long* d_progress;  // [2] K-skew counters (fwd, bwd)
     TileCoord* d_tiles_fwd; int ntiles_fwd;
     TileCoord* d_tiles_bwd; int ntiles_bwd;
     int opt_kind; float lr, b1, b2, eps; int64_t t; bool opt_ready;

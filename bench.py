@@ -59,6 +59,16 @@ def dist_env():
     return ws, rank, local
 
 
+def max_over_ranks(x: float, dist, device) -> float:
+    """Max of a per-rank scalar over all ranks (timing rule: max over ranks)."""
+    import torch
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def step_flops(N: int, r: int) -> dict:
     """Algorithmic fp32-equivalent flops of one step."""
     fwd = N * (N + 1) * r          # N(N+1)/2 Gram entries (upper triangle) x 2r
@@ -132,12 +142,13 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- cpu oracle --
-def oracle_rows_sample(cfg, V, target_s: float, seed: int):
+def oracle_rows_sample(cfg, V, target_s: float, seed: int, o=None):
     """Time the fp64 oracle's gradient rows (grad_rows, plain C, 1 thread) on
     config `cfg`; the oracle's full step = forward pair loop (N^2 r MACs) +
     gradient (N rows of N r MACs) ~ 2 N x (time per gradient row)."""
-    from oracle import OracleIndex
-    o = OracleIndex(cfg.n, cfg.d)
+    if o is None:
+        from oracle import OracleIndex
+        o = OracleIndex(cfg.n, cfg.d)
     res = si.residual_probe(o.M, seed=seed)
     Vd = np.ascontiguousarray(V, dtype=np.float64)
     rows_done, t_total = 0, 0.0
@@ -156,11 +167,13 @@ def run_reference(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return 0
+    from oracle import OracleIndex
     cfg = si.CONFIGS[args.workload]
-    V = si.v0(cfg.N, cfg.r, seed=args.seed)
+    o = OracleIndex(cfg.n, cfg.d)
+    V = np.ascontiguousarray(si.v0(cfg.N, cfg.r, seed=args.seed), dtype=np.float64)
     per_step = []
     for t in range(args.warmup + args.steps):
-        s = oracle_rows_sample(cfg, V, target_s=3.0, seed=args.seed + t)
+        s = oracle_rows_sample(cfg, V, target_s=3.0, seed=args.seed + t, o=o)
         if t >= args.warmup:
             per_step.append(s)
     step_s = float(np.mean([s["step_s"] for s in per_step]))
@@ -250,10 +263,7 @@ def run_ours(args):
     plan.timing(False)
     kt = plan.timing_read()
     clk = clocks.stop()
-    if ws > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(ms, dist, dev)
     loss_hist = losses.cpu().numpy()
 
     # ---- end to end through the host-buffer C-ABI call (copies inside) ----
@@ -269,10 +279,7 @@ def run_ours(args):
         t0 = time.perf_counter()
         plan.solve_host(Vn, pn, args.steps)
         e2e_s = time.perf_counter() - t0
-        if ws > 1:
-            tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
+        e2e_s = max_over_ranks(e2e_s, dist, dev)
         e2e = {"value": ws * args.steps / e2e_s, "unit": "steps/s",
                "h2d_bytes_per_step": int((N * r * 4 + M * 4) / args.steps),
                "d2h_bytes_per_step": int((N * r * 4 + args.steps * 8) / args.steps),

@@ -85,6 +85,22 @@ def residual_probe(M: int, seed: int = 0) -> np.ndarray:
     return _rng(seed, STREAM_PROBE).standard_normal(M, dtype=np.float32)
 
 
+def sphere_power_coefficients(beta: np.ndarray, d: int) -> np.ndarray:
+    """Coefficients of (x_1^2 + ... + x_n^2)^d on the degree-2d basis whose
+    exponent table is `beta` (M x n, any order): the multinomial d!/prod(g_v!)
+    on beta = 2g, zero elsewhere.  BASELINE.json config 3 adds eps times this
+    form to the planted target for strict positivity.  Pure target
+    construction (multinomial theorem); no Gram or ranking arithmetic."""
+    beta = np.asarray(beta, dtype=np.int64)
+    even = np.all(beta % 2 == 0, axis=1)
+    g = beta // 2
+    lf = np.array([math.lgamma(k + 1) for k in range(d + 1)])
+    out = np.zeros(beta.shape[0], dtype=np.float64)
+    ge = g[even]
+    out[even] = np.rint(np.exp(lf[d] - lf[ge].sum(axis=1)))
+    return out
+
+
 def points(count: int, n: int, seed: int = 0) -> np.ndarray:
     """Random evaluation points x in R^n (float64, N(0,1))."""
     return _rng(seed, STREAM_POINTS).standard_normal((count, n))

@@ -200,13 +200,16 @@ def test_solve_host_matches_device_steps(sos):
 
 # ---------------------------------------------------------------- full size --
 
-@pytest.fixture(scope="module")
-def big(sos):
-    c = si.CONFIGS[si.BENCH_CONFIG]
+@pytest.fixture(scope="module", params=["c3_n12_2d12", si.BENCH_CONFIG])
+def big(sos, request):
+    """BASELINE configs 3 (1.35M coefficients) and 4 (5.3M coefficients)."""
+    c = si.CONFIGS[request.param]
     ix = sos.SosIndex(c.n, c.d)
     plan = sos.SosPlan(ix, c.r)
     V = si.v0(ix.N, c.r, seed=0)
-    return c, ix, plan, V
+    yield c, ix, plan, V
+    plan.close()
+    ix.close()
 
 
 def test_full_size_index_sampled(sos, big):
@@ -222,8 +225,8 @@ def test_full_size_index_sampled(sos, big):
 
 
 def test_full_size_forward_sampled(sos, big):
-    """BASELINE config 4 (5.3M coefficients): sampled coefficients vs the
-    oracle, plus the point-evaluation identity on the whole vector."""
+    """Sampled coefficients vs the oracle, plus the point-evaluation identity
+    sum_beta coef_beta x^beta = sum_k (m_d(x) . v_k)^2 on the whole vector."""
     c, ix, plan, V = big
     o = oracle(c.n, c.d)
     coef = plan.forward(torch.from_numpy(V).cuda()).cpu().numpy().astype(np.float64)
@@ -231,9 +234,8 @@ def test_full_size_forward_sampled(sos, big):
     betas = np.concatenate([np.arange(8), rng.integers(0, o.M, 56), [o.M - 1]])
     want = o.coef_sample(V, betas)
     err = rel_l2(coef[betas], want)
-    print(f"full-size forward sampled rel err {err:.2e}")
+    print(f"{c.name} forward sampled rel err {err:.2e}")
     assert err <= REL_TOL
-    # sum_beta coef_beta x^beta == sum_k (m_d(x) . v_k)^2 at random points
     B = o.beta().astype(np.float64)
     A = o.alpha().astype(np.float64)
     Vd = V.astype(np.float64)
@@ -245,7 +247,7 @@ def test_full_size_forward_sampled(sos, big):
 
 @pytest.mark.parametrize("nonneg", [False, True])
 def test_full_size_backward_sampled(sos, big, nonneg):
-    """Config 4 backward (K = N = 20349): sampled rows of 4RV vs the oracle;
+    """Backward at full size (K = N): sampled rows of 4RV vs the oracle;
     nonneg=True makes every product R_ij V_jk >= 0 (monotone partial sums)."""
     c, ix, plan, V = big
     o = oracle(c.n, c.d)
@@ -257,5 +259,57 @@ def test_full_size_backward_sampled(sos, big, nonneg):
     got = g[torch.from_numpy(rows).cuda()].cpu().numpy()
     want = o.grad_rows(V, res, rows)
     err = rel_l2(got, want)
-    print(f"full-size backward (nonneg={nonneg}) sampled rel err {err:.2e}")
+    print(f"{c.name} backward (nonneg={nonneg}) sampled rel err {err:.2e}")
     assert err <= REL_TOL
+
+
+def test_config3_target_with_eps_term(sos):
+    """Config 3's target p = coef(W W^T) + eps (sum x_i^2)^6: the eps term is
+    added on the exponent table the index exports; check it on sampled
+    coefficients against the oracle (eps = 1e-3)."""
+    c = si.CONFIGS["c3_n12_2d12"]
+    o = oracle(c.n, c.d)
+    ix = sos.SosIndex(c.n, c.d)
+    plan_w = sos.SosPlan(ix, c.r_star)
+    W = si.planted_w(o.N, c.r_star, seed=0)
+    sphere = si.sphere_power_coefficients(ix.beta().cpu().numpy(), c.d)
+    p = plan_w.forward(torch.from_numpy(W).cuda()).cpu().numpy().astype(np.float64) + c.eps * sphere
+    betas = np.concatenate([np.arange(6), np.random.default_rng(1).integers(0, o.M, 40)])
+    want = o.coef_sample(W, betas) + c.eps * si.sphere_power_coefficients(o.beta()[betas], c.d)
+    assert rel_l2(p[betas], want) <= REL_TOL
+
+
+def test_forward_parity_config2b_r4004(sos):
+    """BASELINE config 2, over-parameterised r = 4004: sampled coefficients and rows."""
+    c = si.CONFIGS["c2b_n10_2d10_r4004"]
+    o = oracle(c.n, c.d)
+    ix = sos.SosIndex(c.n, c.d)
+    plan = sos.SosPlan(ix, c.r)
+    V = si.v0(o.N, c.r, seed=3)
+    coef = plan.forward(torch.from_numpy(V).cuda()).cpu().numpy()
+    betas = np.arange(0, o.M, 97)
+    assert rel_l2(coef[betas], o.coef_sample(V, betas)) <= REL_TOL
+    res = si.residual_probe(o.M, seed=4)
+    g = plan.backward(torch.from_numpy(V).cuda(), torch.from_numpy(res).cuda()).cpu().numpy()
+    rows = np.array([0, 1000, o.N - 1])
+    assert rel_l2(g[rows], o.grad_rows(V, res, rows)) <= REL_TOL
+
+
+def test_descent_config1_planted(sos):
+    """BASELINE config 1 (n=8, 2d=8, N=330, r=330, planted r*=165): GD on the
+    GPU reaches relative residual <= 1e-8 (checked in fp64 by the oracle)."""
+    c = si.CONFIGS["c1_n8_2d8"]
+    o = oracle(c.n, c.d)
+    ix = sos.SosIndex(c.n, c.d)
+    plan = sos.SosPlan(ix, c.r)
+    p = o.forward(si.planted_w(o.N, c.r_star, 0)).astype(np.float32)
+    V = torch.from_numpy(si.v0(o.N, c.r, 0)).cuda()
+    pd = torch.from_numpy(p).cuda()
+    plan.opt_init("gd", 0.01)
+    loss = torch.empty(1, dtype=torch.float64, device="cuda")
+    for t in range(4000):
+        plan.step(V, pd, loss)
+    pn = float(np.dot(p.astype(np.float64), p))
+    loss_final, _, _, _ = o.loss_grad(V.cpu().numpy(), p, want_grad=False)
+    print(f"config1 descent: gpu {loss.item() / pn:.3e} oracle {loss_final / pn:.3e}")
+    assert loss_final / pn <= 1e-8

@@ -251,3 +251,16 @@ def test_descent_config0_reaches_1e8():
     pn = float(p @ p)
     assert L[-1] / pn <= 1e-8
     assert math.sqrt(L[-1] / pn) <= 1e-8
+
+
+def test_sphere_power_target_term():
+    """The eps-term generator of BASELINE config 3: (x1^2+x2^2)^2 has
+    coefficients (1, 0, 2, 0, 1) on (x1^4, x1^3x2, ..., x2^4), and in general
+    the generated coefficients evaluate to |x|^(2d) at random points."""
+    h = OracleIndex(2, 2)
+    np.testing.assert_array_equal(si.sphere_power_coefficients(h.beta(), 2), [1, 0, 2, 0, 1])
+    h = OracleIndex(4, 3)
+    c = si.sphere_power_coefficients(h.beta(), 3)
+    B = h.beta().astype(np.float64)
+    for x in si.points(5, 4, seed=2):
+        assert abs(c @ np.prod(x[None, :] ** B, axis=1) - np.sum(x ** 2) ** 3) < 1e-9 * np.sum(x ** 2) ** 3

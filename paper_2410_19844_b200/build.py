@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsos_b200.so")
-SOURCES = ["sos_api.cu", "sos_index.cu", "sos_pointwise.cu", "sos_gemm.cu"]
+SOURCES = ["sos_api.cu", "sos_index.cu", "sos_pointwise.cu", "sos_gemm2.cu"]
 HEADERS = ["sm100_ptx.cuh", "sos_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -169,15 +170,15 @@ int sos_index_pair_ranks(const sos_index* h, const int64_t* i_dev, const int64_t
 }
 
 // ------------------------------------------------------------------- plan --
-static void build_tiles(int64_t Np, int64_t ncols_blocks, bool upper, std::vector<TileCoord>& out) {
-    // grouped raster: 16 consecutive 128-row blocks share the B panels of a wave
-    const int64_t na = Np / kBlockM;
-    const int64_t GA = 16;
+// CTA-pair tiles: a = 256-row block, b = 256-col block, same grouped raster
+static void build_tiles2(int64_t Np, int64_t ncols_blocks, bool upper, std::vector<TileCoord>& out) {
+    const int64_t na = Np / 256;
+    const int64_t GA = 8;
     for (int64_t g0 = 0; g0 < na; g0 += GA) {
         const int64_t g1 = std::min(na, g0 + GA);
         for (int64_t b = 0; b < ncols_blocks; ++b)
             for (int64_t a = g0; a < g1; ++a) {
-                if (upper && b * kBlockN + kBlockN - 1 < a * kBlockM) continue;  // entirely below diagonal
+                if (upper && b < a) continue;
                 out.push_back(TileCoord{(int)a, (int)b});
             }
     }
@@ -197,23 +198,30 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     P.rN = ((r + kBlockN - 1) / kBlockN) * kBlockN;
     P.num_sms = sms;
     const int64_t Np = h->ix.Np, N = h->ix.N, M = h->ix.M;
-    std::vector<TileCoord> tf, tb;
-    build_tiles(Np, Np / kBlockN, true, tf);
-    build_tiles(Np, P.rN / kBlockN, false, tb);
-    P.ntiles_fwd = (int)tf.size();
-    P.ntiles_bwd = (int)tb.size();
+    std::vector<TileCoord> tf2, tb2;
+    build_tiles2(Np, Np / kBlockN, true, tf2);
+    build_tiles2(Np, P.rN / kBlockN, false, tb2);
+    P.ntiles2_fwd = (int)tf2.size();
+    P.ntiles2_bwd = (int)tb2.size();
+
     if ((rc = dalloc(&P.d_vs, (size_t)(P.rK / 32) * Np * 128)) || (rc = dalloc(&P.d_vts, (size_t)(Np / 32) * P.rN * 128)) ||
         (rc = dalloc(&P.d_rs, (size_t)(Np / 32) * Np * 128)) || (rc = dalloc(&P.d_coef, (size_t)M * 4)) ||
         (rc = dalloc(&P.d_res, (size_t)M * 4)) || (rc = dalloc(&P.d_grad, (size_t)N * r * 4)) ||
-        (rc = dalloc(&P.d_scal, sizeof(Scalars))) || (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) || (rc = dalloc(&P.d_tiles_fwd, tf.size() * sizeof(TileCoord))) ||
-        (rc = dalloc(&P.d_tiles_bwd, tb.size() * sizeof(TileCoord)))) {
+        (rc = dalloc(&P.d_scal, sizeof(Scalars))) || (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) ||
+        (rc = dalloc(&P.d_tiles2_fwd, tf2.size() * sizeof(TileCoord))) ||
+        (rc = dalloc(&P.d_tiles2_bwd, tb2.size() * sizeof(TileCoord)))) {
         sos_plan_destroy(pl);
         return rc;
     }
-    if (cudaMemcpy(P.d_tiles_fwd, tf.data(), tf.size() * sizeof(TileCoord), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(P.d_tiles_bwd, tb.data(), tb.size() * sizeof(TileCoord), cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (cudaMemcpy(P.d_tiles2_fwd, tf2.data(), tf2.size() * sizeof(TileCoord), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(P.d_tiles2_bwd, tb2.data(), tb2.size() * sizeof(TileCoord), cudaMemcpyHostToDevice) != cudaSuccess) {
         sos_plan_destroy(pl);
         return fail(SOS_ERR_CUDA, "tile list upload");
+    }
+    if (!make_split_tmap(P.tmap_vs, P.d_vs, Np, P.rK / 32) || !make_split_tmap(P.tmap_vts, P.d_vts, P.rN, Np / 32) ||
+        !make_split_tmap(P.tmap_rs, P.d_rs, Np, Np / 32)) {
+        sos_plan_destroy(pl);
+        return fail(SOS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     }
     P.timing = new Timing();
     P.opt_kind = SOS_OPT_GD;
@@ -236,8 +244,8 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_v);
     cudaFree(P.d_scal);
     cudaFree(P.d_progress);
-    cudaFree(P.d_tiles_fwd);
-    cudaFree(P.d_tiles_bwd);
+    cudaFree(P.d_tiles2_fwd);
+    cudaFree(P.d_tiles2_bwd);
     if (P.timing) {
         for (cudaEvent_t e : P.timing->pool) cudaEventDestroy(e);
         delete P.timing;
@@ -282,7 +290,7 @@ static int do_forward(Plan& P, const float* V, float* coef, cudaStream_t st) {
     CK(cudaMemsetAsync(coef, 0, (size_t)P.idx->M * 4, st));
     launch_absmax_v(P, V, st);
     launch_pack_v(P, V, st);
-    launch_gemm_fwd(P, coef, st);
+    launch_gemm2_fwd(P, coef, st);
     return check_launch("forward");
 }
 
@@ -300,7 +308,7 @@ int sos_backward(sos_plan* pl, const float* V_dev, const float* res_dev, float* 
     launch_pack_v(P, V_dev, st);
     launch_absmax_res(P, res_dev, st);
     launch_pack_r(P, res_dev, st);
-    launch_gemm_bwd(P, grad_dev, st);
+    launch_gemm2_bwd(P, grad_dev, st);
     return check_launch("backward");
 }
 
@@ -312,7 +320,7 @@ static int do_loss_grad(Plan& P, const float* V, const float* p, double* loss, f
     launch_residual(P, P.d_coef, p, r, st);
     if (grad) {
         launch_pack_r(P, r, st);
-        launch_gemm_bwd(P, grad, st);
+        launch_gemm2_bwd(P, grad, st);
     }
     if (loss) CK(cudaMemcpyAsync(loss, &P.d_scal->loss, sizeof(double), cudaMemcpyDeviceToDevice, st));
     return check_launch("loss_grad");

@@ -1,7 +1,7 @@
-// sos_gemm.cu -- the two tensor-core kernels of the step (tcgen05 + TMEM,
-// operands fed by the bulk-copy engine through an mbarrier ring).
+// sos_gemm2.cu -- the two tensor-core kernels of the step on CTA PAIRS
+// (tcgen05 cta_group::2, UMMA M = 256 split over the two SMs of a cluster).
 //
-//   forward:  G = V V^T on upper-triangular 128x256
+//   forward:  G = V V^T on upper-triangular 256x256
 //            tiles; the epilogue reduces every G_ij straight into
 //            coef[rank(alpha_i + alpha_j)] (weight 2 off the diagonal, 1 on it),
 //            so the N x N Gram matrix never reaches HBM.
@@ -14,141 +14,157 @@
 // and the epilogue divides the scales out.  The dropped A_lo B_lo^T term is
 // O(2^-22) relative.
 //
-// Warp roles (320 threads, 1 CTA per SM, persistent over a static tile list):
-//   warp 0      one lane issues the bulk copies (A 16 KB + B 32 KB per stage)
-//   warp 1      allocates 512 TMEM columns; one lane issues tcgen05.mma
+// A cluster of 2 CTAs owns one 256x256 output tile: CTA rank c holds rows
+// [128c, 128c+128) of the A tile and of the B tile in its shared memory (16 KB
+// each per 32-wide K-block), the leader (rank 0) issues tcgen05.mma.cta_group::2
+// and each CTA's TMEM receives its 128 output rows x 256 columns.  Per SM this
+// halves the B operand traffic (smem fill, L2 reads, smem reads by the tensor
+// core) against one CTA per 128x256 tile.
+//
+// Warp roles (320 threads per CTA, 1 CTA per SM, persistent over a static tile list):
+//   warp 0      one lane issues 2-SM TMA loads (A 16 KB + B 16 KB per stage),
+//               completion counted on the leader's full barrier
+//   warp 1      allocates 512 TMEM columns (pair-wide); the leader's lane 0 issues MMAs
 //   warps 2..9  epilogue: drain each K-segment accumulator (tcgen05.ld) into
-//               fp32 register sums, then scatter / store the finished tile.
-//               TMEM is double-buffered (2 x 256 columns) so draining segment
-//               s overlaps the MMAs of segment s+1.
+//               fp32 register sums, then scatter / store the finished tile;
+//               the peer's warps release TMEM buffers on the leader's barrier.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "sm100_ptx.cuh"
 #include "sos_internal.cuh"
 
 namespace sos {
 
-struct GemmArgs {
-    const uint8_t* A;
-    const uint8_t* B;
+struct Gemm2Args {
     int64_t a_rows;  // rows_total of the A S-layout
     int64_t b_rows;  // rows_total of the B S-layout
     int num_kb;      // K-blocks of 32
-    const TileCoord* tiles;
+    const TileCoord* tiles;  // (256-row block, 256-col block)
     int ntiles;
     const Scalars* scal;
-    int64_t N;   // valid rows (monomials)
-    int64_t Np;  // padded rows
-    const uint32_t* pt;  // forward: pair-rank table
-    float* coef;         // forward: output coefficients
-    float* grad;         // backward: output N x r
-    int64_t r;           // backward: columns of grad
-    unsigned long long* progress;  // K-skew counter (zeroed before the launch)
+    int64_t N;
+    int64_t Np;
+    const uint32_t* pt;
+    float* coef;
+    float* grad;
+    int64_t r;
+    unsigned long long* progress;
 };
 
-constexpr uint32_t kSmemBytes = kStages * kStageBytes + 256 + 1024;
+constexpr int kStages2 = 6;
+constexpr uint32_t kHalfTileBytes = 128 * 128;  // 128 rows x 128 B
+constexpr uint32_t kStage2Bytes = 2 * kHalfTileBytes;
+constexpr uint32_t kSmem2Bytes = kStages2 * kStage2Bytes + 256 + 1024;
+constexpr int kPairM = 256;
 
 template <bool kFwd>
-__global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Gemm2Args args) {
     extern __shared__ uint8_t smem_raw[];
-    // 1024-byte alignment of the shared-window address (SWIZZLE_128B atoms)
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    uint64_t* empty = full + kStages;
-    uint64_t* tfull = empty + kStages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStage2Bytes);
+    uint64_t* empty = full + kStages2;
+    uint64_t* tfull = empty + kStages2;
     uint64_t* tempty = tfull + 2;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kStages2; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
+            mbar_init(&tempty[a], 2 * kEpiWarps);  // epilogue warps of both CTAs
         }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(tslot, 512);
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+    }
+    if (warp == 1) tmem_alloc_2sm(tslot, 512);
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();  // barrier inits + TMEM address visible pair-wide
     tc_fence_after();
     const uint32_t tbase = *tslot;
 
     if (warp == 0) {
         // ------------------------------------------------------- producer --
         if (lane == 0) {
-            // Bounded K-skew: every kSkewEpoch K-blocks the producer publishes its
-            // progress and does not run more than kSkewLag epochs ahead of the grid,
-            // so the CTAs of a wave stream the same K-slabs of their shared panels
-            // through L2 instead of whole panels (cooperative launch: all resident).
             int stage = 0;
             uint32_t phase = 0;
-            int64_t g = 0;  // K-blocks issued by this CTA
+            int64_t g = 0;
             const unsigned long long G = gridDim.x;
-            for (int tile = blockIdx.x; tile < args.ntiles; tile += gridDim.x) {
+            for (int tile = cid; tile < args.ntiles; tile += ncl) {
                 const TileCoord tc = args.tiles[tile];
-                const uint8_t* srcA = args.A + (int64_t)tc.a * kBlockM * 128;
-                const uint8_t* srcB = args.B + (int64_t)tc.b * kBlockN * 128;
+                const int64_t rowA = (int64_t)tc.a * kPairM + rank * 128;
+                const int64_t rowB = (int64_t)tc.b * kBlockN + rank * 128;
                 for (int kb = 0; kb < args.num_kb; ++kb, ++g) {
+                    // Bounded K-skew: every kSkewEpoch K-blocks the producer publishes its
+                    // progress and waits (bounded) while it is more than kSkewLag epochs
+                    // ahead of the grid, so the CTAs of a wave stream the same K-slabs of
+                    // their shared panels through L2 instead of whole panels.
                     if (g % kSkewEpoch == 0 && g > 0) {
-                        const int64_t e = g / kSkewEpoch;  // epochs completed by this CTA
+                        const int64_t e = g / kSkewEpoch;
                         atomicAdd(args.progress, 1ull);
                         if (e >= kSkewLag) {
                             const unsigned long long need = G * (unsigned long long)(e - kSkewLag + 1);
-                            while (ld_acquire_u64(args.progress) < need) __nanosleep(256);
+                            for (int spin = 0; spin < kSkewMaxSpin && ld_acquire_u64(args.progress) < need; ++spin)
+                                __nanosleep(256);
                         }
                     }
                     mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* sa = smem + stage * kStageBytes;
-                    mbar_arrive_expect_tx(&full[stage], kStageBytes);
-                    bulk_g2s(sa, srcA + (int64_t)kb * args.a_rows * 128, kTileABytes, &full[stage]);
-                    bulk_g2s(sa + kTileABytes, srcB + (int64_t)kb * args.b_rows * 128, kTileBBytes, &full[stage]);
-                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                    uint8_t* sa = smem + stage * kStage2Bytes;
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStage2Bytes);
+                    tma_load_2d_2sm(sa, &tmA, &full[stage], 0, (int32_t)(kb * args.a_rows + rowA));
+                    tma_load_2d_2sm(sa + kHalfTileBytes, &tmB, &full[stage], 0, (int32_t)(kb * args.b_rows + rowB));
+                    if (++stage == kStages2) { stage = 0; phase ^= 1; }
                 }
             }
-            atomicAdd(args.progress, 1ull << 32);  // done: never hold back the others
+            atomicAdd(args.progress, 1ull << 32);
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer --
-        // The K loop of a tile is cut into segments of kSegKB K-blocks; each
-        // segment accumulates into one of the two TMEM buffers from zero and is
-        // drained by the epilogue into fp32 registers (round-to-nearest adds),
-        // bounding the number of in-TMEM accumulations per value.
-        if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_f16_f32(kBlockM, kBlockN);
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_f16_f32(kPairM, kBlockN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = blockIdx.x; tile < args.ntiles; tile += gridDim.x) {
+            for (int tile = cid; tile < args.ntiles; tile += ncl) {
                 for (int kb0 = 0; kb0 < args.num_kb; kb0 += kSegKB) {
                     const int kb1 = min(args.num_kb, kb0 + kSegKB);
-                    mbar_wait(&tempty[acc], acc_phase ^ 1);
+                    mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
                     const uint32_t d = tbase + acc * kBlockN;
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
-                        const uint32_t a0 = smem_u32(smem + stage * kStageBytes);
-                        const uint32_t b0 = a0 + kTileABytes;
+                        const uint32_t a0 = smem_u32(smem + stage * kStage2Bytes);
+                        const uint32_t b0 = a0 + kHalfTileBytes;
 #pragma unroll
                         for (int s = 0; s < 2; ++s) {
                             const uint64_t ah = umma_desc_sw128(a0 + s * 32);
                             const uint64_t al = umma_desc_sw128(a0 + 64 + s * 32);
                             const uint64_t bh = umma_desc_sw128(b0 + s * 32);
                             const uint64_t bl = umma_desc_sw128(b0 + 64 + s * 32);
-                            umma_f16(d, ah, bh, idesc, (kb != kb0 || s != 0) ? 1u : 0u);
-                            umma_f16(d, ah, bl, idesc, 1u);
-                            umma_f16(d, al, bh, idesc, 1u);
+                            umma_f16_2sm(d, ah, bh, idesc, (kb != kb0 || s != 0) ? 1u : 0u);
+                            umma_f16_2sm(d, ah, bl, idesc, 1u);
+                            umma_f16_2sm(d, al, bh, idesc, 1u);
                         }
-                        umma_commit(&empty[stage]);  // smem slot free once these MMAs finish
-                        if (++stage == kStages) { stage = 0; phase ^= 1; }
+                        umma_commit_2sm(&empty[stage], 0x3);  // both CTAs' smem slots free
+                        if (++stage == kStages2) { stage = 0; phase ^= 1; }
                     }
-                    umma_commit(&tfull[acc]);  // segment accumulator ready for the epilogue
+                    umma_commit_2sm(&tfull[acc], 0x3);  // both CTAs' epilogues may drain
                     acc ^= 1;
                     if (acc == 0) acc_phase ^= 1;
                 }
@@ -156,9 +172,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
         }
     } else {
         // -------------------------------------------------------- epilogue --
-        // 8 warps: warp w reads TMEM lane quarter q = w % 4 (rows 32q..32q+31 of
-        // the tile) and column half h (128 columns); each thread keeps its
-        // 128 running sums in registers.
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
         float scale;
@@ -170,9 +183,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
         }
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < args.ntiles; tile += gridDim.x) {
+        for (int tile = cid; tile < args.ntiles; tile += ncl) {
             const TileCoord tc = args.tiles[tile];
-            const int64_t i = (int64_t)tc.a * kBlockM + q * 32 + lane;
+            const int64_t i = (int64_t)tc.a * kPairM + rank * 128 + q * 32 + lane;
             float sum[kEpiCols];
 #pragma unroll
             for (int t = 0; t < kEpiCols; ++t) sum[t] = 0.f;
@@ -190,13 +203,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
             const int64_t cbase = (int64_t)tc.b * kBlockN + h * kEpiCols;
             if (kFwd) {
-                const bool strictly_upper = (int64_t)tc.a * kBlockM + kBlockM - 1 < (int64_t)tc.b * kBlockN;
+                // rows [a*256, a*256+256) vs cols [b*256, b*256+256): off the diagonal iff b > a
+                const bool strictly_upper = tc.b > tc.a;
 #pragma unroll
                 for (int ch = 0; ch < kEpiCols / 32; ++ch) {
                     const int64_t c0 = cbase + ch * 32;
@@ -242,45 +256,71 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(const GemmArgs args) {
 
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // all MMAs consumed and both epilogues done before freeing TMEM
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tbase, 512);
+        tmem_dealloc_2sm(tbase, 512);
     }
 }
 
-static void launch(const Plan& P, const GemmArgs& a, bool fwd, cudaStream_t st) {
+// ------------------------------------------------------------------ host --
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// S-layout viewed as a 2-D byte array [kb * rows_total + row][128]; a box of
+// 128 rows x 128 bytes is one contiguous, pre-swizzled 16 KB half tile.
+bool make_split_tmap(void* map_out, const uint8_t* base, int64_t rows_total, int64_t num_kb) {
+    CUtensorMap* map = reinterpret_cast<CUtensorMap*>(map_out);
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {128, (cuuint64_t)(rows_total * num_kb)};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {128, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <bool kFwd>
+static cudaError_t launch2(const Plan& P, const CUtensorMap& ma, const CUtensorMap& mb, const Gemm2Args& a,
+                           cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        cudaFuncSetAttribute(k_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(k_gemm2<kFwd>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes);
         configured = true;
     }
-    const int grid = a.ntiles < P.num_sms ? a.ntiles : P.num_sms;
-    if (grid <= 0) return;
+    int grid = 2 * a.ntiles < P.num_sms ? 2 * a.ntiles : P.num_sms;
+    grid &= ~1;
+    if (grid <= 0) return cudaSuccess;
     cudaMemsetAsync(a.progress, 0, sizeof(unsigned long long), st);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.dynamicSmemBytes = kSmem2Bytes;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (skew waits)
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (fwd) cudaLaunchKernelEx(&cfg, k_gemm<true>, a);
-    else cudaLaunchKernelEx(&cfg, k_gemm<false>, a);
+    cfg.attrs = nullptr;
+    cfg.numAttrs = 0;
+    return cudaLaunchKernelEx(&cfg, k_gemm2<kFwd>, ma, mb, a);
 }
 
-void launch_gemm_fwd(Plan& P, float* coef, cudaStream_t st) {
-    GemmArgs a{};
-    a.A = P.d_vs;
-    a.B = P.d_vs;
+void launch_gemm2_fwd(Plan& P, float* coef, cudaStream_t st) {
+    Gemm2Args a{};
     a.a_rows = P.idx->Np;
     a.b_rows = P.idx->Np;
     a.num_kb = (int)(P.rK / kBlockK);
-    a.tiles = P.d_tiles_fwd;
-    a.ntiles = P.ntiles_fwd;
+    a.tiles = P.d_tiles2_fwd;
+    a.ntiles = P.ntiles2_fwd;
     a.scal = P.d_scal;
     a.N = P.idx->N;
     a.Np = P.idx->Np;
@@ -288,18 +328,17 @@ void launch_gemm_fwd(Plan& P, float* coef, cudaStream_t st) {
     a.coef = coef;
     a.progress = P.d_progress;
     LaunchScope ls(P, KK_GEMM_FWD, st);
-    launch(P, a, true, st);
+    launch2<true>(P, *reinterpret_cast<const CUtensorMap*>(P.tmap_vs), *reinterpret_cast<const CUtensorMap*>(P.tmap_vs),
+                  a, st);
 }
 
-void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st) {
-    GemmArgs a{};
-    a.A = P.d_rs;
-    a.B = P.d_vts;
+void launch_gemm2_bwd(Plan& P, float* grad, cudaStream_t st) {
+    Gemm2Args a{};
     a.a_rows = P.idx->Np;
     a.b_rows = P.rN;
     a.num_kb = (int)(P.idx->Np / kBlockK);
-    a.tiles = P.d_tiles_bwd;
-    a.ntiles = P.ntiles_bwd;
+    a.tiles = P.d_tiles2_bwd;
+    a.ntiles = P.ntiles2_bwd;
     a.scal = P.d_scal;
     a.N = P.idx->N;
     a.Np = P.idx->Np;
@@ -307,7 +346,8 @@ void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st) {
     a.r = P.r;
     a.progress = P.d_progress + 1;
     LaunchScope ls(P, KK_GEMM_BWD, st);
-    launch(P, a, false, st);
+    launch2<false>(P, *reinterpret_cast<const CUtensorMap*>(P.tmap_rs),
+                   *reinterpret_cast<const CUtensorMap*>(P.tmap_vts), a, st);
 }
 
 }  // namespace sos

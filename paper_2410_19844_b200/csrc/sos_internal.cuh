@@ -41,14 +41,10 @@ struct Timing {
     }
 };
 
-constexpr int kBlockM = 128;   // tile rows  (UMMA M)
+constexpr int kBlockM = 128;   // tile rows per CTA (UMMA M = 256 per CTA pair)
 constexpr int kBlockN = 256;   // tile cols  (UMMA N)
 constexpr int kBlockK = 32;    // fp32-equivalent K per stage (hi+lo = 128 B rows)
 constexpr int kPad = 256;      // Np = N rounded up to kPad
-constexpr int kStages = 4;
-constexpr uint32_t kTileABytes = kBlockM * 128;  // 16 KB
-constexpr uint32_t kTileBBytes = kBlockN * 128;  // 32 KB
-constexpr uint32_t kStageBytes = kTileABytes + kTileBBytes;
 constexpr int kEpiWarps = 8;       // 4 TMEM lane quarters x 2 column halves
 constexpr int kEpiCols = kBlockN / 2;
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // warp0 producer, warp1 MMA, warps 2..9 epilogue
@@ -59,6 +55,7 @@ constexpr int kSegKB = 16;
 // bounded K-skew between the CTAs of a GEMM (see the producer in sos_gemm.cu)
 constexpr int kSkewEpoch = 16;  // K-blocks per progress epoch
 constexpr int kSkewLag = 2;     // epochs a CTA may run ahead of the slowest
+constexpr int kSkewMaxSpin = 8192;  // bounded wait (x 256 ns): the skew bound is a locality hint, never a deadlock
 constexpr uint32_t kInvalidRank = 0xFFFFFFFFu;
 constexpr int kMaxVars = 64;       // n + 2d <= 64
 constexpr int kMaxDeg2 = 64;
@@ -82,7 +79,7 @@ struct Index {
     uint32_t* d_pt;            // pair-rank table PT (Np*Np)
 };
 
-struct TileCoord { int a; int b; };  // a: 128-row block, b: 256-col block
+struct TileCoord { int a; int b; };  // a: 256-row block (CTA pair), b: 256-col block
 
 struct Plan {
     const Index* idx;
@@ -97,8 +94,11 @@ struct Plan {
     float* d_v;
     Scalars* d_scal;
     unsigned long long* d_progress;  // [2] K-skew counters (fwd, bwd)
-    TileCoord* d_tiles_fwd; int ntiles_fwd;
-    TileCoord* d_tiles_bwd; int ntiles_bwd;
+    TileCoord* d_tiles2_fwd; int ntiles2_fwd;  // CTA-pair tiles (256-row blocks)
+    TileCoord* d_tiles2_bwd; int ntiles2_bwd;
+    alignas(64) uint8_t tmap_vs[128];   // CUtensorMap of VS, VTS, RS (2-SM TMA loads)
+    alignas(64) uint8_t tmap_vts[128];
+    alignas(64) uint8_t tmap_rs[128];
     int opt_kind; float lr, b1, b2, eps; int64_t t; bool opt_ready;
     int64_t launches;
     int num_sms;
@@ -139,8 +139,9 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
 void launch_absmax_res(Plan& P, const float* res, cudaStream_t st);
 void launch_pack_r(Plan& P, const float* res, cudaStream_t st);
-void launch_gemm_fwd(Plan& P, float* coef, cudaStream_t st);
-void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st);
+void launch_gemm2_fwd(Plan& P, float* coef, cudaStream_t st);
+void launch_gemm2_bwd(Plan& P, float* grad, cudaStream_t st);
+bool make_split_tmap(void* map, const uint8_t* base, int64_t rows_total, int64_t num_kb);
 void launch_update(Plan& P, float* V, const float* grad, cudaStream_t st);
 
 }  // namespace sos

@@ -82,7 +82,7 @@ int sos_index_pair_ranks(const sos_index *idx, const int64_t *i_dev, const int64
 
 /* ------------------------------------------------------------------------
  * Plan: workspaces for one (index, r).  Device memory ~ 4*Np*(2*r + Np) bytes
- * plus 8*N*r for the gradient scratch (and 8*N*r more once Adam is enabled).
+ * (split operand tiles of V, V^T and R) plus 8*N*r once Adam is enabled.
  * ------------------------------------------------------------------------ */
 int sos_plan_create(const sos_index *idx, int64_t r, sos_plan **out);
 int sos_plan_destroy(sos_plan *plan);
@@ -103,7 +103,7 @@ int64_t sos_plan_launch_count(const sos_plan *plan);
 #define SOS_KERNEL_ABSMAX_R 4
 #define SOS_KERNEL_PACK_R 5
 #define SOS_KERNEL_GEMM_BWD 6
-#define SOS_KERNEL_UPDATE 7
+#define SOS_KERNEL_UPDATE 7 /* unused: sos_step applies the update inside GEMM_BWD */
 #define SOS_KERNEL_COUNT 8
 int sos_plan_timing(sos_plan *plan, int enable);
 int sos_plan_timing_read(sos_plan *plan, int kernel, double *total_ms, int64_t *launches);
@@ -141,7 +141,10 @@ typedef struct {
 int sos_opt_init(sos_plan *plan, const sos_opt_params *params, void *stream);
 
 /* One descent step, in place on V_dev:  loss_dev[0] = L(V) (before the update),
- * then V <- V - lr*g (GD) or the bias-corrected Adam update with t += 1. */
+ * then V <- V - lr*g (GD) or the bias-corrected Adam update with t += 1:
+ *   m <- b1 m + (1-b1) g,  v <- b2 v + (1-b2) g^2,
+ *   V <- V - lr (m / (1-b1^t)) / (sqrt(v / (1-b2^t)) + eps).
+ * The update runs inside the backward GEMM (the gradient never reaches HBM). */
 int sos_step(sos_plan *plan, float *V_dev, const float *p_dev, double *loss_dev, void *stream);
 
 /* Host-buffer entry point: copies p_host (M) and V_host (N x r) to the device,

@@ -206,8 +206,9 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
 
     if ((rc = dalloc(&P.d_vs, (size_t)(P.rK / 32) * Np * 128)) || (rc = dalloc(&P.d_vts, (size_t)(Np / 32) * P.rN * 128)) ||
         (rc = dalloc(&P.d_rs, (size_t)(Np / 32) * Np * 128)) || (rc = dalloc(&P.d_coef, (size_t)M * 4)) ||
-        (rc = dalloc(&P.d_res, (size_t)M * 4)) || (rc = dalloc(&P.d_grad, (size_t)N * r * 4)) ||
-        (rc = dalloc(&P.d_scal, sizeof(Scalars))) || (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) ||
+        (rc = dalloc(&P.d_res, (size_t)M * 4)) ||
+        (rc = dalloc(&P.d_scal, sizeof(Scalars))) ||
+        (rc = dalloc(&P.d_ring, (size_t)sms * 2 * 128 * 256 * 4)) || (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) ||
         (rc = dalloc(&P.d_tiles2_fwd, tf2.size() * sizeof(TileCoord))) ||
         (rc = dalloc(&P.d_tiles2_bwd, tb2.size() * sizeof(TileCoord)))) {
         sos_plan_destroy(pl);
@@ -239,10 +240,10 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_rs);
     cudaFree(P.d_coef);
     cudaFree(P.d_res);
-    cudaFree(P.d_grad);
     cudaFree(P.d_m);
     cudaFree(P.d_v);
     cudaFree(P.d_scal);
+    cudaFree(P.d_ring);
     cudaFree(P.d_progress);
     cudaFree(P.d_tiles2_fwd);
     cudaFree(P.d_tiles2_bwd);
@@ -361,11 +362,14 @@ int sos_step(sos_plan* pl, float* V_dev, const float* p_dev, double* loss_dev, v
     Plan& P = pl->P;
     if (!P.opt_ready) return fail(SOS_ERR_ARG, "sos_opt_init not called");
     cudaStream_t st = (cudaStream_t)stream;
-    int rc = do_loss_grad(P, V_dev, p_dev, loss_dev, P.d_grad, nullptr, st);
+    // loss and residual of the current V, then the backward GEMM whose aux
+    // warps apply the optimiser update to V in place, tile by tile
+    int rc = do_loss_grad(P, V_dev, p_dev, loss_dev, nullptr, nullptr, st);
     if (rc) return rc;
     P.t += 1;
-    launch_update(P, V_dev, P.d_grad, st);
-    return check_launch("step update");
+    launch_pack_r(P, P.d_res, st);
+    launch_gemm2_bwd_update(P, V_dev, st);
+    return check_launch("step");
 }
 
 int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t steps, double* losses_host) {

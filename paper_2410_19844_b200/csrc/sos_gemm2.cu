@@ -50,17 +50,72 @@ struct Gemm2Args {
     float* grad;
     int64_t r;
     unsigned long long* progress;
+    // kModeBwdUpdate: the optimiser step of PAPER.md:221, applied by the aux warps
+    float* ring;  // per-CTA ring of 2 finished gradient tiles (128 x 256 fp32 each)
+    float* V;
+    float* m;
+    float* v;
+    int adam;
+    float lr, b1, b2, lr_c1, inv_sqrt_c2, eps;
 };
+
+constexpr int kModeFwd = 0;        // Gram tile -> coefficient scatter
+constexpr int kModeBwdStore = 1;   // 4RV tile -> grad (sos_backward, sos_loss_grad)
+constexpr int kModeBwdUpdate = 2;  // 4RV tile -> ring -> aux warps update V (and Adam moments)
+constexpr int kRingTile = 128 * kBlockN;  // floats per ring slot
 
 constexpr int kStages2 = 6;
 constexpr uint32_t kHalfTileBytes = 128 * 128;  // 128 rows x 128 B
 constexpr uint32_t kStage2Bytes = 2 * kHalfTileBytes;
-constexpr uint32_t kSmem2Bytes = kStages2 * kStage2Bytes + 256 + 1024;
+constexpr uint32_t kSmem2Bytes = kStages2 * kStage2Bytes + 512 + 1024;
 constexpr int kPairM = 256;
 
-template <bool kFwd>
+// aux warps: one optimiser step on a finished 128 x 256 gradient tile
+// (coalesced: a warp covers 32 consecutive columns of one row per access)
+__device__ __forceinline__ void update_tile(const Gemm2Args& a, const float* __restrict__ gt, int64_t row0,
+                                            int64_t col0, int t) {
+#pragma unroll 1
+    for (int rr = 0; rr < 128; rr += 2) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int64_t i = row0 + rr + k;
+            if (i >= a.N) continue;
+            float gv[4], x[4], mm[4], vv[4];
+            int64_t off[4];
+            bool ok[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int c = t + 64 * e;
+                ok[e] = col0 + c < a.r;
+                off[e] = i * a.r + col0 + c;
+                gv[e] = __ldcg(gt + (rr + k) * kBlockN + c);
+                x[e] = ok[e] ? a.V[off[e]] : 0.f;
+                if (a.adam) {
+                    mm[e] = ok[e] ? a.m[off[e]] : 0.f;
+                    vv[e] = ok[e] ? a.v[off[e]] : 0.f;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (!ok[e]) continue;
+                if (a.adam) {
+                    mm[e] = a.b1 * mm[e] + (1.f - a.b1) * gv[e];
+                    vv[e] = a.b2 * vv[e] + (1.f - a.b2) * gv[e] * gv[e];
+                    a.m[off[e]] = mm[e];
+                    a.v[off[e]] = vv[e];
+                    a.V[off[e]] = x[e] - a.lr_c1 * mm[e] / (sqrtf(vv[e]) * a.inv_sqrt_c2 + a.eps);
+                } else {
+                    a.V[off[e]] = x[e] - a.lr * gv[e];
+                }
+            }
+        }
+    }
+}
+
+template <int kMode>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Gemm2Args args) {
+    constexpr bool kFwd = kMode == kModeFwd;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
@@ -68,7 +123,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint64_t* empty = full + kStages2;
     uint64_t* tfull = empty + kStages2;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* gready = tempty + 2;  // ring slot holds a finished gradient tile
+    uint64_t* gfree = gready + 2;   // ring slot consumed by the aux warps
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(gfree + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -84,6 +141,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 2 * kEpiWarps);  // epilogue warps of both CTAs
+            mbar_init(&gready[a], kEpiWarps);
+            mbar_init(&gfree[a], kAuxWarps);
         }
         fence_mbar_init();
     }
@@ -170,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 }
             }
         }
-    } else {
+    } else if (warp < 2 + kEpiWarps) {
         // -------------------------------------------------------- epilogue --
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
@@ -183,7 +242,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = cid; tile < args.ntiles; tile += ncl) {
+        int it = 0;
+        for (int tile = cid; tile < args.ntiles; tile += ncl, ++it) {
             const TileCoord tc = args.tiles[tile];
             const int64_t i = (int64_t)tc.a * kPairM + rank * 128 + q * 32 + lane;
             float sum[kEpiCols];
@@ -229,6 +289,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                         }
                     }
                 }
+            } else if (kMode == kModeBwdUpdate) {
+                // hand the finished tile to the aux warps through the per-CTA ring
+                const int slot = it & 1;
+                mbar_wait(&gfree[slot], ((it >> 1) & 1) ^ 1);
+                float4* gr = reinterpret_cast<float4*>(args.ring + ((int64_t)blockIdx.x * 2 + slot) * kRingTile +
+                                                       (q * 32 + lane) * kBlockN + h * kEpiCols);
+#pragma unroll
+                for (int u = 0; u < kEpiCols / 4; ++u)
+                    gr[u] = make_float4(scale * sum[4 * u], scale * sum[4 * u + 1], scale * sum[4 * u + 2],
+                                        scale * sum[4 * u + 3]);
+                __threadfence_block();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&gready[slot]);
             } else if (i < args.N) {
 #pragma unroll
                 for (int ch = 0; ch < kEpiCols / 32; ++ch) {
@@ -251,6 +324,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     }
                 }
             }
+        }
+    } else if (kMode == kModeBwdUpdate) {
+        // ----------------------------------------------------------- aux --
+        // optimiser step on tile t while the tensor cores work on tile t+1
+        const int t = threadIdx.x - 32 * (2 + kEpiWarps);  // 0..63
+        int it = 0;
+        for (int tile = cid; tile < args.ntiles; tile += ncl, ++it) {
+            const TileCoord tc = args.tiles[tile];
+            const int slot = it & 1;
+            mbar_wait(&gready[slot], (it >> 1) & 1);
+            update_tile(args, args.ring + ((int64_t)blockIdx.x * 2 + slot) * kRingTile,
+                        (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.b * kBlockN, t);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&gfree[slot]);
         }
     }
 
@@ -292,12 +379,12 @@ bool make_split_tmap(void* map_out, const uint8_t* base, int64_t rows_total, int
     return r == CUDA_SUCCESS;
 }
 
-template <bool kFwd>
+template <int kMode>
 static cudaError_t launch2(const Plan& P, const CUtensorMap& ma, const CUtensorMap& mb, const Gemm2Args& a,
                            cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_gemm2<kFwd>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes);
+        cudaFuncSetAttribute(k_gemm2<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes);
         configured = true;
     }
     int grid = 2 * a.ntiles < P.num_sms ? 2 * a.ntiles : P.num_sms;
@@ -311,8 +398,10 @@ static cudaError_t launch2(const Plan& P, const CUtensorMap& ma, const CUtensorM
     cfg.stream = st;
     cfg.attrs = nullptr;
     cfg.numAttrs = 0;
-    return cudaLaunchKernelEx(&cfg, k_gemm2<kFwd>, ma, mb, a);
+    return cudaLaunchKernelEx(&cfg, k_gemm2<kMode>, ma, mb, a);
 }
+
+static const CUtensorMap& tm(const uint8_t* raw) { return *reinterpret_cast<const CUtensorMap*>(raw); }
 
 void launch_gemm2_fwd(Plan& P, float* coef, cudaStream_t st) {
     Gemm2Args a{};
@@ -328,11 +417,10 @@ void launch_gemm2_fwd(Plan& P, float* coef, cudaStream_t st) {
     a.coef = coef;
     a.progress = P.d_progress;
     LaunchScope ls(P, KK_GEMM_FWD, st);
-    launch2<true>(P, *reinterpret_cast<const CUtensorMap*>(P.tmap_vs), *reinterpret_cast<const CUtensorMap*>(P.tmap_vs),
-                  a, st);
+    launch2<kModeFwd>(P, tm(P.tmap_vs), tm(P.tmap_vs), a, st);
 }
 
-void launch_gemm2_bwd(Plan& P, float* grad, cudaStream_t st) {
+static Gemm2Args bwd_args(Plan& P) {
     Gemm2Args a{};
     a.a_rows = P.idx->Np;
     a.b_rows = P.rN;
@@ -342,12 +430,40 @@ void launch_gemm2_bwd(Plan& P, float* grad, cudaStream_t st) {
     a.scal = P.d_scal;
     a.N = P.idx->N;
     a.Np = P.idx->Np;
-    a.grad = grad;
     a.r = P.r;
     a.progress = P.d_progress + 1;
+    return a;
+}
+
+void launch_gemm2_bwd(Plan& P, float* grad, cudaStream_t st) {
+    Gemm2Args a = bwd_args(P);
+    a.grad = grad;
     LaunchScope ls(P, KK_GEMM_BWD, st);
-    launch2<false>(P, *reinterpret_cast<const CUtensorMap*>(P.tmap_rs),
-                   *reinterpret_cast<const CUtensorMap*>(P.tmap_vts), a, st);
+    launch2<kModeBwdStore>(P, tm(P.tmap_rs), tm(P.tmap_vts), a, st);
+}
+
+// backward whose finished gradient tiles are consumed in the same kernel by the
+// optimiser step (GD or Adam): the gradient never makes an HBM round trip.  The
+// GEMM reads the packed copy VTS, never V, so updating V in place is safe.
+void launch_gemm2_bwd_update(Plan& P, float* V, cudaStream_t st) {
+    Gemm2Args a = bwd_args(P);
+    a.ring = P.d_ring;
+    a.V = V;
+    a.lr = P.lr;
+    a.adam = P.opt_kind == 1;
+    if (a.adam) {
+        const double c1 = 1.0 - pow((double)P.b1, (double)P.t);
+        const double c2 = 1.0 - pow((double)P.b2, (double)P.t);
+        a.m = P.d_m;
+        a.v = P.d_v;
+        a.b1 = P.b1;
+        a.b2 = P.b2;
+        a.eps = P.eps;
+        a.lr_c1 = (float)(P.lr / c1);
+        a.inv_sqrt_c2 = (float)(1.0 / sqrt(c2));
+    }
+    LaunchScope ls(P, KK_GEMM_BWD, st);
+    launch2<kModeBwdUpdate>(P, tm(P.tmap_rs), tm(P.tmap_vts), a, st);
 }
 
 }  // namespace sos

@@ -47,7 +47,8 @@ constexpr int kBlockK = 32;    // fp32-equivalent K per stage (hi+lo = 128 B row
 constexpr int kPad = 256;      // Np = N rounded up to kPad
 constexpr int kEpiWarps = 8;       // 4 TMEM lane quarters x 2 column halves
 constexpr int kEpiCols = kBlockN / 2;
-constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // warp0 producer, warp1 MMA, warps 2..9 epilogue
+constexpr int kAuxWarps = 2;       // optimiser-update warps of the backward GEMM
+constexpr int kGemmThreads = 64 + 32 * (kEpiWarps + kAuxWarps);  // producer, MMA, epilogue, aux
 // K-blocks accumulated in TMEM before the epilogue drains them into fp32
 // registers: tcgen05 fp32 accumulation truncates, so the number of in-TMEM
 // adds per value is bounded.
@@ -89,10 +90,10 @@ struct Plan {
     uint8_t* d_rs;    // RS
     float* d_coef;    // M
     float* d_res;     // M
-    float* d_grad;    // N*r (scratch for sos_step)
     float* d_m;       // Adam moments (lazy)
     float* d_v;
     Scalars* d_scal;
+    float* d_ring;    // per-CTA gradient tile ring of the fused backward + update
     unsigned long long* d_progress;  // [2] K-skew counters (fwd, bwd)
     TileCoord* d_tiles2_fwd; int ntiles2_fwd;  // CTA-pair tiles (256-row blocks)
     TileCoord* d_tiles2_bwd; int ntiles2_bwd;
@@ -141,7 +142,7 @@ void launch_absmax_res(Plan& P, const float* res, cudaStream_t st);
 void launch_pack_r(Plan& P, const float* res, cudaStream_t st);
 void launch_gemm2_fwd(Plan& P, float* coef, cudaStream_t st);
 void launch_gemm2_bwd(Plan& P, float* grad, cudaStream_t st);
+void launch_gemm2_bwd_update(Plan& P, float* V, cudaStream_t st);
 bool make_split_tmap(void* map, const uint8_t* base, int64_t rows_total, int64_t num_kb);
-void launch_update(Plan& P, float* V, const float* grad, cudaStream_t st);
 
 }  // namespace sos

@@ -1,6 +1,6 @@
 // sos_pointwise.cu -- HBM-bound kernels of the step: operand split/pack of V
-// and of the residual matrix R, the fused residual + loss reduction, and the
-// optimiser update.  All are coalesced, vectorised where the
+// and of the residual matrix R, and the fused residual + loss reduction (the
+// optimiser update of PAPER.md:221 runs inside the backward GEMM, sos_gemm2.cu).  All are coalesced, vectorised where the
 // layout allows, and sized as a multiple of the SM count (grid-stride).
 #include <cuda_fp16.h>
 
@@ -175,64 +175,6 @@ __global__ void __launch_bounds__(256) k_pack_r(const uint32_t* __restrict__ pt,
     }
 }
 
-// --------------------------------------------------------------- update ----
-__global__ void k_update_gd(float* __restrict__ V, const float* __restrict__ g, int64_t len, float lr) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool vec = ((reinterpret_cast<uintptr_t>(V) | reinterpret_cast<uintptr_t>(g)) & 15) == 0;
-    int64_t done = 0;
-    if (vec) {
-        const int64_t n4 = len >> 2;
-        float4* V4 = reinterpret_cast<float4*>(V);
-        const float4* g4 = reinterpret_cast<const float4*>(g);
-        for (int64_t t = tid; t < n4; t += stride) {
-            float4 v = V4[t];
-            const float4 d = __ldg(g4 + t);
-            v.x -= lr * d.x; v.y -= lr * d.y; v.z -= lr * d.z; v.w -= lr * d.w;
-            V4[t] = v;
-        }
-        done = n4 << 2;
-    }
-    for (int64_t t = done + tid; t < len; t += stride) V[t] -= lr * g[t];
-}
-
-__device__ __forceinline__ float adam_one(float& m, float& v, float g, float b1, float b2, float lr_c1, float inv_sqrt_c2,
-                                          float eps) {
-    m = b1 * m + (1.f - b1) * g;
-    v = b2 * v + (1.f - b2) * g * g;
-    return lr_c1 * m / (sqrtf(v) * inv_sqrt_c2 + eps);
-}
-
-// Adam: m <- b1 m + (1-b1) g ; v <- b2 v + (1-b2) g^2 ;
-// V <- V - lr (m/c1) / (sqrt(v/c2) + eps),  c1 = 1-b1^t, c2 = 1-b2^t
-__global__ void k_update_adam(float* __restrict__ V, const float* __restrict__ g, float* __restrict__ m,
-                              float* __restrict__ v, int64_t len, float lr_c1, float inv_sqrt_c2, float b1, float b2,
-                              float eps) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool vec = ((reinterpret_cast<uintptr_t>(V) | reinterpret_cast<uintptr_t>(g)) & 15) == 0;
-    int64_t done = 0;
-    if (vec) {
-        const int64_t n4 = len >> 2;
-        float4* V4 = reinterpret_cast<float4*>(V);
-        float4* m4 = reinterpret_cast<float4*>(m);
-        float4* v4 = reinterpret_cast<float4*>(v);
-        const float4* g4 = reinterpret_cast<const float4*>(g);
-        for (int64_t t = tid; t < n4; t += stride) {
-            float4 x = V4[t], mm = m4[t], vv = v4[t];
-            const float4 d = __ldg(g4 + t);
-            x.x -= adam_one(mm.x, vv.x, d.x, b1, b2, lr_c1, inv_sqrt_c2, eps);
-            x.y -= adam_one(mm.y, vv.y, d.y, b1, b2, lr_c1, inv_sqrt_c2, eps);
-            x.z -= adam_one(mm.z, vv.z, d.z, b1, b2, lr_c1, inv_sqrt_c2, eps);
-            x.w -= adam_one(mm.w, vv.w, d.w, b1, b2, lr_c1, inv_sqrt_c2, eps);
-            V4[t] = x; m4[t] = mm; v4[t] = vv;
-        }
-        done = n4 << 2;
-    }
-    for (int64_t t = done + tid; t < len; t += stride)
-        V[t] -= adam_one(m[t], v[t], g[t], b1, b2, lr_c1, inv_sqrt_c2, eps);
-}
-
 // -------------------------------------------------------------- launches ---
 static int grid_for(const Plan& P, int64_t work, int threads, int per_sm = 8) {
     int64_t b = (work + threads - 1) / threads;
@@ -268,19 +210,6 @@ void launch_pack_r(Plan& P, const float* res, cudaStream_t st) {
     const int64_t rows8 = P.idx->Np * P.idx->Np / 8;
     LaunchScope ls(P, KK_PACK_R, st);
     k_pack_r<<<grid_for(P, rows8, 256), 256, 0, st>>>(P.idx->d_pt, res, rows8, P.d_scal, P.d_rs);
-}
-
-void launch_update(Plan& P, float* V, const float* grad, cudaStream_t st) {
-    const int64_t len = P.idx->N * P.r;
-    LaunchScope ls(P, KK_UPDATE, st);
-    if (P.opt_kind == 0) {
-        k_update_gd<<<grid_for(P, len / 4, 256), 256, 0, st>>>(V, grad, len, P.lr);
-    } else {
-        const double c1 = 1.0 - pow((double)P.b1, (double)P.t);
-        const double c2 = 1.0 - pow((double)P.b2, (double)P.t);
-        k_update_adam<<<grid_for(P, len / 4, 256), 256, 0, st>>>(V, grad, P.d_m, P.d_v, len, (float)(P.lr / c1),
-                                                                (float)(1.0 / sqrt(c2)), P.b1, P.b2, P.eps);
-    }
 }
 
 }  // namespace sos

@@ -286,18 +286,20 @@ int sos_plan_timing_read(sos_plan* pl, int kernel, double* total_ms, int64_t* la
 }
 
 // --------------------------------------------------------------- compute --
-static int do_forward(Plan& P, const float* V, float* coef, cudaStream_t st) {
+// forward; with_vts also packs V^T (the backward's B operand) in the forward
+// GEMM's aux warps, hidden under its tensor-bound main loop
+static int do_forward(Plan& P, const float* V, float* coef, bool with_vts, cudaStream_t st) {
     CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
     CK(cudaMemsetAsync(coef, 0, (size_t)P.idx->M * 4, st));
     launch_absmax_v(P, V, st);
-    launch_pack_v(P, V, st);
-    launch_gemm2_fwd(P, coef, st);
+    launch_pack_v(P, V, false, st);
+    launch_gemm2_fwd(P, coef, with_vts ? V : nullptr, st);
     return check_launch("forward");
 }
 
 int sos_forward(sos_plan* pl, const float* V_dev, float* coef_dev, void* stream) {
     if (!pl || !V_dev || !coef_dev) return fail(SOS_ERR_ARG, "NULL argument");
-    return do_forward(pl->P, V_dev, coef_dev, (cudaStream_t)stream);
+    return do_forward(pl->P, V_dev, coef_dev, false, (cudaStream_t)stream);
 }
 
 int sos_backward(sos_plan* pl, const float* V_dev, const float* res_dev, float* grad_dev, void* stream) {
@@ -306,7 +308,7 @@ int sos_backward(sos_plan* pl, const float* V_dev, const float* res_dev, float* 
     cudaStream_t st = (cudaStream_t)stream;
     CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
     launch_absmax_v(P, V_dev, st);
-    launch_pack_v(P, V_dev, st);
+    launch_pack_v(P, V_dev, true, st);
     launch_absmax_res(P, res_dev, st);
     launch_pack_r(P, res_dev, st);
     launch_gemm2_bwd(P, grad_dev, st);
@@ -314,8 +316,8 @@ int sos_backward(sos_plan* pl, const float* V_dev, const float* res_dev, float* 
 }
 
 static int do_loss_grad(Plan& P, const float* V, const float* p, double* loss, float* grad, float* res,
-                        cudaStream_t st) {
-    int rc = do_forward(P, V, P.d_coef, st);
+                        cudaStream_t st, bool pack_vts_for_step = false) {
+    int rc = do_forward(P, V, P.d_coef, grad != nullptr || pack_vts_for_step, st);
     if (rc) return rc;
     float* r = res ? res : P.d_res;
     launch_residual(P, P.d_coef, p, r, st);
@@ -364,7 +366,7 @@ int sos_step(sos_plan* pl, float* V_dev, const float* p_dev, double* loss_dev, v
     cudaStream_t st = (cudaStream_t)stream;
     // loss and residual of the current V, then the backward GEMM whose aux
     // warps apply the optimiser update to V in place, tile by tile
-    int rc = do_loss_grad(P, V_dev, p_dev, loss_dev, nullptr, nullptr, st);
+    int rc = do_loss_grad(P, V_dev, p_dev, loss_dev, nullptr, nullptr, st, true);
     if (rc) return rc;
     P.t += 1;
     launch_pack_r(P, P.d_res, st);

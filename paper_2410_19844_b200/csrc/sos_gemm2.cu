@@ -33,6 +33,7 @@
 
 #include "sm100_ptx.cuh"
 #include "sos_internal.cuh"
+#include "sos_split.cuh"
 
 namespace sos {
 
@@ -57,6 +58,10 @@ struct Gemm2Args {
     float* v;
     int adam;
     float lr, b1, b2, lr_c1, inv_sqrt_c2, eps;
+    // kModeFwd with Vsrc != nullptr: the aux warps pack V^T into VTS meanwhile
+    const float* Vsrc;
+    uint8_t* vts;
+    int64_t rN;
 };
 
 constexpr int kModeFwd = 0;        // Gram tile -> coefficient scatter
@@ -67,7 +72,8 @@ constexpr int kRingTile = 128 * kBlockN;  // floats per ring slot
 constexpr int kStages2 = 6;
 constexpr uint32_t kHalfTileBytes = 128 * 128;  // 128 rows x 128 B
 constexpr uint32_t kStage2Bytes = 2 * kHalfTileBytes;
-constexpr uint32_t kSmem2Bytes = kStages2 * kStage2Bytes + 512 + 1024;
+constexpr uint32_t kAuxSmemBytes = 32 * 65 * 4;  // V tile staging of the aux warps' V^T pack
+constexpr uint32_t kSmem2Bytes = kStages2 * kStage2Bytes + 512 + kAuxSmemBytes + 1024;
 constexpr int kPairM = 256;
 
 // aux warps: one optimiser step on a finished 128 x 256 gradient tile
@@ -112,6 +118,34 @@ __device__ __forceinline__ void update_tile(const Gemm2Args& a, const float* __r
     }
 }
 
+// aux warps of the forward: VTS (V^T in the S-layout, K = row of V) for the
+// backward that follows, one 32 (rows j) x 64 (columns c) tile at a time,
+// transposed through shared memory; uses the scale s_v of this step's split.
+__device__ __forceinline__ void pack_vts_tiles(const Gemm2Args& a, float (*buf)[65], int t) {
+    const float s = a.scal->s_v;
+    const int64_t ncb = a.rN / 64;
+    const int64_t ntile = (a.Np / 32) * ncb;
+    for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+        const int64_t j0 = (tile / ncb) * 32, c0 = (tile % ncb) * 64;
+        const int64_t c = c0 + t;
+#pragma unroll 8
+        for (int jj = 0; jj < 32; ++jj) {
+            const int64_t j = j0 + jj;
+            buf[jj][t] = (j < a.N && c < a.r) ? __ldg(a.Vsrc + j * a.r + c) * s : 0.f;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int idx = t + 64 * k, cc = idx >> 2, q = idx & 3;
+            float x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = buf[q * 8 + e][cc];
+            store_split_row(a.vts + ((j0 >> 5) * a.rN + c0 + cc) * 128, c0 + cc, q, x);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
+    }
+}
+
 template <int kMode>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Gemm2Args args) {
@@ -126,6 +160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint64_t* gready = tempty + 2;  // ring slot holds a finished gradient tile
     uint64_t* gfree = gready + 2;   // ring slot consumed by the aux warps
     uint32_t* tslot = reinterpret_cast<uint32_t*>(gfree + 2);
+    float(*auxbuf)[65] = reinterpret_cast<float(*)[65]>(smem + kStages2 * kStage2Bytes + 512);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -325,6 +360,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 }
             }
         }
+    } else if (kMode == kModeFwd) {
+        // ----------------------------------------------------------- aux --
+        if (args.Vsrc) pack_vts_tiles(args, auxbuf, threadIdx.x - 32 * (2 + kEpiWarps));
     } else if (kMode == kModeBwdUpdate) {
         // ----------------------------------------------------------- aux --
         // optimiser step on tile t while the tensor cores work on tile t+1
@@ -403,8 +441,12 @@ static cudaError_t launch2(const Plan& P, const CUtensorMap& ma, const CUtensorM
 
 static const CUtensorMap& tm(const uint8_t* raw) { return *reinterpret_cast<const CUtensorMap*>(raw); }
 
-void launch_gemm2_fwd(Plan& P, float* coef, cudaStream_t st) {
+void launch_gemm2_fwd(Plan& P, float* coef, const float* V_for_vts, cudaStream_t st) {
     Gemm2Args a{};
+    a.Vsrc = V_for_vts;
+    a.vts = P.d_vts;
+    a.rN = P.rN;
+    a.r = P.r;
     a.a_rows = P.idx->Np;
     a.b_rows = P.idx->Np;
     a.num_kb = (int)(P.rK / kBlockK);

@@ -136,11 +136,11 @@ void launch_pair_lookup(const Index& ix, const int64_t* i, const int64_t* j, int
                         cudaStream_t st);
 
 void launch_absmax_v(Plan& P, const float* V, cudaStream_t st);
-void launch_pack_v(Plan& P, const float* V, cudaStream_t st);
+void launch_pack_v(Plan& P, const float* V, bool with_vts, cudaStream_t st);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
 void launch_absmax_res(Plan& P, const float* res, cudaStream_t st);
 void launch_pack_r(Plan& P, const float* res, cudaStream_t st);
-void launch_gemm2_fwd(Plan& P, float* coef, cudaStream_t st);
+void launch_gemm2_fwd(Plan& P, float* coef, const float* V_for_vts, cudaStream_t st);
 void launch_gemm2_bwd(Plan& P, float* grad, cudaStream_t st);
 void launch_gemm2_bwd_update(Plan& P, float* V, cudaStream_t st);
 bool make_split_tmap(void* map, const uint8_t* base, int64_t rows_total, int64_t num_kb);

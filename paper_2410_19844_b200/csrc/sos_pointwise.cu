@@ -5,37 +5,9 @@
 #include <cuda_fp16.h>
 
 #include "sos_internal.cuh"
+#include "sos_split.cuh"
 
 namespace sos {
-
-// power-of-two scale s with max|x| * s < 2^14 (fp16 hi/lo split headroom)
-__device__ __forceinline__ float split_scale(unsigned int absmax_bits) {
-    float a = __uint_as_float(absmax_bits);
-    if (!(a > 0.f) || !isfinite(a)) return 1.f;
-    int e;
-    frexpf(a, &e);  // a = f * 2^e, f in [0.5, 1)  =>  a < 2^e
-    return ldexpf(1.f, 14 - e);
-}
-
-// x*s = hi + lo with hi = fp16(x*s), lo = fp16(x*s - hi): ~22 significant bits
-__device__ __forceinline__ void split8(const float* x, uint4& hi, uint4& lo) {
-    __half h[8], l[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-        h[t] = __float2half_rn(x[t]);
-        l[t] = __float2half_rn(x[t] - __half2float(h[t]));
-    }
-    hi = *reinterpret_cast<uint4*>(h);
-    lo = *reinterpret_cast<uint4*>(l);
-}
-
-__device__ __forceinline__ void store_split_row(uint8_t* row128, int64_t row, int q, const float* x8) {
-    uint4 hi, lo;
-    split8(x8, hi, lo);
-    const int sw = (int)(row & 7);
-    reinterpret_cast<uint4*>(row128)[q ^ sw] = hi;
-    reinterpret_cast<uint4*>(row128)[(4 + q) ^ sw] = lo;
-}
 
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
@@ -113,6 +85,34 @@ __global__ void __launch_bounds__(256) k_pack_v(const float* __restrict__ V, int
             for (int t = 0; t < 8; ++t) x[t] = tile[q * 8 + t][cc];
             store_split_row(VTS + ((j0 >> 5) * rN + c) * 128, c, q, x);
         }
+    }
+}
+
+// ------------------------------------------------------------- pack VS ----
+// VS only: thread (row i, K-block kb, chunk q) splits V[i][32kb+8q .. +8].
+// A warp reads 256 consecutive floats of one row and writes 8 full 128-byte
+// S-layout rows.
+__global__ void __launch_bounds__(256) k_pack_vs(const float* __restrict__ V, int64_t N, int64_t r, int64_t Np,
+                                                 int64_t nkb, Scalars* __restrict__ sc, uint8_t* __restrict__ VS) {
+    const float s = split_scale(sc->absmax_v);
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->s_v = s;
+    const int64_t total = Np * nkb * 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int q = (int)(t & 3);
+        const int64_t rest = t >> 2;
+        const int64_t i = rest / nkb, kb = rest - i * nkb;
+        const int64_t c0 = kb * 32 + q * 8;
+        float x[8];
+        if (i < N && c0 + 8 <= r) {
+            const float* src = V + i * r + c0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = __ldg(src + e) * s;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = (i < N && c0 + e < r) ? __ldg(V + i * r + c0 + e) * s : 0.f;
+        }
+        store_split_row(VS + (kb * Np + i) * 128, i, q, x);
     }
 }
 
@@ -195,10 +195,15 @@ void launch_absmax_res(Plan& P, const float* res, cudaStream_t st) {
     k_absmax<<<grid_for(P, P.idx->M / 4, 256), 256, 0, st>>>(res, P.idx->M, &P.d_scal->absmax_r);
 }
 
-void launch_pack_v(Plan& P, const float* V, cudaStream_t st) {
-    dim3 grid((unsigned)(P.rN / 64), (unsigned)(P.idx->Np / 32));
+void launch_pack_v(Plan& P, const float* V, bool with_vts, cudaStream_t st) {
     LaunchScope ls(P, KK_PACK_V, st);
-    k_pack_v<<<grid, 256, 0, st>>>(V, P.idx->N, P.r, P.idx->Np, P.rK, P.rN, P.d_scal, P.d_vs, P.d_vts);
+    if (with_vts) {
+        dim3 grid((unsigned)(P.rN / 64), (unsigned)(P.idx->Np / 32));
+        k_pack_v<<<grid, 256, 0, st>>>(V, P.idx->N, P.r, P.idx->Np, P.rK, P.rN, P.d_scal, P.d_vs, P.d_vts);
+    } else {
+        const int64_t work = P.idx->Np * (P.rK / 32) * 4;
+        k_pack_vs<<<grid_for(P, work, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.idx->Np, P.rK / 32, P.d_scal, P.d_vs);
+    }
 }
 
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st) {

@@ -140,11 +140,26 @@ typedef struct {
 /* Reset the optimiser: zero the Adam moments, step counter t = 0. */
 int sos_opt_init(sos_plan *plan, const sos_opt_params *params, void *stream);
 
+/* Change the learning rate of an initialised optimiser without touching its
+ * state (Adam moments and step count t are kept): a step-size schedule for the
+ * descent of PAPER.md:221.  lr must be > 0.  Host-only; takes effect from the
+ * next sos_step. */
+int sos_opt_set_lr(sos_plan *plan, float lr);
+
+/* Stopping rule of the descent, decided ON THE DEVICE (no host sync): once the
+ * current V meets  ||coef(V V^T) - p||^2 <= rel_tol * ||p||^2  (Eq. 2 relative
+ * to the target's norm, reading R2), sos_step still evaluates the
+ * loss but skips the backward and the update, so V and the optimiser state stay
+ * at the first iterate that met the tolerance.  rel_tol <= 0 disables the rule
+ * (the default after sos_opt_init).  Host-only setter. */
+int sos_opt_set_stop(sos_plan *plan, double rel_tol);
+
 /* One descent step, in place on V_dev:  loss_dev[0] = L(V) (before the update),
  * then V <- V - lr*g (GD) or the bias-corrected Adam update with t += 1:
  *   m <- b1 m + (1-b1) g,  v <- b2 v + (1-b2) g^2,
  *   V <- V - lr (m / (1-b1^t)) / (sqrt(v / (1-b2^t)) + eps).
- * The update runs inside the backward GEMM (the gradient never reaches HBM). */
+ * The update runs inside the backward GEMM (the gradient never reaches HBM).
+ * With a stopping tolerance set (sos_opt_set_stop) and met, V is left unchanged. */
 int sos_step(sos_plan *plan, float *V_dev, const float *p_dev, double *loss_dev, void *stream);
 
 /* Host-buffer entry point: copies p_host (M) and V_host (N x r) to the device,

@@ -53,6 +53,8 @@ SIGNATURES = {
     "sos_backward": [_vp, _vp, _vp, _vp, _vp],
     "sos_loss_grad": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "sos_opt_init": [_vp, ctypes.POINTER(_OptParams), _vp],
+    "sos_opt_set_lr": [_vp, ctypes.c_float],
+    "sos_opt_set_stop": [_vp, ctypes.c_double],
     "sos_step": [_vp, _vp, _vp, _vp, _vp],
     "sos_solve_host": [_vp, _vp, _vp, _i64, _vp],
 }
@@ -207,6 +209,15 @@ class SosPlan:
                  eps: float = 1e-8):
         prm = _OptParams({"gd": SOS_OPT_GD, "adam": SOS_OPT_ADAM}[kind], lr, beta1, beta2, eps)
         _check(load().sos_opt_init(self._h, ctypes.byref(prm), _stream()))
+
+    def set_lr(self, lr: float):
+        """New learning rate for the next steps; optimiser state is kept."""
+        _check(load().sos_opt_set_lr(self._h, lr))
+
+    def set_stop(self, rel_tol: float):
+        """Device-side stopping rule: once ||coef - p||^2 <= rel_tol ||p||^2,
+        step() leaves V unchanged (0 disables)."""
+        _check(load().sos_opt_set_stop(self._h, rel_tol))
 
     def step(self, V: torch.Tensor, p: torch.Tensor, loss_out: Optional[torch.Tensor] = None) -> torch.Tensor:
         self._V(V)

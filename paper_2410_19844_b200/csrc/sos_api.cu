@@ -310,7 +310,7 @@ int sos_backward(sos_plan* pl, const float* V_dev, const float* res_dev, float* 
     launch_absmax_v(P, V_dev, st);
     launch_pack_v(P, V_dev, true, st);
     launch_absmax_res(P, res_dev, st);
-    launch_pack_r(P, res_dev, st);
+    launch_pack_r(P, res_dev, st, 0.0);
     launch_gemm2_bwd(P, grad_dev, st);
     return check_launch("backward");
 }
@@ -322,7 +322,7 @@ static int do_loss_grad(Plan& P, const float* V, const float* p, double* loss, f
     float* r = res ? res : P.d_res;
     launch_residual(P, P.d_coef, p, r, st);
     if (grad) {
-        launch_pack_r(P, r, st);
+        launch_pack_r(P, r, st, 0.0);
         launch_gemm2_bwd(P, grad, st);
     }
     if (loss) CK(cudaMemcpyAsync(loss, &P.d_scal->loss, sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -346,6 +346,7 @@ int sos_opt_init(sos_plan* pl, const sos_opt_params* prm, void* stream) {
     P.b2 = prm->beta2;
     P.eps = prm->eps;
     P.t = 0;
+    P.stop_tol = 0.0;
     if (prm->kind == SOS_OPT_ADAM) {
         if (!(prm->beta1 >= 0.f && prm->beta1 < 1.f && prm->beta2 >= 0.f && prm->beta2 < 1.f))
             return fail(SOS_ERR_ARG, "betas must be in [0,1)");
@@ -359,6 +360,21 @@ int sos_opt_init(sos_plan* pl, const sos_opt_params* prm, void* stream) {
     return SOS_OK;
 }
 
+int sos_opt_set_lr(sos_plan* pl, float lr) {
+    if (!pl) return fail(SOS_ERR_ARG, "plan is NULL");
+    if (!pl->P.opt_ready) return fail(SOS_ERR_ARG, "sos_opt_init not called");
+    if (!(lr > 0.f)) return fail(SOS_ERR_ARG, "lr must be > 0");
+    pl->P.lr = lr;
+    return SOS_OK;
+}
+
+int sos_opt_set_stop(sos_plan* pl, double rel_tol) {
+    if (!pl) return fail(SOS_ERR_ARG, "plan is NULL");
+    if (!(rel_tol == rel_tol)) return fail(SOS_ERR_ARG, "rel_tol is NaN");
+    pl->P.stop_tol = rel_tol > 0.0 ? rel_tol : 0.0;
+    return SOS_OK;
+}
+
 int sos_step(sos_plan* pl, float* V_dev, const float* p_dev, double* loss_dev, void* stream) {
     if (!pl || !V_dev || !p_dev) return fail(SOS_ERR_ARG, "NULL argument");
     Plan& P = pl->P;
@@ -369,7 +385,7 @@ int sos_step(sos_plan* pl, float* V_dev, const float* p_dev, double* loss_dev, v
     int rc = do_loss_grad(P, V_dev, p_dev, loss_dev, nullptr, nullptr, st, true);
     if (rc) return rc;
     P.t += 1;
-    launch_pack_r(P, P.d_res, st);
+    launch_pack_r(P, P.d_res, st, P.stop_tol);
     launch_gemm2_bwd_update(P, V_dev, st);
     return check_launch("step");
 }

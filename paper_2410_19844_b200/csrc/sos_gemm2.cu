@@ -62,6 +62,7 @@ struct Gemm2Args {
     const float* Vsrc;
     uint8_t* vts;
     int64_t rN;
+    double stop_tol;  // kModeBwdUpdate: sos_opt_set_stop rule (0 = off)
 };
 
 constexpr int kModeFwd = 0;        // Gram tile -> coefficient scatter
@@ -150,6 +151,9 @@ template <int kMode>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Gemm2Args args) {
     constexpr bool kFwd = kMode == kModeFwd;
+    // converged (sos_opt_set_stop): the whole grid leaves before any barrier,
+    // TMEM or cluster work, so V and the optimiser state stay as they are
+    if (kMode == kModeBwdUpdate && descent_stopped(args.scal, args.stop_tol)) return;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
@@ -491,6 +495,7 @@ void launch_gemm2_bwd_update(Plan& P, float* V, cudaStream_t st) {
     Gemm2Args a = bwd_args(P);
     a.ring = P.d_ring;
     a.V = V;
+    a.stop_tol = P.stop_tol;
     a.lr = P.lr;
     a.adam = P.opt_kind == 1;
     if (a.adam) {

@@ -70,6 +70,12 @@ struct Scalars {           // device-resident per-step scalars
     double pnorm2;         // sum p^2
 };
 
+// the device-side stopping rule of sos_step (sos_opt_set_stop), read after
+// the residual kernel completed the loss and |p|^2 reductions
+__device__ __forceinline__ bool descent_stopped(const Scalars* sc, double tol) {
+    return tol > 0.0 && sc->loss <= tol * sc->pnorm2;
+}
+
 struct Index {
     int n, d;
     int64_t N, M, Np;
@@ -101,6 +107,7 @@ struct Plan {
     alignas(64) uint8_t tmap_vts[128];
     alignas(64) uint8_t tmap_rs[128];
     int opt_kind; float lr, b1, b2, eps; int64_t t; bool opt_ready;
+    double stop_tol;  // sos_opt_set_stop: skip backward + update once loss <= stop_tol * |p|^2
     int64_t launches;
     int num_sms;
     Timing* timing;
@@ -139,7 +146,7 @@ void launch_absmax_v(Plan& P, const float* V, cudaStream_t st);
 void launch_pack_v(Plan& P, const float* V, bool with_vts, cudaStream_t st);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
 void launch_absmax_res(Plan& P, const float* res, cudaStream_t st);
-void launch_pack_r(Plan& P, const float* res, cudaStream_t st);
+void launch_pack_r(Plan& P, const float* res, cudaStream_t st, double stop_tol);
 void launch_gemm2_fwd(Plan& P, float* coef, const float* V_for_vts, cudaStream_t st);
 void launch_gemm2_bwd(Plan& P, float* grad, cudaStream_t st);
 void launch_gemm2_bwd_update(Plan& P, float* V, cudaStream_t st);

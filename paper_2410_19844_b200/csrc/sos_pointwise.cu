@@ -159,7 +159,9 @@ __global__ void k_residual(const float* __restrict__ coef, const float* __restri
 // R_ij = res[rank(alpha_i + alpha_j)] gathered through the pair-rank table,
 // written as the RS S-layout (same [jb][i][32] row structure as PT).
 __global__ void __launch_bounds__(256) k_pack_r(const uint32_t* __restrict__ pt, const float* __restrict__ res,
-                                                int64_t rows8, Scalars* __restrict__ sc, uint8_t* __restrict__ RS) {
+                                                int64_t rows8, Scalars* __restrict__ sc, uint8_t* __restrict__ RS,
+                                                double stop_tol) {
+    if (descent_stopped(sc, stop_tol)) return;
     const float s = split_scale(sc->absmax_r);
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->s_r = s;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -211,10 +213,10 @@ void launch_residual(Plan& P, const float* coef, const float* p, float* res, cud
     k_residual<<<grid_for(P, P.idx->M, 256, 4), 256, 0, st>>>(coef, p, res, P.idx->M, P.d_scal);
 }
 
-void launch_pack_r(Plan& P, const float* res, cudaStream_t st) {
+void launch_pack_r(Plan& P, const float* res, cudaStream_t st, double stop_tol) {
     const int64_t rows8 = P.idx->Np * P.idx->Np / 8;
     LaunchScope ls(P, KK_PACK_R, st);
-    k_pack_r<<<grid_for(P, rows8, 256), 256, 0, st>>>(P.idx->d_pt, res, rows8, P.d_scal, P.d_rs);
+    k_pack_r<<<grid_for(P, rows8, 256), 256, 0, st>>>(P.idx->d_pt, res, rows8, P.d_scal, P.d_rs, stop_tol);
 }
 
 }  // namespace sos

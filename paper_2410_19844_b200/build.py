@@ -8,8 +8,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsos_b200.so")
-SOURCES = ["sos_api.cu", "sos_index.cu", "sos_pointwise.cu", "sos_gemm2.cu"]
-HEADERS = ["sm100_ptx.cuh", "sos_internal.cuh"]
+SOURCES = ["sos_api.cu", "sos_index.cu", "sos_pointwise.cu", "sos_gemmq.cu"]
+HEADERS = ["sm100_ptx.cuh", "sos_internal.cuh", "sos_slice.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -1,7 +1,7 @@
 // sos_api.cu -- the C ABI declared in include/sos_b200.h (host side).
 // Argument checking, device memory ownership, launch sequencing.  Every
 // arithmetic step of the path runs in the kernels of sos_index.cu,
-// sos_pointwise.cu and sos_gemm.cu; there is no host or CPU fallback.
+// sos_pointwise.cu and sos_gemmq.cu; there is no host or CPU fallback.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -170,15 +170,17 @@ int sos_index_pair_ranks(const sos_index* h, const int64_t* i_dev, const int64_t
 }
 
 // ------------------------------------------------------------------- plan --
-// CTA-pair tiles: a = 256-row block, b = 256-col block, same grouped raster
-static void build_tiles2(int64_t Np, int64_t ncols_blocks, bool upper, std::vector<TileCoord>& out) {
-    const int64_t na = Np / 256;
-    const int64_t GA = 8;
-    for (int64_t g0 = 0; g0 < na; g0 += GA) {
-        const int64_t g1 = std::min(na, g0 + GA);
-        for (int64_t b = 0; b < ncols_blocks; ++b)
+// CTA-pair tiles: a = 256-row block, b = 160-col block, grouped raster (8 row
+// blocks per group) so a wave of CTAs shares A and B panels in L2
+static void build_tiles(int64_t row_blocks, int64_t col_blocks, bool upper, std::vector<TileCoord>& out) {
+    const char* ga = getenv("SOS_TILE_GROUP");
+    const int64_t GA = ga && atoi(ga) > 0 ? atoi(ga) : 8;
+    for (int64_t g0 = 0; g0 < row_blocks; g0 += GA) {
+        const int64_t g1 = std::min(row_blocks, g0 + GA);
+        for (int64_t b = 0; b < col_blocks; ++b)
             for (int64_t a = g0; a < g1; ++a) {
-                if (upper && b < a) continue;
+                // forward: keep the tile iff it holds some (i, j) with j >= i
+                if (upper && b * kTileN + kTileN - 1 < a * kPairM) continue;
                 out.push_back(TileCoord{(int)a, (int)b});
             }
     }
@@ -194,33 +196,48 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     Plan& P = pl->P;
     P.idx = &h->ix;
     P.r = r;
-    P.rK = ((r + kBlockK - 1) / kBlockK) * kBlockK;
-    P.rN = ((r + kBlockN - 1) / kBlockN) * kBlockN;
     P.num_sms = sms;
     const int64_t Np = h->ix.Np, N = h->ix.N, M = h->ix.M;
-    std::vector<TileCoord> tf2, tb2;
-    build_tiles2(Np, Np / kBlockN, true, tf2);
-    build_tiles2(Np, P.rN / kBlockN, false, tb2);
-    P.ntiles2_fwd = (int)tf2.size();
-    P.ntiles2_bwd = (int)tb2.size();
+    const int64_t colBlocksV = (N + kTileN - 1) / kTileN;
+    P.rowsV = std::max(Np, colBlocksV * kTileN);
+    P.nkbV = (r + kQK - 1) / kQK;
+    P.rowsVT = ((r + kTileN - 1) / kTileN) * kTileN;
+    P.nkbN = Np / kQK;
+    std::vector<TileCoord> tf, tb;
+    build_tiles(Np / kPairM, colBlocksV, true, tf);
+    build_tiles(Np / kPairM, P.rowsVT / kTileN, false, tb);
+    P.ntiles_fwd = (int)tf.size();
+    P.ntiles_bwd = (int)tb.size();
 
-    if ((rc = dalloc(&P.d_vs, (size_t)(P.rK / 32) * Np * 128)) || (rc = dalloc(&P.d_vts, (size_t)(Np / 32) * P.rN * 128)) ||
-        (rc = dalloc(&P.d_rs, (size_t)(Np / 32) * Np * 128)) || (rc = dalloc(&P.d_coef, (size_t)M * 4)) ||
-        (rc = dalloc(&P.d_res, (size_t)M * 4)) ||
-        (rc = dalloc(&P.d_scal, sizeof(Scalars))) ||
-        (rc = dalloc(&P.d_ring, (size_t)sms * 2 * 128 * 256 * 4)) || (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) ||
-        (rc = dalloc(&P.d_tiles2_fwd, tf2.size() * sizeof(TileCoord))) ||
-        (rc = dalloc(&P.d_tiles2_bwd, tb2.size() * sizeof(TileCoord)))) {
+    if ((rc = dalloc(&P.d_vq, (size_t)kSlices * P.nkbV * P.rowsV * 64)) ||
+        (rc = dalloc(&P.d_vtq, (size_t)kSlices * P.nkbN * P.rowsVT * 64)) ||
+        (rc = dalloc(&P.d_rq, (size_t)kSlices * P.nkbN * Np * 64)) ||
+        (rc = dalloc(&P.d_vrow, (size_t)P.rowsV * 4)) || (rc = dalloc(&P.d_vcol, (size_t)P.rowsVT * 4)) ||
+        (rc = dalloc(&P.d_rrow, (size_t)Np * 4)) || (rc = dalloc(&P.d_coef, (size_t)M * 4)) ||
+        (rc = dalloc(&P.d_res, (size_t)M * 4)) || (rc = dalloc(&P.d_scal, sizeof(Scalars))) ||
+        (rc = dalloc(&P.d_ring, (size_t)sms * 2 * 128 * kTileN * 4)) ||
+        (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) ||
+        (rc = dalloc(&P.d_tiles_fwd, std::max<size_t>(1, tf.size()) * sizeof(TileCoord))) ||
+        (rc = dalloc(&P.d_tiles_bwd, std::max<size_t>(1, tb.size()) * sizeof(TileCoord)))) {
         sos_plan_destroy(pl);
         return rc;
     }
-    if (cudaMemcpy(P.d_tiles2_fwd, tf2.data(), tf2.size() * sizeof(TileCoord), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(P.d_tiles2_bwd, tb2.data(), tb2.size() * sizeof(TileCoord), cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (cudaMemcpy(P.d_tiles_fwd, tf.data(), tf.size() * sizeof(TileCoord), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(P.d_tiles_bwd, tb.data(), tb.size() * sizeof(TileCoord), cudaMemcpyHostToDevice) != cudaSuccess) {
         sos_plan_destroy(pl);
         return fail(SOS_ERR_CUDA, "tile list upload");
     }
-    if (!make_split_tmap(P.tmap_vs, P.d_vs, Np, P.rK / 32) || !make_split_tmap(P.tmap_vts, P.d_vts, P.rN, Np / 32) ||
-        !make_split_tmap(P.tmap_rs, P.d_rs, Np, Np / 32)) {
+    // zero-initialised maxima: the GEMMs read them for padding rows too
+    if (cudaMemset(P.d_vrow, 0, (size_t)P.rowsV * 4) != cudaSuccess ||
+        cudaMemset(P.d_vcol, 0, (size_t)P.rowsVT * 4) != cudaSuccess ||
+        cudaMemset(P.d_rrow, 0, (size_t)Np * 4) != cudaSuccess) {
+        sos_plan_destroy(pl);
+        return fail(SOS_ERR_CUDA, "workspace init");
+    }
+    if (!make_q_tmap(P.tmap_vq_a, P.d_vq, P.rowsV, P.nkbV, 128) ||
+        !make_q_tmap(P.tmap_vq_b, P.d_vq, P.rowsV, P.nkbV, kHalfN) ||
+        !make_q_tmap(P.tmap_vtq_b, P.d_vtq, P.rowsVT, P.nkbN, kHalfN) ||
+        !make_q_tmap(P.tmap_rq_a, P.d_rq, Np, P.nkbN, 128)) {
         sos_plan_destroy(pl);
         return fail(SOS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     }
@@ -235,9 +252,12 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
 int sos_plan_destroy(sos_plan* pl) {
     if (!pl) return SOS_OK;
     Plan& P = pl->P;
-    cudaFree(P.d_vs);
-    cudaFree(P.d_vts);
-    cudaFree(P.d_rs);
+    cudaFree(P.d_vq);
+    cudaFree(P.d_vtq);
+    cudaFree(P.d_rq);
+    cudaFree(P.d_vrow);
+    cudaFree(P.d_vcol);
+    cudaFree(P.d_rrow);
     cudaFree(P.d_coef);
     cudaFree(P.d_res);
     cudaFree(P.d_m);
@@ -245,8 +265,8 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_scal);
     cudaFree(P.d_ring);
     cudaFree(P.d_progress);
-    cudaFree(P.d_tiles2_fwd);
-    cudaFree(P.d_tiles2_bwd);
+    cudaFree(P.d_tiles_fwd);
+    cudaFree(P.d_tiles_bwd);
     if (P.timing) {
         for (cudaEvent_t e : P.timing->pool) cudaEventDestroy(e);
         delete P.timing;
@@ -286,14 +306,14 @@ int sos_plan_timing_read(sos_plan* pl, int kernel, double* total_ms, int64_t* la
 }
 
 // --------------------------------------------------------------- compute --
-// forward; with_vts also packs V^T (the backward's B operand) in the forward
-// GEMM's aux warps, hidden under its tensor-bound main loop
-static int do_forward(Plan& P, const float* V, float* coef, bool with_vts, cudaStream_t st) {
+// forward; with_vtq also packs the V^T slices (the backward's B operand) in the
+// forward GEMM's aux warps, hidden under its tensor-bound main loop
+static int do_forward(Plan& P, const float* V, float* coef, bool with_vtq, cudaStream_t st) {
     CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
     CK(cudaMemsetAsync(coef, 0, (size_t)P.idx->M * 4, st));
-    launch_absmax_v(P, V, st);
-    launch_pack_v(P, V, false, st);
-    launch_gemm2_fwd(P, coef, with_vts ? V : nullptr, st);
+    launch_vmax(P, V, st);
+    launch_pack_vq(P, V, st);
+    launch_gemm_fwd(P, coef, with_vtq ? V : nullptr, st);
     return check_launch("forward");
 }
 
@@ -307,23 +327,24 @@ int sos_backward(sos_plan* pl, const float* V_dev, const float* res_dev, float* 
     Plan& P = pl->P;
     cudaStream_t st = (cudaStream_t)stream;
     CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
-    launch_absmax_v(P, V_dev, st);
-    launch_pack_v(P, V_dev, true, st);
-    launch_absmax_res(P, res_dev, st);
-    launch_pack_r(P, res_dev, st, 0.0);
-    launch_gemm2_bwd(P, grad_dev, st);
+    launch_vmax(P, V_dev, st);
+    launch_pack_vtq(P, V_dev, st);
+    launch_rmax(P, res_dev, st, 0.0);
+    launch_pack_rq(P, res_dev, st, 0.0);
+    launch_gemm_bwd(P, grad_dev, st);
     return check_launch("backward");
 }
 
 static int do_loss_grad(Plan& P, const float* V, const float* p, double* loss, float* grad, float* res,
-                        cudaStream_t st, bool pack_vts_for_step = false) {
-    int rc = do_forward(P, V, P.d_coef, grad != nullptr || pack_vts_for_step, st);
+                        cudaStream_t st, bool pack_vtq_for_step = false) {
+    int rc = do_forward(P, V, P.d_coef, grad != nullptr || pack_vtq_for_step, st);
     if (rc) return rc;
     float* r = res ? res : P.d_res;
     launch_residual(P, P.d_coef, p, r, st);
     if (grad) {
-        launch_pack_r(P, r, st, 0.0);
-        launch_gemm2_bwd(P, grad, st);
+        launch_rmax(P, r, st, 0.0);
+        launch_pack_rq(P, r, st, 0.0);
+        launch_gemm_bwd(P, grad, st);
     }
     if (loss) CK(cudaMemcpyAsync(loss, &P.d_scal->loss, sizeof(double), cudaMemcpyDeviceToDevice, st));
     return check_launch("loss_grad");
@@ -385,8 +406,9 @@ int sos_step(sos_plan* pl, float* V_dev, const float* p_dev, double* loss_dev, v
     int rc = do_loss_grad(P, V_dev, p_dev, loss_dev, nullptr, nullptr, st, true);
     if (rc) return rc;
     P.t += 1;
-    launch_pack_r(P, P.d_res, st, P.stop_tol);
-    launch_gemm2_bwd_update(P, V_dev, st);
+    launch_rmax(P, P.d_res, st, P.stop_tol);
+    launch_pack_rq(P, P.d_res, st, P.stop_tol);
+    launch_gemm_bwd_update(P, V_dev, st);
     return check_launch("step");
 }
 

@@ -1,0 +1,523 @@
+// sos_gemmq.cu -- the two tensor-core kernels of the step on CTA PAIRS
+// (tcgen05 cta_group::2, UMMA M = 256 split over the two SMs of a cluster),
+// int8 slice arithmetic with exact s32 accumulation (sos_internal.cuh).
+//
+//   forward:  G = V V^T on upper-triangular 256 x 160
+//            tiles; the epilogue reduces every G_ij straight into
+//            coef[rank(alpha_i + alpha_j)] (weight 2 above the diagonal, 1 on it),
+//            so the N x N Gram matrix never reaches HBM.
+//   backward (gradient of Eq. 2):      grad = 4 R V, R_ij = res[rank(alpha_i+alpha_j)]
+//            read as int8 slices of R, V^T as the B operand.
+//
+// Per 64-wide K-block each CTA stages its 128 A rows and 80 B rows, 3 slices
+// each (24 KB + 15 KB, SWIZZLE_64B), in a 5-stage mbarrier ring filled by 2-SM
+// TMA tensor loads; the leader issues, per 32-wide K step, the six slice
+// products into three s32 TMEM accumulators (columns 0, 160, 320):
+//     acc0 += a1 b1;  acc1 += a1 b2 + a2 b1;  acc2 += a1 b3 + a2 b2 + a3 b1.
+// s32 accumulation is exact, so the accumulators are drained once per tile (or
+// per kSegKBMax K-blocks for very long K) and combined in fp32 with the row
+// scales: value = u_i u_j (acc0 + acc1/254 + acc2/254^2).
+//
+// Warp roles (384 threads per CTA, 1 CTA per SM, persistent over a static tile list):
+//   warp 0      one lane issues the 2-SM TMA loads, completion on the leader's barrier
+//   warp 1      allocates 512 TMEM columns (pair-wide); the leader's lane 0 issues MMAs
+//   warps 2..9  epilogue: TMEM lane quarter (warp & 3) x column half (80 columns)
+//   warps 10,11 aux: forward -> pack V^T slices for the backward that follows;
+//               backward in sos_step -> optimiser update from the gradient-tile ring
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "sm100_ptx.cuh"
+#include "sos_internal.cuh"
+#include "sos_slice.cuh"
+
+namespace sos {
+
+struct GemmArgs {
+    int64_t a_rows;   // rows_total of the A Q-layout
+    int64_t b_rows;   // rows_total of the B Q-layout
+    int num_kb;       // K-blocks of 64
+    int seg_kb;       // K-blocks per exact s32 TMEM segment
+    const TileCoord* tiles;  // (256-row block, 160-col block)
+    int ntiles;
+    const unsigned* umaxA;  // row maxima (float bits) of the A operand rows
+    const unsigned* umaxB;  // row maxima of the B operand rows
+    int64_t N;
+    int64_t Np;
+    const uint32_t* pt;
+    float* coef;
+    float* grad;
+    int64_t r;
+    unsigned long long* progress;
+    int skew_epoch, skew_lag;  // bounded K-skew (K-blocks per epoch, epochs of lead)
+    // kModeBwdUpdate: the optimiser step of PAPER.md:221, applied by the aux warps
+    float* ring;  // per-CTA ring of 2 finished gradient tiles (128 x 160 fp32 each)
+    float* V;
+    float* m;
+    float* v;
+    int adam;
+    float lr, b1, b2, lr_c1, inv_sqrt_c2, eps;
+    const Scalars* scal;
+    double stop_tol;  // sos_opt_set_stop rule (0 = off)
+    // kModeFwd with Vsrc != nullptr: the aux warps pack V^T slices meanwhile
+    const float* Vsrc;
+    uint8_t* vtq;
+    int64_t rowsVT;
+    int64_t nkbN;
+    const unsigned* vcol;
+};
+
+constexpr int kModeFwd = 0;        // Gram tile -> coefficient scatter
+constexpr int kModeBwdStore = 1;   // 4RV tile -> grad (sos_backward, sos_loss_grad)
+constexpr int kModeBwdUpdate = 2;  // 4RV tile -> ring -> aux warps update V (and Adam moments)
+constexpr int kRingTile = 128 * kTileN;  // floats per ring slot
+
+constexpr int kStages = 5;
+constexpr uint32_t kASliceBytes = 128 * 64;        // 8 KB
+constexpr uint32_t kBSliceBytes = kHalfN * 64;     // 5 KB
+constexpr uint32_t kABytes = kSlices * kASliceBytes;
+constexpr uint32_t kBBytes = kSlices * kBSliceBytes;
+constexpr uint32_t kStageBytes = kABytes + kBBytes;  // 39936
+constexpr uint32_t kBarBytes = 256;
+constexpr uint32_t kAuxSmemBytes = 64 * 65 * 4;    // V tile staging of the aux warps' V^T pack
+constexpr uint32_t kSmemBytes = kStages * kStageBytes + kBarBytes + kAuxSmemBytes + 1024;
+constexpr float kInv254 = 1.f / 254.f;
+constexpr float kInv254sq = 1.f / (254.f * 254.f);
+
+// aux warps: one optimiser step on a finished 128 x 160 gradient tile
+// (coalesced: 64 threads cover consecutive columns of one row per access)
+__device__ __forceinline__ void update_tile(const GemmArgs& a, const float* __restrict__ gt, int64_t row0,
+                                            int64_t col0, int t) {
+#pragma unroll 1
+    for (int rr = 0; rr < 128; ++rr) {
+        const int64_t i = row0 + rr;
+        if (i >= a.N) break;
+        float gv[3], x[3], mm[3], vv[3];
+        int64_t off[3];
+        bool ok[3];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            const int c = t + 64 * e;
+            ok[e] = c < kTileN && col0 + c < a.r;
+            off[e] = i * a.r + col0 + c;
+            gv[e] = ok[e] ? __ldcg(gt + rr * kTileN + c) : 0.f;
+            x[e] = ok[e] ? a.V[off[e]] : 0.f;
+            if (a.adam) {
+                mm[e] = ok[e] ? a.m[off[e]] : 0.f;
+                vv[e] = ok[e] ? a.v[off[e]] : 0.f;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            if (!ok[e]) continue;
+            if (a.adam) {
+                mm[e] = a.b1 * mm[e] + (1.f - a.b1) * gv[e];
+                vv[e] = a.b2 * vv[e] + (1.f - a.b2) * gv[e] * gv[e];
+                a.m[off[e]] = mm[e];
+                a.v[off[e]] = vv[e];
+                a.V[off[e]] = x[e] - a.lr_c1 * mm[e] / (sqrtf(vv[e]) * a.inv_sqrt_c2 + a.eps);
+            } else {
+                a.V[off[e]] = x[e] - a.lr * gv[e];
+            }
+        }
+    }
+}
+
+template <int kMode>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    k_gemmq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
+    constexpr bool kFwd = kMode == kModeFwd;
+    // converged (sos_opt_set_stop): the whole grid leaves before any barrier,
+    // TMEM or cluster work, so V and the optimiser state stay as they are
+    if (kMode == kModeBwdUpdate && descent_stopped(args.scal, args.stop_tol)) return;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 1;
+    uint64_t* gready = tempty + 1;  // ring slot holds a finished gradient tile
+    uint64_t* gfree = gready + 2;   // ring slot consumed by the aux warps
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(gfree + 2);
+    float(*auxbuf)[65] = reinterpret_cast<float(*)[65]>(smem + kStages * kStageBytes + kBarBytes);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 2 * kEpiWarps);  // epilogue warps of both CTAs
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&gready[a], kEpiWarps);
+            mbar_init(&gfree[a], kAuxWarps);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+    }
+    if (warp == 1) tmem_alloc_2sm(tslot, 512);
+    tc_fence_before();
+    cluster_sync();  // barrier inits + TMEM address visible pair-wide
+    tc_fence_after();
+    const uint32_t tbase = *tslot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------- producer --
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int64_t g = 0;
+            const unsigned long long G = gridDim.x;
+            for (int tile = cid; tile < args.ntiles; tile += ncl) {
+                const TileCoord tc = args.tiles[tile];
+                const int32_t rowA = tc.a * kPairM + (int)rank * 128;
+                const int32_t rowB = tc.b * kTileN + (int)rank * kHalfN;
+                for (int kb = 0; kb < args.num_kb; ++kb, ++g) {
+                    // Bounded K-skew: every kSkewEpoch K-blocks the producer publishes its
+                    // progress and waits (bounded) while it is more than kSkewLag epochs
+                    // ahead of the grid, so the CTAs of a wave stream the same K-slabs of
+                    // their shared panels through L2 instead of whole panels.
+                    if (g % args.skew_epoch == 0 && g > 0) {
+                        const int64_t e = g / args.skew_epoch;
+                        atomicAdd(args.progress, 1ull);
+                        if (e >= args.skew_lag) {
+                            const unsigned long long need = G * (unsigned long long)(e - args.skew_lag + 1);
+                            for (int spin = 0; spin < kSkewMaxSpin && ld_acquire_u64(args.progress) < need; ++spin)
+                                __nanosleep(256);
+                        }
+                    }
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * kStageBytes;
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+                    tma_load_3d_2sm(sa, &tmA, &full[stage], 0, (int32_t)(kb * args.a_rows + rowA), 0);
+                    tma_load_3d_2sm(sa + kABytes, &tmB, &full[stage], 0, (int32_t)(kb * args.b_rows + rowB), 0);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+            }
+            atomicAdd(args.progress, 1ull << 32);
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------ MMA issuer --
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_s8_s32(kPairM, kTileN);
+            const uint32_t d0 = tbase, d1 = tbase + kTileN, d2 = tbase + 2 * kTileN;
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = cid; tile < args.ntiles; tile += ncl) {
+                for (int kb0 = 0; kb0 < args.num_kb; kb0 += args.seg_kb) {
+                    const int kb1 = min(args.num_kb, kb0 + args.seg_kb);
+                    mbar_wait_cluster(tempty, acc_phase ^ 1);
+                    tc_fence_after();
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(smem + stage * kStageBytes);
+                        const uint32_t b0 = a0 + kABytes;
+#pragma unroll
+                        for (int ks = 0; ks < 2; ++ks) {
+                            const uint64_t a1 = umma_desc_sw64(a0 + ks * 32);
+                            const uint64_t a2 = umma_desc_sw64(a0 + kASliceBytes + ks * 32);
+                            const uint64_t a3 = umma_desc_sw64(a0 + 2 * kASliceBytes + ks * 32);
+                            const uint64_t b1 = umma_desc_sw64(b0 + ks * 32);
+                            const uint64_t b2 = umma_desc_sw64(b0 + kBSliceBytes + ks * 32);
+                            const uint64_t b3 = umma_desc_sw64(b0 + 2 * kBSliceBytes + ks * 32);
+                            const uint32_t acc = (kb != kb0 || ks != 0) ? 1u : 0u;
+                            umma_s8_2sm(d0, a1, b1, idesc, acc);
+                            umma_s8_2sm(d1, a1, b2, idesc, acc);
+                            umma_s8_2sm(d1, a2, b1, idesc, 1u);
+                            umma_s8_2sm(d2, a1, b3, idesc, acc);
+                            umma_s8_2sm(d2, a2, b2, idesc, 1u);
+                            umma_s8_2sm(d2, a3, b1, idesc, 1u);
+                        }
+                        umma_commit_2sm(&empty[stage], 0x3);  // both CTAs' smem slots free
+                        if (++stage == kStages) { stage = 0; phase ^= 1; }
+                    }
+                    umma_commit_2sm(tfull, 0x3);  // both CTAs' epilogues may drain
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp < 2 + kEpiWarps) {
+        // -------------------------------------------------------- epilogue --
+        const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
+        uint32_t acc_phase = 0;
+        int it = 0;
+        for (int tile = cid; tile < args.ntiles; tile += ncl, ++it) {
+            const TileCoord tc = args.tiles[tile];
+            const int64_t i = (int64_t)tc.a * kPairM + rank * 128 + q * 32 + lane;
+            float sum[kEpiCols];
+#pragma unroll
+            for (int t = 0; t < kEpiCols; ++t) sum[t] = 0.f;
+            for (int kb0 = 0; kb0 < args.num_kb; kb0 += args.seg_kb) {
+                mbar_wait(tfull, acc_phase);
+                tc_fence_after();
+                const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + h * kEpiCols;
+#pragma unroll
+                for (int ch = 0; ch < kEpiCols / 16; ++ch) {
+                    uint32_t v0[16], v1[16], v2[16];
+                    tmem_ld16(tq + ch * 16, v0);
+                    tmem_ld16(tq + kTileN + ch * 16, v1);
+                    tmem_ld16(tq + 2 * kTileN + ch * 16, v2);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int t = 0; t < 16; ++t)
+                        sum[ch * 16 + t] += fmaf((float)(int)v2[t], kInv254sq,
+                                                 fmaf((float)(int)v1[t], kInv254, (float)(int)v0[t]));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty, 0);
+                acc_phase ^= 1;
+            }
+            const int64_t cbase = (int64_t)tc.b * kTileN + h * kEpiCols;
+            const float ui = slice_unit(__ldg(args.umaxA + i));
+            if (kFwd) {
+                // rows [256a, 256a+256) vs cols [160b, 160b+160): all above the diagonal iff 160b >= 256a + 256
+                const bool strictly_upper = (int64_t)tc.b * kTileN >= (int64_t)tc.a * kPairM + kPairM;
+                if (i < args.N) {
+#pragma unroll
+                    for (int ch = 0; ch < kEpiCols / 16; ++ch) {
+                        const int64_t c0 = cbase + ch * 16;
+                        if (c0 >= args.N) break;
+                        const uint4* prow = reinterpret_cast<const uint4*>(
+                            args.pt + ((c0 / kPtW) * args.Np + i) * kPtW + (c0 % kPtW));
+                        const uint4* pu = reinterpret_cast<const uint4*>(args.umaxB + c0);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint4 rk = __ldg(prow + u);
+                            const uint4 ub = __ldg(pu + u);
+                            const uint32_t rr[4] = {rk.x, rk.y, rk.z, rk.w};
+                            const uint32_t bb[4] = {ub.x, ub.y, ub.z, ub.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const int t = u * 4 + e;
+                                if (rr[e] == kInvalidRank) continue;
+                                const int64_t j = c0 + t;
+                                const float w = strictly_upper ? 2.f : (i < j ? 2.f : (i == j ? 1.f : 0.f));
+                                if (w != 0.f)
+                                    red_add_f32(args.coef + rr[e], w * ui * slice_unit(bb[e]) * sum[ch * 16 + t]);
+                            }
+                        }
+                    }
+                }
+            } else if (kMode == kModeBwdUpdate) {
+                // hand the finished tile to the aux warps through the per-CTA ring
+                const int slot = it & 1;
+                mbar_wait(&gfree[slot], ((it >> 1) & 1) ^ 1);
+                float4* gr = reinterpret_cast<float4*>(args.ring + ((int64_t)blockIdx.x * 2 + slot) * kRingTile +
+                                                       (q * 32 + lane) * kTileN + h * kEpiCols);
+                const float s4 = 4.f * ui;
+#pragma unroll
+                for (int u = 0; u < kEpiCols / 4; ++u) {
+                    const uint4 ub = __ldg(reinterpret_cast<const uint4*>(args.umaxB + cbase) + u);
+                    gr[u] = make_float4(s4 * slice_unit(ub.x) * sum[4 * u], s4 * slice_unit(ub.y) * sum[4 * u + 1],
+                                        s4 * slice_unit(ub.z) * sum[4 * u + 2], s4 * slice_unit(ub.w) * sum[4 * u + 3]);
+                }
+                __threadfence_block();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&gready[slot]);
+            } else if (i < args.N) {
+                const float s4 = 4.f * ui;
+#pragma unroll
+                for (int u = 0; u < kEpiCols / 4; ++u) {
+                    const int64_t c0 = cbase + 4 * u;
+                    const uint4 ub = __ldg(reinterpret_cast<const uint4*>(args.umaxB + cbase) + u);
+                    const float o[4] = {s4 * slice_unit(ub.x) * sum[4 * u], s4 * slice_unit(ub.y) * sum[4 * u + 1],
+                                        s4 * slice_unit(ub.z) * sum[4 * u + 2], s4 * slice_unit(ub.w) * sum[4 * u + 3]};
+                    float* g = args.grad + i * args.r + c0;
+                    if (c0 + 4 <= args.r && ((reinterpret_cast<uintptr_t>(g) & 15) == 0)) {
+                        *reinterpret_cast<float4*>(g) = make_float4(o[0], o[1], o[2], o[3]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (c0 + e < args.r) g[e] = o[e];
+                    }
+                }
+            }
+        }
+    } else if (kMode == kModeFwd) {
+        // ----------------------------------------------------------- aux --
+        // V^T slices for the backward that follows (hidden under the MMA loop)
+        if (args.Vsrc) {
+            const int t = threadIdx.x - 32 * (2 + kEpiWarps);
+            const int64_t nkt = (args.rowsVT + 63) / 64;
+            for (int64_t b = blockIdx.x; b < args.nkbN * nkt; b += gridDim.x)
+                pack_vtq_tile(args.Vsrc, args.N, args.r, args.rowsVT, args.nkbN, args.vcol, args.vtq, b / nkt,
+                              (b % nkt) * 64, auxbuf, t, 32 * kAuxWarps);
+        }
+    } else if (kMode == kModeBwdUpdate) {
+        // ----------------------------------------------------------- aux --
+        // optimiser step on tile t while the tensor cores work on tile t+1
+        const int t = threadIdx.x - 32 * (2 + kEpiWarps);  // 0..63
+        int it = 0;
+        for (int tile = cid; tile < args.ntiles; tile += ncl, ++it) {
+            const TileCoord tc = args.tiles[tile];
+            const int slot = it & 1;
+            mbar_wait(&gready[slot], (it >> 1) & 1);
+            update_tile(args, args.ring + ((int64_t)blockIdx.x * 2 + slot) * kRingTile,
+                        (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.b * kTileN, t);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&gfree[slot]);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // all MMAs consumed and both epilogues done before freeing TMEM
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_2sm(tbase, 512);
+    }
+}
+
+// ------------------------------------------------------------------ host --
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// Q-layout viewed as a 3-D byte array [slice][kb * rows_total + row][64]; a box
+// of box_rows x 64 bytes x 3 slices is one pipeline stage of one operand.
+bool make_q_tmap(void* map_out, const uint8_t* base, int64_t rows_total, int64_t nkb, int box_rows) {
+    CUtensorMap* map = reinterpret_cast<CUtensorMap*>(map_out);
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {64, (cuuint64_t)(rows_total * nkb), (cuuint64_t)kSlices};
+    cuuint64_t strides[2] = {64, (cuuint64_t)(rows_total * nkb * 64)};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)kSlices};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+static int env_int(const char* name, int dflt) {
+    const char* s = getenv(name);
+    return s && *s ? atoi(s) : dflt;
+}
+
+template <int kMode>
+static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorMap& mb, GemmArgs a,
+                           cudaStream_t st) {
+    static const int epoch = env_int("SOS_SKEW_EPOCH", kSkewEpoch), lag = env_int("SOS_SKEW_LAG", kSkewLag);
+    a.skew_epoch = epoch > 0 ? epoch : 1 << 30;
+    a.skew_lag = lag;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_gemmq<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        configured = true;
+    }
+    int grid = 2 * a.ntiles < P.num_sms ? 2 * a.ntiles : P.num_sms;
+    grid &= ~1;
+    if (grid <= 0) return cudaSuccess;
+    cudaMemsetAsync(a.progress, 0, sizeof(unsigned long long), st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = st;
+    cfg.attrs = nullptr;
+    cfg.numAttrs = 0;
+    return cudaLaunchKernelEx(&cfg, k_gemmq<kMode>, ma, mb, a);
+}
+
+static const CUtensorMap& tm(const uint8_t* raw) { return *reinterpret_cast<const CUtensorMap*>(raw); }
+
+void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st) {
+    GemmArgs a{};
+    a.Vsrc = V_for_vtq;
+    a.vtq = P.d_vtq;
+    a.rowsVT = P.rowsVT;
+    a.nkbN = P.nkbN;
+    a.vcol = P.d_vcol;
+    a.r = P.r;
+    a.a_rows = P.rowsV;
+    a.b_rows = P.rowsV;
+    a.num_kb = (int)P.nkbV;
+    a.seg_kb = kSegKBMax;
+    a.tiles = P.d_tiles_fwd;
+    a.ntiles = P.ntiles_fwd;
+    a.umaxA = P.d_vrow;
+    a.umaxB = P.d_vrow;
+    a.N = P.idx->N;
+    a.Np = P.idx->Np;
+    a.pt = P.idx->d_pt;
+    a.coef = coef;
+    a.progress = P.d_progress;
+    LaunchScope ls(P, KK_GEMM_FWD, st);
+    launchq<kModeFwd>(P, tm(P.tmap_vq_a), tm(P.tmap_vq_b), a, st);
+}
+
+static GemmArgs bwd_args(Plan& P) {
+    GemmArgs a{};
+    a.a_rows = P.idx->Np;
+    a.b_rows = P.rowsVT;
+    a.num_kb = (int)P.nkbN;
+    a.seg_kb = kSegKBMax;
+    a.tiles = P.d_tiles_bwd;
+    a.ntiles = P.ntiles_bwd;
+    a.umaxA = P.d_rrow;
+    a.umaxB = P.d_vcol;
+    a.N = P.idx->N;
+    a.Np = P.idx->Np;
+    a.r = P.r;
+    a.scal = P.d_scal;
+    a.progress = P.d_progress + 1;
+    return a;
+}
+
+void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st) {
+    GemmArgs a = bwd_args(P);
+    a.grad = grad;
+    LaunchScope ls(P, KK_GEMM_BWD, st);
+    launchq<kModeBwdStore>(P, tm(P.tmap_rq_a), tm(P.tmap_vtq_b), a, st);
+}
+
+// backward whose finished gradient tiles are consumed in the same kernel by the
+// optimiser step (GD or Adam): the gradient never makes an HBM round trip.  The
+// GEMM reads the packed copy VTQ, never V, so updating V in place is safe.
+void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st) {
+    GemmArgs a = bwd_args(P);
+    a.ring = P.d_ring;
+    a.V = V;
+    a.stop_tol = P.stop_tol;
+    a.lr = P.lr;
+    a.adam = P.opt_kind == 1;
+    if (a.adam) {
+        const double c1 = 1.0 - pow((double)P.b1, (double)P.t);
+        const double c2 = 1.0 - pow((double)P.b2, (double)P.t);
+        a.m = P.d_m;
+        a.v = P.d_v;
+        a.b1 = P.b1;
+        a.b2 = P.b2;
+        a.eps = P.eps;
+        a.lr_c1 = (float)(P.lr / c1);
+        a.inv_sqrt_c2 = (float)(1.0 / sqrt(c2));
+    }
+    LaunchScope ls(P, KK_GEMM_BWD, st);
+    launchq<kModeBwdUpdate>(P, tm(P.tmap_rq_a), tm(P.tmap_vtq_b), a, st);
+}
+
+}  // namespace sos

@@ -69,7 +69,7 @@ __device__ __forceinline__ uint32_t pair_rank(const uint8_t* mi, const uint8_t* 
     return rank;
 }
 
-// PT in [jb][i][32] order; one thread per entry
+// PT in [jb][i][64] order (jb = j / 64); one thread per entry
 __global__ void k_pair_table(int64_t N, int64_t Np, int d, const uint32_t* __restrict__ g_binom, int nb,
                              const uint8_t* __restrict__ ms, uint32_t* __restrict__ pt) {
     extern __shared__ uint32_t s_binom[];
@@ -79,10 +79,10 @@ __global__ void k_pair_table(int64_t N, int64_t Np, int d, const uint32_t* __res
     const int64_t total = Np * Np;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t jb = t / (Np * 32);
-        int64_t rem = t - jb * Np * 32;
-        int64_t i = rem >> 5;
-        int64_t j = jb * 32 + (rem & 31);
+        int64_t jb = t / (Np * kPtW);
+        int64_t rem = t - jb * Np * kPtW;
+        int64_t i = rem / kPtW;
+        int64_t j = jb * kPtW + rem % kPtW;
         uint32_t out = kInvalidRank;
         if (i < N && j < N) {
             uint8_t mi[kMaxDeg2 / 2], mj[kMaxDeg2 / 2];
@@ -102,7 +102,7 @@ __global__ void k_pair_lookup(const uint32_t* __restrict__ pt, int64_t N, int64_
     if (t >= cnt) return;
     int64_t i = I[t], j = J[t];
     uint32_t v = kInvalidRank;
-    if (i >= 0 && j >= 0 && i < N && j < N) v = pt[((j >> 5) * Np + i) * 32 + (j & 31)];
+    if (i >= 0 && j >= 0 && i < N && j < N) v = pt[((j / kPtW) * Np + i) * kPtW + (j % kPtW)];
     out[t] = v;
 }
 

@@ -1,19 +1,29 @@
 // sos_internal.cuh -- shared definitions of the CUDA path (not part of the ABI).
 //
-// HBM layouts (DESIGN.md "Data layout"):
-//   * split operand tiles "S-layout": an fp32 matrix X[rows][K] is stored as
-//     fp16 hi/lo pairs scaled by a power of two s (x*s = hi + lo + O(2^-22 |x*s|)),
-//     in K-blocks of 32:   byte offset of row `row`, K-block kb =
-//         (kb * rows_total + row) * 128
-//     and inside that 128-byte row the 16-byte chunk c (c<4: hi of k=8c..8c+7,
-//     c>=4: lo of k=8(c-4)..) lives at physical chunk c ^ (row & 7) -- exactly
-//     the UMMA K-major SWIZZLE_128B image, so a 128-row x 32-K tile is one
-//     contiguous 16 KB block copied to shared memory by one bulk copy.
-//       VS  = V   as [rK/32][Np][128B]   (forward A and B operands, K = column of V)
-//       VTS = V^T as [Np/32][rN][128B]   (backward B operand, K = row of V)
-//       RS  = R   as [Np/32][Np][128B]   (backward A operand, K = column j of R)
-//   * pair-rank table PT[jb][i][32] (uint32): PT[((j/32)*Np + i)*32 + j%32] =
-//     rank(alpha_i + alpha_j), 0xFFFFFFFF for padding (i >= N or j >= N).
+// Precision scheme: every fp32 operand row x (a row of
+// V, of V^T or of R) is stored as three signed-int8 slices against a per-row
+// scale u = max|x| / 127:
+//     x / u = a1 + a2/254 + a3/254^2 + e,   |a_s| <= 127,  |e| <= 0.5/254^2
+// (about 24 significant bits relative to the row maximum).  A product of two
+// such rows is accumulated EXACTLY in s32 on the tensor cores (kind::i8):
+//     acc0 = sum a1 b1,  acc1 = sum a1 b2 + a2 b1,  acc2 = sum a1 b3 + a2 b2 + a3 b1
+// and the epilogue forms u_x u_y (acc0 + acc1/254 + acc2/254^2) in fp32.  The
+// dropped slice products (2,3), (3,2), (3,3) are O(254^-3) of the leading term.
+//
+// HBM layouts:
+//   * "Q-layout" of an operand X[rows][K] (int8 slices): K-blocks of 64, rows
+//     of 64 bytes; byte (s, kb, row, k) at
+//         ((s * nkb + kb) * rows_total + row) * 64 + ((c ^ ((row >> 1) & 3)) * 16) + k % 16,
+//     c = (k % 64) / 16 -- the UMMA K-major SWIZZLE_64B image, so a box of
+//     `rows` x 64 B x 3 slices is one TMA tensor copy into a pipeline stage.
+//       VQ  = V   (rows = monomial i, K = square k)      fwd A and B operands
+//       VTQ = V^T (rows = square k,   K = monomial j)    bwd B operand
+//       RQ  = R   (rows = monomial i, K = monomial j)    bwd A operand
+//   * per-row scales u = max / 127, kept as the float bits of the row maximum:
+//     vrow[i] = max_k |V_ik|, vcol[k] = max_j |V_jk|, rrow[i] = max_j |R_ij|.
+//   * pair-rank table PT[jb][i][64] (uint32, jb = j / 64):
+//         PT[((j / 64) * Np + i) * 64 + j % 64] = rank(alpha_i + alpha_j),
+//     0xFFFFFFFF for padding (i >= N or j >= N).
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -41,31 +51,30 @@ struct Timing {
     }
 };
 
-constexpr int kBlockM = 128;   // tile rows per CTA (UMMA M = 256 per CTA pair)
-constexpr int kBlockN = 256;   // tile cols  (UMMA N)
-constexpr int kBlockK = 32;    // fp32-equivalent K per stage (hi+lo = 128 B rows)
-constexpr int kPad = 256;      // Np = N rounded up to kPad
-constexpr int kEpiWarps = 8;       // 4 TMEM lane quarters x 2 column halves
-constexpr int kEpiCols = kBlockN / 2;
-constexpr int kAuxWarps = 2;       // optimiser-update warps of the backward GEMM
+constexpr int kSlices = 3;        // int8 slices per operand value
+constexpr int kQK = 64;           // K-elements per Q-layout row (64 bytes, SWIZZLE_64B)
+constexpr int kPairM = 256;       // UMMA M over a CTA pair (128 rows per CTA)
+constexpr int kTileN = 160;       // UMMA N (3 s32 accumulators x 160 columns fit TMEM's 512)
+constexpr int kHalfN = kTileN / 2;  // B rows staged per CTA
+constexpr int kPad = 256;         // Np = N rounded up to kPad (R rows, PT)
+constexpr int kEpiWarps = 8;      // 4 TMEM lane quarters x 2 column halves
+constexpr int kEpiCols = kTileN / 2;  // 80 output columns per epilogue thread
+constexpr int kAuxWarps = 2;      // optimiser-update / V^T-pack warps of the GEMMs
 constexpr int kGemmThreads = 64 + 32 * (kEpiWarps + kAuxWarps);  // producer, MMA, epilogue, aux
-// K-blocks accumulated in TMEM before the epilogue drains them into fp32
-// registers: tcgen05 fp32 accumulation truncates, so the number of in-TMEM
-// adds per value is bounded.
-constexpr int kSegKB = 16;
-// bounded K-skew between the CTAs of a GEMM (see the producer in sos_gemm.cu)
-constexpr int kSkewEpoch = 16;  // K-blocks per progress epoch
-constexpr int kSkewLag = 2;     // epochs a CTA may run ahead of the slowest
-constexpr int kSkewMaxSpin = 8192;  // bounded wait (x 256 ns): the skew bound is a locality hint, never a deadlock
+constexpr int kPtW = 64;          // pair-rank table chunk width (columns j per [jb][i] row)
+// bounded K-skew between the CTAs of a GEMM (see the producer in sos_gemmq.cu)
+constexpr int kSkewEpoch = 16;    // K-blocks (of 64) per progress epoch
+constexpr int kSkewLag = 2;       // epochs a CTA may run ahead of the slowest
+constexpr int kSkewMaxSpin = 8192;  // bounded wait (x 256 ns): a locality hint, never a deadlock
 constexpr uint32_t kInvalidRank = 0xFFFFFFFFu;
-constexpr int kMaxVars = 64;       // n + 2d <= 64
+constexpr int kMaxVars = 64;      // n + 2d <= 64
 constexpr int kMaxDeg2 = 64;
 
+// s32 accumulation stays exact while K * 3 * 127^2 < 2^31: K-blocks of 64 per
+// TMEM segment (longer K is split into segments drained into fp32 sums)
+constexpr int kSegKBMax = (int)(2147483647LL / (3LL * 127 * 127 * kQK));
+
 struct Scalars {           // device-resident per-step scalars
-    unsigned int absmax_v; // float bits of max |V|
-    unsigned int absmax_r; // float bits of max |res|
-    float s_v;             // power-of-two scale for the V split
-    float s_r;             // power-of-two scale for the R split
     double loss;           // sum res^2
     double pnorm2;         // sum p^2
 };
@@ -86,14 +95,21 @@ struct Index {
     uint32_t* d_pt;            // pair-rank table PT (Np*Np)
 };
 
-struct TileCoord { int a; int b; };  // a: 256-row block (CTA pair), b: 256-col block
+struct TileCoord { int a; int b; };  // a: 256-row block (CTA pair), b: 160-col block
 
 struct Plan {
     const Index* idx;
-    int64_t r, rK, rN;
-    uint8_t* d_vs;    // VS
-    uint8_t* d_vts;   // VTS
-    uint8_t* d_rs;    // RS
+    int64_t r;
+    int64_t rowsV;    // VQ rows_total: covers the 256-row A blocks and 160-row B blocks of N
+    int64_t nkbV;     // VQ K-blocks: ceil(r / 64)
+    int64_t rowsVT;   // VTQ rows_total: r rounded up to 160
+    int64_t nkbN;     // VTQ / RQ K-blocks: Np / 64
+    uint8_t* d_vq;    // VQ
+    uint8_t* d_vtq;   // VTQ
+    uint8_t* d_rq;    // RQ
+    unsigned* d_vrow; // max_k |V_ik| (float bits), rowsV
+    unsigned* d_vcol; // max_j |V_jk| (float bits), rowsVT
+    unsigned* d_rrow; // max_j |R_ij| (float bits), Np
     float* d_coef;    // M
     float* d_res;     // M
     float* d_m;       // Adam moments (lazy)
@@ -101,11 +117,12 @@ struct Plan {
     Scalars* d_scal;
     float* d_ring;    // per-CTA gradient tile ring of the fused backward + update
     unsigned long long* d_progress;  // [2] K-skew counters (fwd, bwd)
-    TileCoord* d_tiles2_fwd; int ntiles2_fwd;  // CTA-pair tiles (256-row blocks)
-    TileCoord* d_tiles2_bwd; int ntiles2_bwd;
-    alignas(64) uint8_t tmap_vs[128];   // CUtensorMap of VS, VTS, RS (2-SM TMA loads)
-    alignas(64) uint8_t tmap_vts[128];
-    alignas(64) uint8_t tmap_rs[128];
+    TileCoord* d_tiles_fwd; int ntiles_fwd;
+    TileCoord* d_tiles_bwd; int ntiles_bwd;
+    alignas(64) uint8_t tmap_vq_a[128];   // CUtensorMaps (3-D: 64 B x rows x slice planes)
+    alignas(64) uint8_t tmap_vq_b[128];
+    alignas(64) uint8_t tmap_vtq_b[128];
+    alignas(64) uint8_t tmap_rq_a[128];
     int opt_kind; float lr, b1, b2, eps; int64_t t; bool opt_ready;
     double stop_tol;  // sos_opt_set_stop: skip backward + update once loss <= stop_tol * |p|^2
     int64_t launches;
@@ -142,14 +159,15 @@ void launch_beta_table(const Index& ix, uint8_t* beta, cudaStream_t st);
 void launch_pair_lookup(const Index& ix, const int64_t* i, const int64_t* j, int64_t cnt, uint32_t* out,
                         cudaStream_t st);
 
-void launch_absmax_v(Plan& P, const float* V, cudaStream_t st);
-void launch_pack_v(Plan& P, const float* V, bool with_vts, cudaStream_t st);
+void launch_vmax(Plan& P, const float* V, cudaStream_t st);
+void launch_pack_vq(Plan& P, const float* V, cudaStream_t st);
+void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
-void launch_absmax_res(Plan& P, const float* res, cudaStream_t st);
-void launch_pack_r(Plan& P, const float* res, cudaStream_t st, double stop_tol);
-void launch_gemm2_fwd(Plan& P, float* coef, const float* V_for_vts, cudaStream_t st);
-void launch_gemm2_bwd(Plan& P, float* grad, cudaStream_t st);
-void launch_gemm2_bwd_update(Plan& P, float* V, cudaStream_t st);
-bool make_split_tmap(void* map, const uint8_t* base, int64_t rows_total, int64_t num_kb);
+void launch_rmax(Plan& P, const float* res, cudaStream_t st, double stop_tol);
+void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, double stop_tol);
+void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st);
+void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st);
+void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st);
+bool make_q_tmap(void* map, const uint8_t* base, int64_t rows_total, int64_t nkb, int box_rows);
 
 }  // namespace sos

@@ -10,6 +10,7 @@
 //
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o mma_power tools/mma_power.cu -lcuda
 //   ./mma_power <mode> <seconds>
+//   ./mma_power <mode> <seconds> [N]
 // modes: 0 f16 gaussian   1 f16 "lo" split residues   2 f16 zeros   3 bf16 gaussian
 //        4 s8 uniform [-127,127]   5 s8 zeros   6 e4m3 gaussian   7 s8 small [-8,8]
 #include <cuda.h>
@@ -44,7 +45,7 @@ __device__ float gauss(uint32_t k) {  // Box-Muller from two hashes
     return sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
 }
 
-__global__ void __launch_bounds__(128, 1) k_mma(int mode, long long iters, unsigned long long* out_mmas) {
+__global__ void __launch_bounds__(128, 1) k_mma(int mode, int nn, long long iters, unsigned long long* out_mmas) {
     extern __shared__ __align__(1024) uint8_t smraw[];
     uint8_t* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
     uint8_t* A = sm;              // 128 rows x 128 B
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(128, 1) k_mma(int mode, long long iters, unsig
     if (i8) idesc = (2u << 4) | (1u << 7) | (1u << 10);   // S32 <- S8 x S8
     else if (f8) idesc = (1u << 4);                        // F32 <- E4M3 x E4M3
     else idesc = (1u << 4) | ((mode == 3 ? 1u : 0u) << 7) | ((mode == 3 ? 1u : 0u) << 10);  // F32 <- F16/BF16
-    idesc |= (256u >> 3) << 17;
+    idesc |= ((uint32_t)nn >> 3) << 17;
     idesc |= (128u >> 4) << 24;
     if (tid == 0) {
         const uint32_t a0 = smem_u32(A), b0 = smem_u32(B);
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(128, 1) k_mma(int mode, long long iters, unsig
 int main(int argc, char** argv) {
     const int mode = argc > 1 ? atoi(argv[1]) : 0;
     const double seconds = argc > 2 ? atof(argv[2]) : 3.0;
+    const int nn = argc > 3 ? atoi(argv[3]) : 256;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int smem = 49152 + 1024;
@@ -166,7 +168,7 @@ int main(int argc, char** argv) {
     for (;;) {
         cudaMemset(d, 0, 8);
         cudaEventRecord(e0);
-        k_mma<<<sms, 128, smem>>>(mode, iters, d);
+        k_mma<<<sms, 128, smem>>>(mode, nn, iters, d);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
@@ -177,7 +179,7 @@ int main(int argc, char** argv) {
     iters = (long long)(iters * (seconds * 1e3 / ms));
     cudaMemset(d, 0, 8);
     cudaEventRecord(e0);
-    k_mma<<<sms, 128, smem>>>(mode, iters, d);
+    k_mma<<<sms, 128, smem>>>(mode, nn, iters, d);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
@@ -185,8 +187,8 @@ int main(int argc, char** argv) {
     cudaMemcpy(&mm, d, 8, cudaMemcpyDeviceToHost);
     const bool byte8 = mode >= 4;
     // MACs per MMA: 128 x 256 x K, K = 16 (16-bit) or 32 (8-bit)
-    const double macs = (double)mm * 128 * 256 * (byte8 ? 32 : 16);
-    printf("{\"mode\": %d, \"ms\": %.1f, \"mmas\": %llu, \"tops\": %.1f, \"mma_per_us_per_sm\": %.3f, \"err\": \"%s\"}\n",
-           mode, ms, mm, 2 * macs / (ms * 1e-3) / 1e12, mm / (ms * 1e3) / sms, cudaGetErrorString(cudaGetLastError()));
+    const double macs = (double)mm * 128 * nn * (byte8 ? 32 : 16);
+    printf("{\"N\": %d, \"mode\": %d, \"ms\": %.1f, \"mmas\": %llu, \"tops\": %.1f, \"mma_per_us_per_sm\": %.3f, \"err\": \"%s\"}\n",
+           nn, mode, ms, mm, 2 * macs / (ms * 1e-3) / 1e12, mm / (ms * 1e3) / sms, cudaGetErrorString(cudaGetLastError()));
     return 0;
 }

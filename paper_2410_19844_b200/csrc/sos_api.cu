@@ -311,8 +311,7 @@ int sos_plan_timing_read(sos_plan* pl, int kernel, double* total_ms, int64_t* la
 static int do_forward(Plan& P, const float* V, float* coef, bool with_vtq, cudaStream_t st) {
     CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
     CK(cudaMemsetAsync(coef, 0, (size_t)P.idx->M * 4, st));
-    launch_vmax(P, V, st);
-    launch_pack_vq(P, V, st);
+    launch_pack_v(P, V, st);
     launch_gemm_fwd(P, coef, with_vtq ? V : nullptr, st);
     return check_launch("forward");
 }
@@ -329,8 +328,7 @@ int sos_backward(sos_plan* pl, const float* V_dev, const float* res_dev, float* 
     CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
     launch_vmax(P, V_dev, st);
     launch_pack_vtq(P, V_dev, st);
-    launch_rmax(P, res_dev, st, 0.0);
-    launch_pack_rq(P, res_dev, st, 0.0);
+    launch_pack_r(P, res_dev, st, 0.0);
     launch_gemm_bwd(P, grad_dev, st);
     return check_launch("backward");
 }
@@ -342,8 +340,7 @@ static int do_loss_grad(Plan& P, const float* V, const float* p, double* loss, f
     float* r = res ? res : P.d_res;
     launch_residual(P, P.d_coef, p, r, st);
     if (grad) {
-        launch_rmax(P, r, st, 0.0);
-        launch_pack_rq(P, r, st, 0.0);
+        launch_pack_r(P, r, st, 0.0);
         launch_gemm_bwd(P, grad, st);
     }
     if (loss) CK(cudaMemcpyAsync(loss, &P.d_scal->loss, sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -406,8 +403,7 @@ int sos_step(sos_plan* pl, float* V_dev, const float* p_dev, double* loss_dev, v
     int rc = do_loss_grad(P, V_dev, p_dev, loss_dev, nullptr, nullptr, st, true);
     if (rc) return rc;
     P.t += 1;
-    launch_rmax(P, P.d_res, st, P.stop_tol);
-    launch_pack_rq(P, P.d_res, st, P.stop_tol);
+    launch_pack_r(P, P.d_res, st, P.stop_tol);
     launch_gemm_bwd_update(P, V_dev, st);
     return check_launch("step");
 }

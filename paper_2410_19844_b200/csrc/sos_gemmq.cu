@@ -16,7 +16,7 @@
 //     acc0 += a1 b1;  acc1 += a1 b2 + a2 b1;  acc2 += a1 b3 + a2 b2 + a3 b1.
 // s32 accumulation is exact, so the accumulators are drained once per tile (or
 // per kSegKBMax K-blocks for very long K) and combined in fp32 with the row
-// scales: value = u_i u_j (acc0 + acc1/254 + acc2/254^2).
+// scales: value = u_i u_j (acc0 + acc1/256 + acc2/65536).
 //
 // Warp roles (384 threads per CTA, 1 CTA per SM, persistent over a static tile list):
 //   warp 0      one lane issues the 2-SM TMA loads, completion on the leader's barrier
@@ -52,6 +52,7 @@ struct GemmArgs {
     int64_t r;
     unsigned long long* progress;
     int skew_epoch, skew_lag;  // bounded K-skew (K-blocks per epoch, epochs of lead)
+    int debug_nodrain;         // timing experiment only: skip the TMEM drain (wrong results)
     // kModeBwdUpdate: the optimiser step of PAPER.md:221, applied by the aux warps
     float* ring;  // per-CTA ring of 2 finished gradient tiles (128 x 160 fp32 each)
     float* V;
@@ -83,8 +84,8 @@ constexpr uint32_t kStageBytes = kABytes + kBBytes;  // 39936
 constexpr uint32_t kBarBytes = 256;
 constexpr uint32_t kAuxSmemBytes = 64 * 65 * 4;    // V tile staging of the aux warps' V^T pack
 constexpr uint32_t kSmemBytes = kStages * kStageBytes + kBarBytes + kAuxSmemBytes + 1024;
-constexpr float kInv254 = 1.f / 254.f;
-constexpr float kInv254sq = 1.f / (254.f * 254.f);
+constexpr float kInv256 = 1.f / 256.f;
+constexpr float kInv65536 = 1.f / 65536.f;
 
 // aux warps: one optimiser step on a finished 128 x 160 gradient tile
 // (coalesced: 64 threads cover consecutive columns of one row per access)
@@ -268,6 +269,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + h * kEpiCols;
 #pragma unroll
                 for (int ch = 0; ch < kEpiCols / 16; ++ch) {
+                    if (args.debug_nodrain) break;
                     uint32_t v0[16], v1[16], v2[16];
                     tmem_ld16(tq + ch * 16, v0);
                     tmem_ld16(tq + kTileN + ch * 16, v1);
@@ -275,8 +277,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     tmem_ld_wait();
 #pragma unroll
                     for (int t = 0; t < 16; ++t)
-                        sum[ch * 16 + t] += fmaf((float)(int)v2[t], kInv254sq,
-                                                 fmaf((float)(int)v1[t], kInv254, (float)(int)v0[t]));
+                        sum[ch * 16 + t] += fmaf((float)(int)v2[t], kInv65536,
+                                                 fmaf((float)(int)v1[t], kInv256, (float)(int)v0[t]));
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -423,6 +425,7 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
                            cudaStream_t st) {
     static const int epoch = env_int("SOS_SKEW_EPOCH", kSkewEpoch), lag = env_int("SOS_SKEW_LAG", kSkewLag);
     a.skew_epoch = epoch > 0 ? epoch : 1 << 30;
+    a.debug_nodrain = env_int("SOS_DEBUG_NODRAIN", 0);
     a.skew_lag = lag;
     static bool configured = false;
     if (!configured) {

@@ -2,13 +2,13 @@
 //
 // Precision scheme: every fp32 operand row x (a row of
 // V, of V^T or of R) is stored as three signed-int8 slices against a per-row
-// scale u = max|x| / 127:
-//     x / u = a1 + a2/254 + a3/254^2 + e,   |a_s| <= 127,  |e| <= 0.5/254^2
-// (about 24 significant bits relative to the row maximum).  A product of two
+// scale u = max|x| / 127 (sos_slice.cuh):
+//     x / u = a1 + a2/256 + a3/65536 + e,   |a1| <= 127, |a2|,|a3| <= 128,  |e| <= 2^-16
+// (about 23 significant bits relative to the row maximum).  A product of two
 // such rows is accumulated EXACTLY in s32 on the tensor cores (kind::i8):
 //     acc0 = sum a1 b1,  acc1 = sum a1 b2 + a2 b1,  acc2 = sum a1 b3 + a2 b2 + a3 b1
-// and the epilogue forms u_x u_y (acc0 + acc1/254 + acc2/254^2) in fp32.  The
-// dropped slice products (2,3), (3,2), (3,3) are O(254^-3) of the leading term.
+// and the epilogue forms u_x u_y (acc0 + acc1/256 + acc2/65536) in fp32.  The
+// dropped slice products (2,3), (3,2), (3,3) are O(2^-24) of the leading term.
 //
 // HBM layouts:
 //   * "Q-layout" of an operand X[rows][K] (int8 slices): K-blocks of 64, rows
@@ -70,9 +70,9 @@ constexpr uint32_t kInvalidRank = 0xFFFFFFFFu;
 constexpr int kMaxVars = 64;      // n + 2d <= 64
 constexpr int kMaxDeg2 = 64;
 
-// s32 accumulation stays exact while K * 3 * 127^2 < 2^31: K-blocks of 64 per
+// s32 accumulation stays exact while K * 3 * 128^2 < 2^31: K-blocks of 64 per
 // TMEM segment (longer K is split into segments drained into fp32 sums)
-constexpr int kSegKBMax = (int)(2147483647LL / (3LL * 127 * 127 * kQK));
+constexpr int kSegKBMax = (int)(2147483647LL / (3LL * 128 * 128 * kQK));
 
 struct Scalars {           // device-resident per-step scalars
     double loss;           // sum res^2
@@ -160,11 +160,12 @@ void launch_pair_lookup(const Index& ix, const int64_t* i, const int64_t* j, int
                         cudaStream_t st);
 
 void launch_vmax(Plan& P, const float* V, cudaStream_t st);
-void launch_pack_vq(Plan& P, const float* V, cudaStream_t st);
+void launch_pack_v(Plan& P, const float* V, cudaStream_t st);  // maxima + VQ
 void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
 void launch_rmax(Plan& P, const float* res, cudaStream_t st, double stop_tol);
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, double stop_tol);
+void launch_pack_r(Plan& P, const float* res, cudaStream_t st, double stop_tol);  // maxima + RQ
 void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st);
 void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st);
 void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st);

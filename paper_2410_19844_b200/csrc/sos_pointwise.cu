@@ -4,6 +4,8 @@
 // loss reduction.  The optimiser update of PAPER.md:221 runs inside the backward
 // GEMM (sos_gemmq.cu).  All kernels are coalesced and sized as a multiple of
 // the SM count (grid-stride).
+#include <algorithm>
+
 #include "sos_internal.cuh"
 #include "sos_slice.cuh"
 
@@ -21,66 +23,97 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ------------------------------------------------------------- V maxima ----
-// vrow[i] = max_k |V_ik|, vcol[k] = max_i |V_ik| (float bits, atomicMax on
-// non-negative floats).  Block tile: 64 rows x 128 columns; warp w owns 8 rows.
+// vrow[i] = max_k |V_ik|, vcol[k] = max_i |V_ik| in one read of V (float bits,
+// atomicMax on non-negative floats).  Block tile: 64 rows x 1024 columns,
+// thread = 4 consecutive columns (float4), 8 rows in flight per thread; row
+// maxima are warp-reduced per row and combined across the 8 warps in shared
+// memory, so a tile issues 64 + 1024 atomics.
 __global__ void __launch_bounds__(256) k_vmax(const float* __restrict__ V, int64_t N, int64_t r,
                                               unsigned* __restrict__ vrow, unsigned* __restrict__ vcol) {
-    __shared__ float scol[8][128];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t ntr = (N + 63) / 64, ntc = (r + 127) / 128;
+    __shared__ float rowred[64][8];
+    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+    const int64_t ntr = (N + 63) / 64, ntc = (r + 1023) / 1024;
+    const bool vec = (r & 3) == 0;
     for (int64_t tile = blockIdx.x; tile < ntr * ntc; tile += gridDim.x) {
-        const int64_t i0 = (tile / ntc) * 64 + w * 8, c0 = (tile % ntc) * 128;
+        const int64_t i0 = (tile / ntc) * 64, k0 = (tile % ntc) * 1024 + 4 * t;
         float cm[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-        for (int rr = 0; rr < 8; ++rr) {
-            const int64_t i = i0 + rr;
-            float m = 0.f;
-            if (i < N) {
-                float x[4];
+#pragma unroll 1
+        for (int rr0 = 0; rr0 < 64; rr0 += 8) {
+            float4 x[8];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int64_t c = c0 + lane + 32 * q;
-                    x[q] = c < r ? fabsf(__ldg(V + i * r + c)) : 0.f;
+            for (int e = 0; e < 8; ++e) {
+                const int64_t i = i0 + rr0 + e;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (i < N) {
+                    if (vec && k0 + 4 <= r) {
+                        v = __ldg(reinterpret_cast<const float4*>(V + i * r + k0));
+                    } else {
+                        if (k0 < r) v.x = __ldg(V + i * r + k0);
+                        if (k0 + 1 < r) v.y = __ldg(V + i * r + k0 + 1);
+                        if (k0 + 2 < r) v.z = __ldg(V + i * r + k0 + 2);
+                        if (k0 + 3 < r) v.w = __ldg(V + i * r + k0 + 3);
+                    }
                 }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    m = fmaxf(m, x[q]);
-                    cm[q] = fmaxf(cm[q], x[q]);
-                }
+                x[e] = v;
             }
-            m = warp_max(m);
-            if (lane == 0 && m > 0.f) atomicMax(vrow + i, __float_as_uint(m));
-        }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) scol[w][lane + 32 * q] = cm[q];
+            for (int e = 0; e < 8; ++e) {
+                const float a0 = fabsf(x[e].x), a1 = fabsf(x[e].y), a2 = fabsf(x[e].z), a3 = fabsf(x[e].w);
+                cm[0] = fmaxf(cm[0], a0);
+                cm[1] = fmaxf(cm[1], a1);
+                cm[2] = fmaxf(cm[2], a2);
+                cm[3] = fmaxf(cm[3], a3);
+                const float m = warp_max(fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
+                if (lane == 0) rowred[rr0 + e][w] = m;
+            }
+        }
         __syncthreads();
-        if (threadIdx.x < 128) {
-            float m = 0.f;
+        if (t < 64) {
+            float m = rowred[t][0];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) m = fmaxf(m, scol[k][threadIdx.x]);
-            const int64_t c = c0 + threadIdx.x;
-            if (c < r && m > 0.f) atomicMax(vcol + c, __float_as_uint(m));
+            for (int q = 1; q < 8; ++q) m = fmaxf(m, rowred[t][q]);
+            if (i0 + t < N && m > 0.f) atomicMax(vrow + i0 + t, __float_as_uint(m));
         }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (k0 + e < r && cm[e] > 0.f) atomicMax(vcol + k0 + e, __float_as_uint(cm[e]));
         __syncthreads();
     }
 }
 
 // --------------------------------------------------------------- pack VQ ----
-// thread = (row i, 16-wide K chunk); 4 consecutive threads fill one 64-byte
-// Q-row of each slice.  Rows >= N and K >= r are written as zeros.
-__global__ void __launch_bounds__(256) k_pack_vq(const float* __restrict__ V, int64_t N, int64_t r, int64_t rowsV,
+// thread = (row i, 16-wide K chunk): one 64-byte read (float4 when r % 4 == 0),
+// 4 consecutive threads fill one 64-byte Q-row of each slice.  Rows >= N and
+// K >= r are written as zeros.
+__global__ void __launch_bounds__(256, 6) k_pack_vq(const float* __restrict__ V, int64_t N, int64_t r, int64_t rowsV,
                                                  int64_t nkb, const unsigned* __restrict__ vrow,
                                                  uint8_t* __restrict__ VQ) {
     const int64_t cpr = nkb * 4;  // chunks per row
     const int64_t total = rowsV * cpr;
+    const bool vec = (r & 3) == 0;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = t / cpr, cc = t - i * cpr;
         const int64_t k0 = cc * 16;
         float x[16];
-        const float c = i < N ? slice_scale(__ldg(vrow + i)) : 0.f;
+        float c = 0.f;
+        if (i < N) {
+            c = slice_scale(__ldg(vrow + i));
+            if (vec && k0 + 16 <= r) {
+                const float4* s = reinterpret_cast<const float4*>(V + i * r + k0);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) x[e] = (i < N && k0 + e < r) ? __ldg(V + i * r + k0 + e) : 0.f;
+                for (int q = 0; q < 4; ++q) {
+                    const float4 f = __ldg(s + q);
+                    x[4 * q] = f.x; x[4 * q + 1] = f.y; x[4 * q + 2] = f.z; x[4 * q + 3] = f.w;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) x[e] = k0 + e < r ? __ldg(V + i * r + k0 + e) : 0.f;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = 0.f;
+        }
         uint4 q[3];
         slice16(x, c, q);
         store_q16(VQ, cc >> 2, i, (int)(cc & 3), nkb, rowsV, q);
@@ -184,6 +217,71 @@ __global__ void __launch_bounds__(256) k_pack_rq(const uint32_t* __restrict__ pt
     }
 }
 
+
+// ----------------------------------------------------- fused row packers ----
+// One pass per row: a block stages a whole row in shared memory (contiguous
+// loads for V, gathers through PT for R), reduces the row maximum, then slices
+// the row from shared memory -- no separate maxima pass, and each residual is
+// gathered once per step.
+__device__ __forceinline__ float block_max(float m, float* red, int nthreads) {
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    float x = red[0];
+    for (int w = 1; w < nthreads / 32; ++w) x = fmaxf(x, red[w]);
+    return x;
+}
+
+// slice the staged row (nkb * 64 floats in buf) into a Q-layout; chunk cc = 16 values
+__device__ __forceinline__ void slice_row(const float* buf, int64_t nkb, int64_t row, int64_t rows_total, float c,
+                                          uint8_t* __restrict__ Q, int nthreads) {
+    const int64_t chunks = nkb * 4;
+    for (int64_t cc = threadIdx.x; cc < chunks; cc += nthreads) {
+        const float4* s4 = reinterpret_cast<const float4*>(buf + cc * 16);
+        float x[16];
+        const int rot = threadIdx.x & 3;  // rotate the 4 float4 reads: fewer bank conflicts
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int qq = (q + rot) & 3;
+            const float4 f = s4[qq];
+            x[4 * qq] = f.x; x[4 * qq + 1] = f.y; x[4 * qq + 2] = f.z; x[4 * qq + 3] = f.w;
+        }
+        uint4 q[3];
+        slice16(x, c, q);
+        store_q16(Q, cc >> 2, row, (int)(cc & 3), nkb, rows_total, q);
+    }
+}
+
+// RQ rows with their maxima (rrow): row i of R gathered through PT once.  Lane
+// l of a warp owns column j = base + l: for a fixed row, consecutive j give
+// nearby ranks rank(alpha_i + alpha_j) in colex order, so a warp's 32 gathers
+// fall into few 32-byte sectors of res.
+constexpr int kRThreads = 512;
+__global__ void __launch_bounds__(kRThreads, 2) k_pack_r_rows(const uint32_t* __restrict__ pt,
+                                                              const float* __restrict__ res, int64_t Np,
+                                                              unsigned* __restrict__ rrow, uint8_t* __restrict__ RQ,
+                                                              const Scalars* sc, double stop_tol) {
+    if (descent_stopped(sc, stop_tol)) return;
+    extern __shared__ float buf[];  // Np floats = the row
+    __shared__ float red[kRThreads / 32];
+    const int64_t nkb = Np / kPtW;
+    for (int64_t i = blockIdx.x; i < Np; i += gridDim.x) {
+        float m = 0.f;
+        const uint32_t* prow = pt + i * kPtW;
+#pragma unroll 4
+        for (int64_t j = threadIdx.x; j < Np; j += kRThreads) {
+            const uint32_t k = __ldg(prow + (j / kPtW) * Np * kPtW + (j % kPtW));
+            const float x = k != kInvalidRank ? __ldg(res + k) : 0.f;
+            buf[j] = x;
+            m = fmaxf(m, fabsf(x));
+        }
+        m = block_max(m, red, kRThreads);
+        if (threadIdx.x == 0) rrow[i] = __float_as_uint(m);
+        slice_row(buf, nkb, i, Np, slice_scale(__float_as_uint(m)), RQ, kRThreads);
+        __syncthreads();
+    }
+}
+
 // -------------------------------------------------------------- launches ---
 static int grid_for(const Plan& P, int64_t work, int threads, int per_sm = 8) {
     int64_t b = (work + threads - 1) / threads;
@@ -198,14 +296,8 @@ void launch_vmax(Plan& P, const float* V, cudaStream_t st) {
     cudaMemsetAsync(P.d_vrow, 0, P.rowsV * sizeof(unsigned), st);
     cudaMemsetAsync(P.d_vcol, 0, P.rowsVT * sizeof(unsigned), st);
     LaunchScope ls(P, KK_ABSMAX_V, st);
-    const int64_t tiles = ((N + 63) / 64) * ((P.r + 127) / 128);
+    const int64_t tiles = ((N + 63) / 64) * ((P.r + 1023) / 1024);
     k_vmax<<<grid_for(P, tiles * 256, 256), 256, 0, st>>>(V, N, P.r, P.d_vrow, P.d_vcol);
-}
-
-void launch_pack_vq(Plan& P, const float* V, cudaStream_t st) {
-    LaunchScope ls(P, KK_PACK_V, st);
-    const int64_t work = P.rowsV * P.nkbV * 4;
-    k_pack_vq<<<grid_for(P, work, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.rowsV, P.nkbV, P.d_vrow, P.d_vq);
 }
 
 void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st) {
@@ -224,6 +316,39 @@ void launch_rmax(Plan& P, const float* res, cudaStream_t st, double stop_tol) {
     LaunchScope ls(P, KK_ABSMAX_R, st);
     k_rmax<<<grid_for(P, P.idx->Np * 32, 256), 256, 0, st>>>(P.idx->d_pt, res, P.idx->Np, P.d_rrow, P.d_scal,
                                                              stop_tol);
+}
+
+// rows whose staging buffer fits shared memory take the fused one-pass packers
+constexpr int64_t kRowSmemMax = 200 * 1024;
+
+// maxima (one read of V) + VQ (one elementwise pass)
+void launch_pack_v(Plan& P, const float* V, cudaStream_t st) {
+    launch_vmax(P, V, st);
+    LaunchScope ls(P, KK_PACK_V, st);
+    const int64_t work = P.rowsV * P.nkbV * 4;
+    k_pack_vq<<<grid_for(P, work, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.rowsV, P.nkbV, P.d_vrow, P.d_vq);
+}
+
+// row maxima + RQ: one fused gather pass per row when the row fits the staging
+// buffer, else k_rmax followed by k_pack_rq (two gather passes)
+void launch_pack_r(Plan& P, const float* res, cudaStream_t st, double stop_tol) {
+    const int64_t Np = P.idx->Np;
+    const int64_t row_bytes = Np * 4;
+    if (row_bytes > kRowSmemMax) {
+        launch_rmax(P, res, st, stop_tol);
+        launch_pack_rq(P, res, st, stop_tol);
+        return;
+    }
+    LaunchScope ls(P, KK_PACK_R, st);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_pack_r_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmemMax);
+        attr = true;
+    }
+    const int bps = row_bytes <= 100 * 1024 ? 2 : 1;
+    const unsigned blocks = (unsigned)std::min<int64_t>(Np, (int64_t)P.num_sms * bps);
+    k_pack_r_rows<<<blocks, kRThreads, (size_t)row_bytes, st>>>(P.idx->d_pt, res, Np, P.d_rrow, P.d_rq, P.d_scal,
+                                                                stop_tol);
 }
 
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, double stop_tol) {

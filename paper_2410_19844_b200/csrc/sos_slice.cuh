@@ -1,47 +1,43 @@
 // sos_slice.cuh -- the three-slice int8 representation of fp32 operand rows
-// (see sos_internal.cuh): with c = 127 / max|row| and x = value * c (|x| <= 127),
-//     a1 = rint(x),  a2 = rint(254 (x - a1)),  a3 = rint(254 (254 (x - a1) - a2)),
-// so x = a1 + a2/254 + a3/254^2 + e with |e| <= 0.5/254^2 and |a_s| <= 127.
+// (see sos_internal.cuh).  With c = 127 * 2^16 / max|row| and the fixed-point
+// value q = rint(value * c) (|q| <= 127 * 2^16 + 1), the balanced base-256
+// digits of q are the slices:
+//     a3 = int8(q mod 256),  q2 = (q + 128) >> 8,
+//     a2 = int8(q2 mod 256), a1 = (q2 + 128) >> 8,
+// so q = a1 * 2^16 + a2 * 2^8 + a3 exactly, a1 in [-127, 127], a2, a3 in
+// [-128, 127], and value = (max / 127) (a1 + a2 / 256 + a3 / 65536) up to
+// the rounding of q (<= 2^-16 in units of max / 127, i.e. 6e-8 of the row max).
 #pragma once
 #include <cstdint>
 
 namespace sos {
 
-// 127 / max for a row maximum given as float bits (0 for an all-zero row)
+// 127 * 2^16 / max for a row maximum given as float bits (0 for an all-zero row)
 __device__ __forceinline__ float slice_scale(unsigned max_bits) {
     const float m = __uint_as_float(max_bits);
-    return m > 0.f ? 127.f / m : 0.f;
+    return m > 0.f ? 8323072.f / m : 0.f;
 }
 // u = max / 127: the factor that turns slice products back into values
 __device__ __forceinline__ float slice_unit(unsigned max_bits) { return __uint_as_float(max_bits) * (1.f / 127.f); }
 
-__device__ __forceinline__ void slice1(float x, int& a1, int& a2, int& a3) {
-    const float t1 = fminf(fmaxf(rintf(x), -127.f), 127.f);
-    const float y = (x - t1) * 254.f;  // x - t1 exact; |y| <= 127
-    const float t2 = rintf(y);
-    const float t3 = rintf((y - t2) * 254.f);  // y - t2 exact
-    a1 = (int)t1;
-    a2 = (int)t2;
-    a3 = (int)t3;
-}
-
-// 16 consecutive K-values of one row (scaled by c inside) -> one 16-byte chunk per slice
+// 16 consecutive K-values of one row -> one 16-byte chunk per slice
 __device__ __forceinline__ void slice16(const float* v, float c, uint4 (&q)[3]) {
     uint32_t w[3][4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-        uint32_t b0 = 0, b1 = 0, b2 = 0;
+        int d3[4], d2[4], d1[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            int a1, a2, a3;
-            slice1(v[4 * g + e] * c, a1, a2, a3);
-            b0 |= (uint32_t)(a1 & 0xFF) << (8 * e);
-            b1 |= (uint32_t)(a2 & 0xFF) << (8 * e);
-            b2 |= (uint32_t)(a3 & 0xFF) << (8 * e);
+            const int x = __float2int_rn(v[4 * g + e] * c);
+            const int x2 = (x + 128) >> 8;
+            d3[e] = x;                 // low byte = a3
+            d2[e] = x2;                // low byte = a2
+            d1[e] = (x2 + 128) >> 8;   // a1
         }
-        w[0][g] = b0;
-        w[1][g] = b1;
-        w[2][g] = b2;
+        // gather the low bytes of four ints into one word
+        w[2][g] = __byte_perm(__byte_perm(d3[0], d3[1], 0x0040), __byte_perm(d3[2], d3[3], 0x0040), 0x5410);
+        w[1][g] = __byte_perm(__byte_perm(d2[0], d2[1], 0x0040), __byte_perm(d2[2], d2[3], 0x0040), 0x5410);
+        w[0][g] = __byte_perm(__byte_perm(d1[0], d1[1], 0x0040), __byte_perm(d1[2], d1[3], 0x0040), 0x5410);
     }
 #pragma unroll
     for (int s = 0; s < 3; ++s) q[s] = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
@@ -60,7 +56,7 @@ __device__ __forceinline__ void store_q16(uint8_t* base, int64_t kb, int64_t row
 
 // VTQ row k (a column of V), K = j (a row of V): a 64 (j) x 64 (k) tile of V is
 // transposed through shared memory; thread (k, chunk c) writes 16 j's.  Used by
-// k_pack_vtq and by the aux warps of the forward GEMM (barrier id 1).
+// k_pack_vtq and by the aux warps of the forward GEMM (named barrier 1).
 __device__ __forceinline__ void pack_vtq_tile(const float* __restrict__ V, int64_t N, int64_t r, int64_t rowsVT,
                                               int64_t nkbN, const unsigned* __restrict__ vcol,
                                               uint8_t* __restrict__ VTQ, int64_t jb, int64_t k0,

@@ -409,3 +409,75 @@ def test_descent_full_size_adam_reaches_1e8(sos, cfg_name):
     assert rel_l2(coef[betas], o.coef_sample(Vh, betas)) <= REL_TOL
     plan.close()
     ix.close()
+
+
+# ------------------------------------------------- slice-arithmetic edge cases --
+
+def test_backward_spiky_residual(sos):
+    """Per-row slice scales: one residual 1e6 x larger than the rest (the
+    x1^{2d} coefficient, reached by one pair only) must not wash out the other
+    entries of the rows that do not contain it, nor those that do."""
+    n, d, r = 6, 3, 64
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    V = si.v0(o.N, r, seed=21)
+    res = si.residual_probe(o.M, seed=22)
+    res[0] *= 1e6
+    res[o.M - 1] *= 1e6
+    g = plan.backward(torch.from_numpy(V).cuda(), torch.from_numpy(res).cuda()).cpu().numpy()
+    want = o.grad_rows(V, res, np.arange(o.N))
+    assert rel_l2(g, want) <= REL_TOL
+    # rows whose R row holds no spike keep their own relative accuracy
+    rows = np.nonzero(np.abs(want).max(axis=1) < 1e3 * np.median(np.abs(want)))[0]
+    assert rows.size > 0
+    assert rel_l2(g[rows], want[rows]) <= REL_TOL
+
+
+def test_forward_wide_dynamic_range(sos):
+    """Rows and columns of V spanning 12 orders of magnitude: every row (and
+    column) is sliced against its own maximum."""
+    n, d, r = 5, 3, 48
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    V = si.v0(o.N, r, seed=31).astype(np.float64)
+    V *= np.logspace(-6, 6, o.N)[:, None]
+    V *= np.logspace(3, -3, r)[None, :]
+    V = V.astype(np.float32)
+    coef = plan.forward(torch.from_numpy(V).cuda()).cpu().numpy()
+    assert rel_l2(coef, o.forward(V)) <= REL_TOL
+    res = si.residual_probe(o.M, seed=32)
+    g = plan.backward(torch.from_numpy(V).cuda(), torch.from_numpy(res).cuda()).cpu().numpy()
+    want = o.grad_rows(V, res, np.arange(o.N))
+    assert rel_l2(g, want) <= REL_TOL
+
+
+def test_forward_segmented_s32_accumulation(sos):
+    """K = r = 50000 > 43648: exact s32 accumulation would overflow its bound,
+    so the GEMM drains TMEM per segment into fp32 sums; all products >= 0."""
+    n, d, r = 6, 3, 50000
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    V = np.abs(si.v0(o.N, r, seed=41))
+    coef = plan.forward(torch.from_numpy(V).cuda()).cpu().numpy()
+    assert rel_l2(coef, o.forward(V)) <= REL_TOL
+
+
+def test_zero_rows_and_columns(sos):
+    """All-zero rows/columns of V and an all-zero residual: scale 0, exact zeros out."""
+    n, d, r = 4, 3, 40
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    V = si.v0(o.N, r, seed=51)
+    V[3] = 0.0
+    V[:, 7] = 0.0
+    coef = plan.forward(torch.from_numpy(V).cuda()).cpu().numpy()
+    assert rel_l2(coef, o.forward(V)) <= REL_TOL
+    g = plan.backward(torch.from_numpy(V).cuda(), torch.zeros(o.M, device="cuda")).cpu().numpy()
+    assert np.all(g == 0.0)
+    g0 = plan.backward(torch.zeros_like(torch.from_numpy(V)).cuda(),
+                       torch.from_numpy(si.residual_probe(o.M, seed=52)).cuda()).cpu().numpy()
+    assert np.all(g0 == 0.0)

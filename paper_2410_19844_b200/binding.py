@@ -159,7 +159,7 @@ class SosPlan:
     def launch_count(self) -> int:
         return int(load().sos_plan_launch_count(self._h))
 
-    KERNELS = ("absmax_v", "pack_v", "gemm_fwd", "residual", "absmax_r", "pack_r", "gemm_bwd", "update")
+    KERNELS = ("vmax", "pack_v", "gemm_fwd", "residual", "rmax", "pack_r", "gemm_bwd", "update")
 
     def timing(self, enable: bool):
         """Start (clears old records) / stop per-kernel CUDA-event timing."""

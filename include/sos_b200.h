@@ -165,9 +165,22 @@ int sos_opt_set_stop(sos_plan *plan, double rel_tol);
  * With a stopping tolerance set (sos_opt_set_stop) and met, V is left unchanged. */
 int sos_step(sos_plan *plan, float *V_dev, const float *p_dev, double *loss_dev, void *stream);
 
+/* `steps` descent steps in one call, in place on V_dev: losses_dev[t] = L(V_t)
+ * (fp64, device) before update t.  Same iteration as `steps` calls of sos_step,
+ * faster because the library owns V between the steps: the backward of step t
+ * also writes the int8 slices and the exact row / column maxima of V_{t+1}
+ * (slices scaled by 2x the row maximum of V_t; rows whose new maximum leaves
+ * [1/2, 2] of the old one are re-sliced exactly before the next forward), so
+ * the per-step maxima and slicing passes over V disappear.  Results agree with
+ * sos_step to the slice precision (~1e-7 relative), not bit for bit.  V_dev must
+ * not be modified by anyone else during the call (it is asynchronous on
+ * `stream`).  Honours sos_opt_set_lr / sos_opt_set_stop settings. */
+int sos_descend(sos_plan *plan, float *V_dev, const float *p_dev, int64_t steps, double *losses_dev,
+                void *stream);
+
 /* Host-buffer entry point: copies p_host (M) and V_host (N x r) to the device,
- * runs `steps` sos_step calls, copies V back to V_host and the per-step losses
- * (steps values, fp64) to losses_host.  Synchronous.  Uses the plan's
+ * runs sos_descend for `steps` steps, copies V back to V_host and the per-step
+ * losses (steps values, fp64) to losses_host.  Synchronous.  Uses the plan's
  * optimiser settings (sos_opt_init must have been called). */
 int sos_solve_host(sos_plan *plan, float *V_host, const float *p_host, int64_t steps,
                    double *losses_host);

@@ -56,6 +56,7 @@ SIGNATURES = {
     "sos_opt_set_lr": [_vp, ctypes.c_float],
     "sos_opt_set_stop": [_vp, ctypes.c_double],
     "sos_step": [_vp, _vp, _vp, _vp, _vp],
+    "sos_descend": [_vp, _vp, _vp, _i64, _vp, _vp],
     "sos_solve_host": [_vp, _vp, _vp, _i64, _vp],
 }
 _RESTYPES = {"sos_last_error": ctypes.c_char_p, "sos_plan_launch_count": _i64}
@@ -225,6 +226,18 @@ class SosPlan:
         loss = loss_out if loss_out is not None else torch.empty(1, dtype=torch.float64, device="cuda")
         _check(load().sos_step(self._h, _vp(V.data_ptr()), _vp(p.data_ptr()), _vp(loss.data_ptr()), _stream()))
         return loss
+
+    def descend(self, V: torch.Tensor, p: torch.Tensor, steps: int,
+                losses_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """`steps` descent steps in one call (V in place); returns the fp64 device
+        tensor of the per-step losses L(V_t)."""
+        self._V(V)
+        _dev_f32(p, "p")
+        losses = losses_out if losses_out is not None else torch.empty(max(steps, 1), dtype=torch.float64,
+                                                                          device="cuda")
+        _check(load().sos_descend(self._h, _vp(V.data_ptr()), _vp(p.data_ptr()), steps, _vp(losses.data_ptr()),
+                                  _stream()))
+        return losses[:steps]
 
     def solve_host(self, V: np.ndarray, p: np.ndarray, steps: int) -> np.ndarray:
         """Host-buffer descent (V updated in place); returns per-step losses."""

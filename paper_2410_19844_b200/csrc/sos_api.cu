@@ -214,6 +214,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         (rc = dalloc(&P.d_rq, (size_t)kSlices * P.nkbN * Np * 64)) ||
         (rc = dalloc(&P.d_vrow, (size_t)P.rowsV * 4)) || (rc = dalloc(&P.d_vcol, (size_t)P.rowsVT * 4)) ||
         (rc = dalloc(&P.d_rrow, (size_t)Np * 4)) || (rc = dalloc(&P.d_coef, (size_t)M * 4)) ||
+        (rc = dalloc(&P.d_dbuf, (size_t)(4 * P.rowsV + 2 * P.rowsVT) * 4)) ||
         (rc = dalloc(&P.d_res, (size_t)M * 4)) || (rc = dalloc(&P.d_scal, sizeof(Scalars))) ||
         (rc = dalloc(&P.d_ring, (size_t)sms * 2 * 128 * kTileN * 4)) ||
         (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) ||
@@ -230,7 +231,8 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     // zero-initialised maxima: the GEMMs read them for padding rows too
     if (cudaMemset(P.d_vrow, 0, (size_t)P.rowsV * 4) != cudaSuccess ||
         cudaMemset(P.d_vcol, 0, (size_t)P.rowsVT * 4) != cudaSuccess ||
-        cudaMemset(P.d_rrow, 0, (size_t)Np * 4) != cudaSuccess) {
+        cudaMemset(P.d_rrow, 0, (size_t)Np * 4) != cudaSuccess ||
+        cudaMemset(P.d_dbuf, 0, (size_t)(4 * P.rowsV + 2 * P.rowsVT) * 4) != cudaSuccess) {
         sos_plan_destroy(pl);
         return fail(SOS_ERR_CUDA, "workspace init");
     }
@@ -258,6 +260,7 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_vrow);
     cudaFree(P.d_vcol);
     cudaFree(P.d_rrow);
+    cudaFree(P.d_dbuf);
     cudaFree(P.d_coef);
     cudaFree(P.d_res);
     cudaFree(P.d_m);
@@ -408,6 +411,39 @@ int sos_step(sos_plan* pl, float* V_dev, const float* p_dev, double* loss_dev, v
     return check_launch("step");
 }
 
+int sos_descend(sos_plan* pl, float* V_dev, const float* p_dev, int64_t steps, double* losses_dev, void* stream) {
+    if (!pl || !V_dev || !p_dev || steps < 0 || (steps > 0 && !losses_dev)) return fail(SOS_ERR_ARG, "bad argument");
+    Plan& P = pl->P;
+    if (!P.opt_ready) return fail(SOS_ERR_ARG, "sos_opt_init not called");
+    if (steps == 0) return SOS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned* vrowx[2] = {P.d_dbuf, P.d_dbuf + P.rowsV};
+    unsigned* urow[2] = {P.d_dbuf + 2 * P.rowsV, P.d_dbuf + 3 * P.rowsV};
+    unsigned* vcol[2] = {P.d_dbuf + 4 * P.rowsV, P.d_dbuf + 4 * P.rowsV + P.rowsVT};
+    // step 0: exact maxima and slices of the caller's V
+    launch_pack_v(P, V_dev, st, vrowx[0], vcol[0]);
+    for (int64_t t = 0; t < steps; ++t) {
+        const int b = (int)(t & 1);
+        const unsigned* ucur = t == 0 ? vrowx[0] : urow[b];
+        CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
+        CK(cudaMemsetAsync(P.d_coef, 0, (size_t)P.idx->M * 4, st));
+        launch_gemm_fwd(P, P.d_coef, V_dev, st, ucur, vcol[b]);
+        launch_residual(P, P.d_coef, p_dev, P.d_res, st);
+        CK(cudaMemcpyAsync(losses_dev + t, &P.d_scal->loss, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        P.t += 1;
+        launch_pack_r(P, P.d_res, st, P.stop_tol);
+        CK(cudaMemsetAsync(vrowx[b ^ 1], 0, P.rowsV * 4, st));
+        CK(cudaMemsetAsync(vcol[b ^ 1], 0, P.rowsVT * 4, st));
+        const DescendBufs db{vrowx[b], vcol[b], vrowx[b ^ 1], vcol[b ^ 1]};
+        launch_gemm_bwd_update(P, V_dev, st, &db);
+        if (t + 1 < steps)
+            launch_descend_fixup(P, V_dev, vrowx[b], vrowx[b ^ 1], ucur, urow[b ^ 1], vcol[b], vcol[b ^ 1], st);
+        int rc = check_launch("descend");
+        if (rc) return rc;
+    }
+    return SOS_OK;
+}
+
 int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t steps, double* losses_host) {
     if (!pl || !V_host || !p_host || steps < 0 || (steps > 0 && !losses_host)) return fail(SOS_ERR_ARG, "bad argument");
     Plan& P = pl->P;
@@ -425,7 +461,7 @@ int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t ste
     if (cudaMemcpyAsync(dV, V_host, vb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
         cudaMemcpyAsync(dp, p_host, pb, cudaMemcpyHostToDevice, st) != cudaSuccess)
         rc = fail(SOS_ERR_CUDA, "H2D copy");
-    for (int64_t t = 0; !rc && t < steps; ++t) rc = sos_step(pl, dV, dp, dl + t, st);
+    if (!rc) rc = sos_descend(pl, dV, dp, steps, dl, st);
     if (!rc && (cudaMemcpyAsync(V_host, dV, vb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
                 (steps > 0 && cudaMemcpyAsync(losses_host, dl, sizeof(double) * steps, cudaMemcpyDeviceToHost, st) != cudaSuccess) ||
                 cudaStreamSynchronize(st) != cudaSuccess))

@@ -62,6 +62,14 @@ struct GemmArgs {
     float lr, b1, b2, lr_c1, inv_sqrt_c2, eps;
     const Scalars* scal;
     double stop_tol;  // sos_opt_set_stop rule (0 = off)
+    // kModeBwdUpdate inside sos_descend (vq_next != nullptr): the aux warps also
+    // write the int8 slices of the updated V (scale kHeadroom * vrow_cur) and the
+    // exact row / column maxima of the updated V for the next step
+    uint8_t* vq_next;
+    int64_t rowsV, nkbV;
+    const unsigned* vrow_cur;
+    unsigned* vrow_next;
+    unsigned* vcol_next;
     // kModeFwd with Vsrc != nullptr: the aux warps pack V^T slices meanwhile
     const float* Vsrc;
     uint8_t* vtq;
@@ -124,6 +132,106 @@ __device__ __forceinline__ void update_tile(const GemmArgs& a, const float* __re
             }
         }
     }
+}
+
+// aux warps inside sos_descend: the optimiser step on a finished 128 x 160
+// gradient tile, plus the next step's V slices and maxima.  Batches of 16 rows:
+// (A) the update itself with thread = column (coalesced, as update_tile), the
+// new values staged in shared memory, column maxima in registers, row maxima
+// warp-reduced; (B) the staged rows sliced 16 columns at a time into VQ.  The
+// slices use the scale kHeadroom * max|row of the current V|, valid while the
+// row maximum stays in [1/2, 2] of the old one (k_descend_fixup re-slices the
+// rare rows that leave that window, see sos_pointwise.cu).
+constexpr int kQRows = 16;  // rows per staged batch
+__device__ __forceinline__ void update_tile_q(const GemmArgs& a, const float* __restrict__ gt, int64_t row0,
+                                              int64_t col0, int t, float* stage, unsigned* rmax_s) {
+    const int lane = t & 31, w = t >> 5;
+    float cm[3] = {0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int rb = 0; rb < 128; rb += kQRows) {
+        if (row0 + rb >= a.N) break;
+        // (A) update, thread = column
+#pragma unroll 1
+        for (int rr = rb; rr < rb + kQRows; rr += 2) {
+            float gv[2][3], x[2][3], mm[2][3], vv[2][3];
+            int64_t off[2][3];
+            bool ok[2][3];
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+#pragma unroll
+                for (int e = 0; e < 3; ++e) {
+                    const int c = t + 64 * e;
+                    const int64_t i = row0 + rr + k;
+                    ok[k][e] = c < kTileN && col0 + c < a.r && i < a.N;
+                    off[k][e] = i * a.r + col0 + c;
+                    gv[k][e] = ok[k][e] ? __ldcg(gt + (rr + k) * kTileN + c) : 0.f;
+                    x[k][e] = ok[k][e] ? __ldcs(a.V + off[k][e]) : 0.f;
+                    if (a.adam) {
+                        mm[k][e] = ok[k][e] ? __ldcs(a.m + off[k][e]) : 0.f;
+                        vv[k][e] = ok[k][e] ? __ldcs(a.v + off[k][e]) : 0.f;
+                    }
+                }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                float m = 0.f;
+#pragma unroll
+                for (int e = 0; e < 3; ++e) {
+                    const int c = t + 64 * e;
+                    float xn = 0.f;
+                    if (ok[k][e]) {
+                        if (a.adam) {
+                            mm[k][e] = a.b1 * mm[k][e] + (1.f - a.b1) * gv[k][e];
+                            vv[k][e] = a.b2 * vv[k][e] + (1.f - a.b2) * gv[k][e] * gv[k][e];
+                            xn = x[k][e] - a.lr_c1 * mm[k][e] / (sqrtf(vv[k][e]) * a.inv_sqrt_c2 + a.eps);
+                            __stcs(a.m + off[k][e], mm[k][e]);
+                            __stcs(a.v + off[k][e], vv[k][e]);
+                        } else {
+                            xn = x[k][e] - a.lr * gv[k][e];
+                        }
+                        __stcs(a.V + off[k][e], xn);
+                    }
+                    if (c < kTileN) stage[(rr + k - rb) * kTileN + c] = xn;
+                    const float ax = fabsf(xn);
+                    m = fmaxf(m, ax);
+                    cm[e] = fmaxf(cm[e], ax);
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                if (lane == 0) atomicMax(rmax_s + rr + k, __float_as_uint(m));
+            }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
+        // (B) slices of the staged rows: task = (row, 16-column chunk)
+        for (int task = t; task < kQRows * (kTileN / 16); task += 32 * kAuxWarps) {
+            const int rr = task / (kTileN / 16), cq = task - rr * (kTileN / 16);
+            const int64_t i = row0 + rb + rr, k0 = col0 + 16 * cq;
+            if (i >= a.N || k0 >= a.r) continue;
+            float xs[16];
+            const float4* s4 = reinterpret_cast<const float4*>(stage + rr * kTileN + 16 * cq);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                const float4 f = s4[q4];
+                xs[4 * q4] = f.x; xs[4 * q4 + 1] = f.y; xs[4 * q4 + 2] = f.z; xs[4 * q4 + 3] = f.w;
+            }
+            const float um = kHeadroom * __uint_as_float(__ldg(a.vrow_cur + i));
+            uint4 q[3];
+            slice16(xs, slice_scale(__float_as_uint(um)), q);
+            store_q16(a.vq_next, k0 >> 6, i, (int)((k0 >> 4) & 3), a.nkbV, a.rowsV, q);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
+    }
+    // tile maxima -> global (row maxima were combined in shared memory)
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        const int c = t + 64 * e;
+        if (c < kTileN && col0 + c < a.r && cm[e] > 0.f) atomicMax(a.vcol_next + col0 + c, __float_as_uint(cm[e]));
+    }
+    for (int e = t; e < 128; e += 32 * kAuxWarps) {
+        const unsigned v = rmax_s[e];
+        if (row0 + e < a.N && v) atomicMax(a.vrow_next + row0 + e, v);
+        rmax_s[e] = 0u;  // ready for the next tile
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
 }
 
 template <int kMode>
@@ -370,8 +478,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             const TileCoord tc = args.tiles[tile];
             const int slot = it & 1;
             mbar_wait(&gready[slot], (it >> 1) & 1);
-            update_tile(args, args.ring + ((int64_t)blockIdx.x * 2 + slot) * kRingTile,
-                        (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.b * kTileN, t);
+            const float* gt = args.ring + ((int64_t)blockIdx.x * 2 + slot) * kRingTile;
+            if (args.vq_next) {
+                float* stg = reinterpret_cast<float*>(auxbuf);
+                unsigned* rmax_s = reinterpret_cast<unsigned*>(stg + kQRows * kTileN);
+                if (it == 0) {
+                    for (int e = t; e < 128; e += 32 * kAuxWarps) rmax_s[e] = 0u;
+                    asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
+                }
+                update_tile_q(args, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.b * kTileN, t, stg, rmax_s);
+            } else {
+                update_tile(args, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.b * kTileN, t);
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&gfree[slot]);
         }
@@ -448,13 +566,14 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
 
 static const CUtensorMap& tm(const uint8_t* raw) { return *reinterpret_cast<const CUtensorMap*>(raw); }
 
-void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st) {
+void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st, const unsigned* urow,
+                     const unsigned* vcol) {
     GemmArgs a{};
     a.Vsrc = V_for_vtq;
     a.vtq = P.d_vtq;
     a.rowsVT = P.rowsVT;
     a.nkbN = P.nkbN;
-    a.vcol = P.d_vcol;
+    a.vcol = vcol ? vcol : P.d_vcol;
     a.r = P.r;
     a.a_rows = P.rowsV;
     a.b_rows = P.rowsV;
@@ -462,8 +581,8 @@ void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t 
     a.seg_kb = kSegKBMax;
     a.tiles = P.d_tiles_fwd;
     a.ntiles = P.ntiles_fwd;
-    a.umaxA = P.d_vrow;
-    a.umaxB = P.d_vrow;
+    a.umaxA = urow ? urow : P.d_vrow;
+    a.umaxB = a.umaxA;
     a.N = P.idx->N;
     a.Np = P.idx->Np;
     a.pt = P.idx->d_pt;
@@ -473,7 +592,7 @@ void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t 
     launchq<kModeFwd>(P, tm(P.tmap_vq_a), tm(P.tmap_vq_b), a, st);
 }
 
-static GemmArgs bwd_args(Plan& P) {
+static GemmArgs bwd_args(Plan& P, const unsigned* vcol) {
     GemmArgs a{};
     a.a_rows = P.idx->Np;
     a.b_rows = P.rowsVT;
@@ -482,7 +601,7 @@ static GemmArgs bwd_args(Plan& P) {
     a.tiles = P.d_tiles_bwd;
     a.ntiles = P.ntiles_bwd;
     a.umaxA = P.d_rrow;
-    a.umaxB = P.d_vcol;
+    a.umaxB = vcol ? vcol : P.d_vcol;
     a.N = P.idx->N;
     a.Np = P.idx->Np;
     a.r = P.r;
@@ -492,7 +611,7 @@ static GemmArgs bwd_args(Plan& P) {
 }
 
 void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st) {
-    GemmArgs a = bwd_args(P);
+    GemmArgs a = bwd_args(P, nullptr);
     a.grad = grad;
     LaunchScope ls(P, KK_GEMM_BWD, st);
     launchq<kModeBwdStore>(P, tm(P.tmap_rq_a), tm(P.tmap_vtq_b), a, st);
@@ -501,8 +620,16 @@ void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st) {
 // backward whose finished gradient tiles are consumed in the same kernel by the
 // optimiser step (GD or Adam): the gradient never makes an HBM round trip.  The
 // GEMM reads the packed copy VTQ, never V, so updating V in place is safe.
-void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st) {
-    GemmArgs a = bwd_args(P);
+void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBufs* db) {
+    GemmArgs a = bwd_args(P, db ? db->vcol_cur : nullptr);
+    if (db) {
+        a.vq_next = P.d_vq;
+        a.rowsV = P.rowsV;
+        a.nkbV = P.nkbV;
+        a.vrow_cur = db->vrow_cur;
+        a.vrow_next = db->vrow_next;
+        a.vcol_next = db->vcol_next;
+    }
     a.ring = P.d_ring;
     a.V = V;
     a.stop_tol = P.stop_tol;

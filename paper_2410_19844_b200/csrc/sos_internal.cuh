@@ -110,6 +110,7 @@ struct Plan {
     unsigned* d_vrow; // max_k |V_ik| (float bits), rowsV
     unsigned* d_vcol; // max_j |V_jk| (float bits), rowsVT
     unsigned* d_rrow; // max_j |R_ij| (float bits), Np
+    unsigned* d_dbuf; // sos_descend: [2][rowsV] exact row maxima, [2][rowsV] used row scales, [2][rowsVT] column maxima
     float* d_coef;    // M
     float* d_res;     // M
     float* d_m;       // Adam moments (lazy)
@@ -159,16 +160,31 @@ void launch_beta_table(const Index& ix, uint8_t* beta, cudaStream_t st);
 void launch_pair_lookup(const Index& ix, const int64_t* i, const int64_t* j, int64_t cnt, uint32_t* out,
                         cudaStream_t st);
 
-void launch_vmax(Plan& P, const float* V, cudaStream_t st);
-void launch_pack_v(Plan& P, const float* V, cudaStream_t st);  // maxima + VQ
+void launch_vmax(Plan& P, const float* V, cudaStream_t st, unsigned* vrow = nullptr, unsigned* vcol = nullptr);
+void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow = nullptr,
+                   unsigned* vcol = nullptr);  // maxima + VQ
 void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
 void launch_rmax(Plan& P, const float* res, cudaStream_t st, double stop_tol);
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, double stop_tol);
 void launch_pack_r(Plan& P, const float* res, cudaStream_t st, double stop_tol);  // maxima + RQ
-void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st);
+// sos_descend: maxima buffers of the current and the next step
+struct DescendBufs {
+    const unsigned* vrow_cur;  // exact row maxima of the current V
+    const unsigned* vcol_cur;  // exact column maxima of the current V
+    unsigned* vrow_next;       // exact row maxima of the updated V (atomicMax, zeroed before)
+    unsigned* vcol_next;       // exact column maxima of the updated V
+};
+// slices written by the update use kHeadroom x the current row maximum
+constexpr float kHeadroom = 2.f;
+
+void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st, const unsigned* urow = nullptr,
+                     const unsigned* vcol = nullptr);
 void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st);
-void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st);
+void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBufs* db = nullptr);
+void launch_descend_fixup(Plan& P, const float* V, const unsigned* vrow_cur, unsigned* vrow_next,
+                          const unsigned* urow_cur, unsigned* urow_next, const unsigned* vcol_cur, unsigned* vcol_next,
+                          cudaStream_t st);
 bool make_q_tmap(void* map, const uint8_t* base, int64_t rows_total, int64_t nkb, int box_rows);
 
 }  // namespace sos

@@ -291,13 +291,15 @@ static int grid_for(const Plan& P, int64_t work, int threads, int per_sm = 8) {
     return (int)b;
 }
 
-void launch_vmax(Plan& P, const float* V, cudaStream_t st) {
+void launch_vmax(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, unsigned* vcol) {
     const int64_t N = P.idx->N;
-    cudaMemsetAsync(P.d_vrow, 0, P.rowsV * sizeof(unsigned), st);
-    cudaMemsetAsync(P.d_vcol, 0, P.rowsVT * sizeof(unsigned), st);
+    if (!vrow) vrow = P.d_vrow;
+    if (!vcol) vcol = P.d_vcol;
+    cudaMemsetAsync(vrow, 0, P.rowsV * sizeof(unsigned), st);
+    cudaMemsetAsync(vcol, 0, P.rowsVT * sizeof(unsigned), st);
     LaunchScope ls(P, KK_ABSMAX_V, st);
     const int64_t tiles = ((N + 63) / 64) * ((P.r + 1023) / 1024);
-    k_vmax<<<grid_for(P, tiles * 256, 256), 256, 0, st>>>(V, N, P.r, P.d_vrow, P.d_vcol);
+    k_vmax<<<grid_for(P, tiles * 256, 256), 256, 0, st>>>(V, N, P.r, vrow, vcol);
 }
 
 void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st) {
@@ -322,11 +324,12 @@ void launch_rmax(Plan& P, const float* res, cudaStream_t st, double stop_tol) {
 constexpr int64_t kRowSmemMax = 200 * 1024;
 
 // maxima (one read of V) + VQ (one elementwise pass)
-void launch_pack_v(Plan& P, const float* V, cudaStream_t st) {
-    launch_vmax(P, V, st);
+void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, unsigned* vcol) {
+    if (!vrow) vrow = P.d_vrow;
+    launch_vmax(P, V, st, vrow, vcol);
     LaunchScope ls(P, KK_PACK_V, st);
     const int64_t work = P.rowsV * P.nkbV * 4;
-    k_pack_vq<<<grid_for(P, work, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.rowsV, P.nkbV, P.d_vrow, P.d_vq);
+    k_pack_vq<<<grid_for(P, work, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.rowsV, P.nkbV, vrow, P.d_vq);
 }
 
 // row maxima + RQ: one fused gather pass per row when the row fits the staging
@@ -356,6 +359,65 @@ void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, double stop_tol)
     LaunchScope ls(P, KK_PACK_R, st);
     k_pack_rq<<<grid_for(P, (Np / kPtW) * Np * 4, 256), 256, 0, st>>>(P.idx->d_pt, res, Np, P.d_rrow, P.d_rq,
                                                                        P.d_scal, stop_tol);
+}
+
+
+// ------------------------------------------------------- sos_descend fixup --
+// Before the forward of step t+1: the update of step t wrote the slices of each
+// updated row with the scale kHeadroom * (row max of V_t).  They stay exact to
+// ~22 bits while the new row max lies in [u/4, u], u = kHeadroom * old max; the
+// rare rows outside (growth beyond the headroom, or a large shrink) are re-sliced
+// here from V with their exact new maximum.  urow_next receives the scale the
+// forward must use for every row.  If the stopping rule held at step t the
+// update did not run, and everything of step t carries over.
+__global__ void __launch_bounds__(256) k_descend_fixup(const float* __restrict__ V, int64_t N, int64_t r,
+                                                       int64_t rowsV, int64_t nkbV, int64_t rowsVT,
+                                                       const unsigned* __restrict__ vrow_cur,
+                                                       unsigned* __restrict__ vrow_next,
+                                                       const unsigned* __restrict__ urow_cur,
+                                                       unsigned* __restrict__ urow_next,
+                                                       const unsigned* __restrict__ vcol_cur,
+                                                       unsigned* __restrict__ vcol_next, uint8_t* __restrict__ VQ,
+                                                       const Scalars* sc, double stop_tol) {
+    if (descent_stopped(sc, stop_tol)) {
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rowsV; e += stride) {
+            vrow_next[e] = vrow_cur[e];
+            urow_next[e] = urow_cur[e];
+        }
+        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rowsVT; e += stride)
+            vcol_next[e] = vcol_cur[e];
+        return;
+    }
+    for (int64_t i = blockIdx.x; i < rowsV; i += gridDim.x) {
+        const float u = kHeadroom * __uint_as_float(vrow_cur[i]);
+        const unsigned mb = vrow_next[i];
+        const float mx = __uint_as_float(mb);
+        if (mx <= u && mx >= 0.25f * u) {
+            if (threadIdx.x == 0) urow_next[i] = __float_as_uint(u);
+            continue;
+        }
+        if (threadIdx.x == 0) urow_next[i] = mb;
+        const float c = slice_scale(mb);
+        for (int64_t cc = threadIdx.x; cc < nkbV * 4; cc += blockDim.x) {
+            const int64_t k0 = cc * 16;
+            float x[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = (i < N && k0 + e < r) ? V[i * r + k0 + e] : 0.f;
+            uint4 q[3];
+            slice16(x, c, q);
+            store_q16(VQ, cc >> 2, i, (int)(cc & 3), nkbV, rowsV, q);
+        }
+    }
+}
+
+void launch_descend_fixup(Plan& P, const float* V, const unsigned* vrow_cur, unsigned* vrow_next,
+                          const unsigned* urow_cur, unsigned* urow_next, const unsigned* vcol_cur, unsigned* vcol_next,
+                          cudaStream_t st) {
+    LaunchScope ls(P, KK_PACK_V, st);
+    k_descend_fixup<<<grid_for(P, P.rowsV * 256, 256), 256, 0, st>>>(
+        V, P.idx->N, P.r, P.rowsV, P.nkbV, P.rowsVT, vrow_cur, vrow_next, urow_cur, urow_next, vcol_cur, vcol_next,
+        P.d_vq, P.d_scal, P.stop_tol);
 }
 
 }  // namespace sos

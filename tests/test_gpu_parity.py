@@ -370,13 +370,14 @@ def test_descent_config2_adam_reaches_1e8(sos, cfg_name, lr):
     assert lo / pn <= 1e-8
 
 
-@pytest.mark.parametrize("cfg_name", ["c3_n12_2d12", si.BENCH_CONFIG])
-def test_descent_full_size_adam_reaches_1e8(sos, cfg_name):
+@pytest.mark.parametrize("cfg_name,lr", [("c3_n12_2d12", 5e-4), (si.BENCH_CONFIG, 1e-3)])
+def test_descent_full_size_adam_reaches_1e8(sos, cfg_name, lr):
     """BASELINE configs 3 (1.35M coefficients, target + eps (sum x^2)^6) and 4
-    (5.3M coefficients): Adam on the GPU reaches eps_rel <= 1e-8 (device loss,
-    fp64-accumulated).  The forward at the final V is re-checked against the
-    oracle on sampled coefficients, so the loss it reports is the oracle's up
-    to the forward's 1e-5 relative error."""
+    (5.3M coefficients): Adam through sos_descend, with the device-side stopping
+    rule at eps_rel <= 0.5e-8, reaches the target (device loss, fp64-accumulated).
+    The forward at the final V is re-checked against the oracle on sampled
+    coefficients, so the loss it reports is the oracle's up to the forward's
+    relative error."""
     c = si.CONFIGS[cfg_name]
     ix = sos.SosIndex(c.n, c.d)
     W = torch.from_numpy(si.planted_w(ix.N, c.r_star, 0)).cuda()
@@ -391,22 +392,23 @@ def test_descent_full_size_adam_reaches_1e8(sos, cfg_name):
     pn = float(torch.dot(p.double(), p.double()).item())
     V = torch.from_numpy(si.v0(ix.N, c.r, 0)).cuda()
     plan = sos.SosPlan(ix, c.r)
-    plan.opt_init("adam", 1e-3)
+    plan.opt_init("adam", lr)
     plan.set_stop(0.5e-8)
-    steps = 1500
-    losses = torch.empty(steps, dtype=torch.float64, device="cuda")
-    for t in range(steps):
-        plan.step(V, p, losses[t:t + 1])
-        if t % 100 == 99 and losses[t].item() <= 0.5e-8 * pn:
+    hist = []
+    for _ in range(10):
+        hist.append(plan.descend(V, p, 100).cpu().numpy() / pn)
+        if hist[-1].min() <= 0.5e-8:
             break
-    hist = losses[:t + 1].cpu().numpy() / pn
-    assert np.any(hist <= 0.5e-8), f"min eps_rel {hist.min():.3e} after {t + 1} steps"
+    hist = np.concatenate(hist)
+    assert np.any(hist <= 0.5e-8), f"min eps_rel {hist.min():.3e} after {hist.size} steps"
     print(f"{cfg_name}: eps_rel <= 0.5e-8 at step {int(np.argmax(hist <= 0.5e-8))}")
     o = oracle(c.n, c.d)
     coef = plan.forward(V).cpu().numpy()
     betas = np.concatenate([np.arange(4), np.random.default_rng(2).integers(0, o.M, 28)])
     Vh = V.cpu().numpy()
     assert rel_l2(coef[betas], o.coef_sample(Vh, betas)) <= REL_TOL
+    loss, _, _ = plan.loss_grad(V, p, want_grad=False)
+    assert loss.item() / pn <= 1e-8
     plan.close()
     ix.close()
 
@@ -481,3 +483,65 @@ def test_zero_rows_and_columns(sos):
     g0 = plan.backward(torch.zeros_like(torch.from_numpy(V)).cuda(),
                        torch.from_numpy(si.residual_probe(o.M, seed=52)).cuda()).cpu().numpy()
     assert np.all(g0 == 0.0)
+
+
+# -------------------------------------------------------------- sos_descend --
+
+@pytest.mark.parametrize("kind,lr", [("adam", 1e-3), ("gd", 5e-3)])
+def test_descend_matches_steps(sos, kind, lr):
+    """sos_descend (slices of V_{t+1} written by the update of step t) follows
+    the same iteration as repeated sos_step calls, to the slice precision.
+    Row 5 of V0 is zero, so its first update leaves the headroom window and is
+    re-sliced by the fixup kernel."""
+    c = si.CONFIGS["c1_n8_2d8"]
+    o = oracle(c.n, c.d)
+    ix = sos.SosIndex(c.n, c.d)
+    plan = sos.SosPlan(ix, c.r)
+    p = torch.from_numpy(o.forward(si.planted_w(o.N, c.r_star, 0)).astype(np.float32)).cuda()
+    V0 = si.v0(o.N, c.r, 0)
+    V0[5] = 0.0
+    steps = 30
+    plan.opt_init(kind, lr)
+    Vs = torch.from_numpy(V0.copy()).cuda()
+    ls = torch.empty(steps, dtype=torch.float64, device="cuda")
+    for t in range(steps):
+        plan.step(Vs, p, ls[t:t + 1])
+    plan.opt_init(kind, lr)
+    Vd = torch.from_numpy(V0.copy()).cuda()
+    ld = plan.descend(Vd, p, steps)
+    torch.cuda.synchronize()
+    dv_s = Vs.cpu().numpy() - V0
+    dv_d = Vd.cpu().numpy() - V0
+    assert rel_l2(dv_d, dv_s) <= 1e-4
+    assert np.allclose(ld.cpu().numpy(), ls.cpu().numpy(), rtol=1e-4)
+    # and the final V's loss, by the oracle, matches the device loss curve's trend
+    lo, _, _, _ = o.loss_grad(Vd.cpu().numpy(), p.cpu().numpy(), want_grad=False)
+    assert lo < ld[0].item()
+
+
+def test_descend_reaches_1e8_config2_and_stops(sos):
+    """Config 2 through sos_descend with the device-side stopping rule: the
+    iteration freezes at the first V with eps_rel <= 0.5e-8, checked by the
+    fp64 oracle."""
+    c = si.CONFIGS["c2_n10_2d10"]
+    o = oracle(c.n, c.d)
+    ix = sos.SosIndex(c.n, c.d)
+    plan = sos.SosPlan(ix, c.r)
+    pf = o.forward(si.planted_w(o.N, c.r_star, 0)).astype(np.float32)
+    p = torch.from_numpy(pf).cuda()
+    pn = float(np.dot(pf.astype(np.float64), pf))
+    V = torch.from_numpy(si.v0(o.N, c.r, 0)).cuda()
+    plan.opt_init("adam", 1e-3)
+    plan.set_stop(0.5e-8)
+    losses = plan.descend(V, p, 600).cpu().numpy() / pn
+    hit = np.nonzero(losses <= 0.5e-8)[0]
+    assert hit.size > 0
+    # frozen after the stop (the loss repeats up to the order of the forward's
+    # fp32 atomic reductions), and V does not move in further calls
+    assert np.allclose(losses[hit[0]:], losses[hit[0]], rtol=1e-4)
+    frozen = V.clone()
+    plan.descend(V, p, 5)
+    assert torch.equal(frozen, V)
+    lo, _, _, _ = o.loss_grad(V.cpu().numpy(), pf, want_grad=False)
+    print(f"descend config2: stop at step {hit[0]}, oracle eps_rel {lo / pn:.3e}")
+    assert lo / pn <= 1e-8

@@ -52,7 +52,6 @@ struct GemmArgs {
     int64_t r;
     unsigned long long* progress;
     int skew_epoch, skew_lag;  // bounded K-skew (K-blocks per epoch, epochs of lead)
-    int debug_nodrain;         // timing experiment only: skip the TMEM drain (wrong results)
     // kModeBwdUpdate: the optimiser step of PAPER.md:221, applied by the aux warps
     float* ring;  // per-CTA ring of 2 finished gradient tiles (128 x 160 fp32 each)
     float* V;
@@ -377,7 +376,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + h * kEpiCols;
 #pragma unroll
                 for (int ch = 0; ch < kEpiCols / 16; ++ch) {
-                    if (args.debug_nodrain) break;
                     uint32_t v0[16], v1[16], v2[16];
                     tmem_ld16(tq + ch * 16, v0);
                     tmem_ld16(tq + kTileN + ch * 16, v1);
@@ -543,7 +541,6 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
                            cudaStream_t st) {
     static const int epoch = env_int("SOS_SKEW_EPOCH", kSkewEpoch), lag = env_int("SOS_SKEW_LAG", kSkewLag);
     a.skew_epoch = epoch > 0 ? epoch : 1 << 30;
-    a.debug_nodrain = env_int("SOS_DEBUG_NODRAIN", 0);
     a.skew_lag = lag;
     static bool configured = false;
     if (!configured) {

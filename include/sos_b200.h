@@ -59,7 +59,7 @@ int sos_version(void);
  * the colex-ordered exponent table of the N degree-d monomials, and the table
  * rank(alpha_i + alpha_j) in the degree-2d basis for every ordered pair (i,j),
  * computed by the combinatorial number system.  Synchronous.
- * Limits: 1 <= n, 1 <= d, n + 2d <= 64, M < 2^32 - 1, N <= 65536.
+ * Limits: 1 <= n, 1 <= d <= 32, n + 2d <= 255, M < 2^32 - 1, N <= 65536.
  * Device memory: about 4*Np^2 bytes (Np = N rounded up to 256). */
 int sos_build_index(int n, int d, sos_index **out);
 int sos_index_destroy(sos_index *idx);

@@ -89,7 +89,8 @@ int sos_version(void) { return 1; }
 int sos_build_index(int n, int d, sos_index** out) {
     if (!out) return fail(SOS_ERR_ARG, "out is NULL");
     *out = nullptr;
-    if (n < 1 || d < 1 || n + 2 * d > kMaxVars) return fail(SOS_ERR_ARG, "need n>=1, d>=1, n+2d<=%d", kMaxVars);
+    if (n < 1 || d < 1 || 2 * d > kMaxDeg2 || n + 2 * d > kMaxVars)
+        return fail(SOS_ERR_ARG, "need n>=1, 1<=d<=%d, n+2d<=%d", kMaxDeg2 / 2, kMaxVars);
     const uint64_t N = binom_u64(n + d - 1, d), M = binom_u64(n + 2 * d - 1, 2 * d);
     if (N > 65536) return fail(SOS_ERR_ARG, "N=%llu > 65536", (unsigned long long)N);
     if (M >= 0xFFFFFFFFull) return fail(SOS_ERR_ARG, "M=%llu does not fit uint32 ranks", (unsigned long long)M);

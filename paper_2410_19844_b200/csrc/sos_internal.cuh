@@ -67,7 +67,7 @@ constexpr int kSkewEpoch = 16;    // K-blocks (of 64) per progress epoch
 constexpr int kSkewLag = 2;       // epochs a CTA may run ahead of the slowest
 constexpr int kSkewMaxSpin = 8192;  // bounded wait (x 256 ns): a locality hint, never a deadlock
 constexpr uint32_t kInvalidRank = 0xFFFFFFFFu;
-constexpr int kMaxVars = 64;      // n + 2d <= 64
+constexpr int kMaxVars = 255;     // n + 2d <= 255 (variable indices are uint8)
 constexpr int kMaxDeg2 = 64;
 
 // s32 accumulation stays exact while K * 3 * 128^2 < 2^31: K-blocks of 64 per

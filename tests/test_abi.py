@@ -56,7 +56,11 @@ def test_argument_errors_are_reported(lib):
     h = ctypes.c_void_p()
     lib.sos_build_index.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
     assert lib.sos_build_index(0, 3, ctypes.byref(h)) == 1   # SOS_ERR_ARG
-    assert lib.sos_build_index(60, 5, ctypes.byref(h)) == 1  # n + 2d > 64
+    assert lib.sos_build_index(250, 5, ctypes.byref(h)) == 1  # n + 2d > 255
+    assert lib.sos_build_index(2, 40, ctypes.byref(h)) == 1   # d > 32
+    assert lib.sos_build_index(60, 5, ctypes.byref(h)) == 1   # N = C(64, 5) > 65536
+    lib.sos_descend.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int64] + [ctypes.c_void_p] * 2
+    assert lib.sos_descend(None, None, None, 1, None, None) == 1
     lib.sos_forward.argtypes = [ctypes.c_void_p] * 4
     assert lib.sos_forward(None, None, None, None) == 1
 

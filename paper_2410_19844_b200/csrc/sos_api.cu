@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cstddef>
 #include <vector>
 
 #include "../../include/sos_b200.h"
@@ -216,6 +217,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         (rc = dalloc(&P.d_vrow, (size_t)P.rowsV * 4)) || (rc = dalloc(&P.d_vcol, (size_t)P.rowsVT * 4)) ||
         (rc = dalloc(&P.d_rrow, (size_t)Np * 4)) || (rc = dalloc(&P.d_coef, (size_t)M * 4)) ||
         (rc = dalloc(&P.d_dbuf, (size_t)(4 * P.rowsV + 2 * P.rowsVT) * 4)) ||
+        (rc = dalloc(&P.d_opt, sizeof(DevOpt))) ||
         (rc = dalloc(&P.d_res, (size_t)M * 4)) || (rc = dalloc(&P.d_scal, sizeof(Scalars))) ||
         (rc = dalloc(&P.d_ring, (size_t)sms * 2 * 128 * kTileN * 4)) ||
         (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) ||
@@ -233,7 +235,8 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     if (cudaMemset(P.d_vrow, 0, (size_t)P.rowsV * 4) != cudaSuccess ||
         cudaMemset(P.d_vcol, 0, (size_t)P.rowsVT * 4) != cudaSuccess ||
         cudaMemset(P.d_rrow, 0, (size_t)Np * 4) != cudaSuccess ||
-        cudaMemset(P.d_dbuf, 0, (size_t)(4 * P.rowsV + 2 * P.rowsVT) * 4) != cudaSuccess) {
+        cudaMemset(P.d_dbuf, 0, (size_t)(4 * P.rowsV + 2 * P.rowsVT) * 4) != cudaSuccess ||
+        cudaMemset(P.d_opt, 0, sizeof(DevOpt)) != cudaSuccess) {
         sos_plan_destroy(pl);
         return fail(SOS_ERR_CUDA, "workspace init");
     }
@@ -262,6 +265,8 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_vcol);
     cudaFree(P.d_rrow);
     cudaFree(P.d_dbuf);
+    cudaFree(P.d_opt);
+    if (P.gexec) cudaGraphExecDestroy(P.gexec);
     cudaFree(P.d_coef);
     cudaFree(P.d_res);
     cudaFree(P.d_m);
@@ -332,7 +337,7 @@ int sos_backward(sos_plan* pl, const float* V_dev, const float* res_dev, float* 
     CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
     launch_vmax(P, V_dev, st);
     launch_pack_vtq(P, V_dev, st);
-    launch_pack_r(P, res_dev, st, 0.0);
+    launch_pack_r(P, res_dev, st, 0);
     launch_gemm_bwd(P, grad_dev, st);
     return check_launch("backward");
 }
@@ -344,7 +349,7 @@ static int do_loss_grad(Plan& P, const float* V, const float* p, double* loss, f
     float* r = res ? res : P.d_res;
     launch_residual(P, P.d_coef, p, r, st);
     if (grad) {
-        launch_pack_r(P, r, st, 0.0);
+        launch_pack_r(P, r, st, 0);
         launch_gemm_bwd(P, grad, st);
     }
     if (loss) CK(cudaMemcpyAsync(loss, &P.d_scal->loss, sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -367,8 +372,11 @@ int sos_opt_init(sos_plan* pl, const sos_opt_params* prm, void* stream) {
     P.b1 = prm->beta1;
     P.b2 = prm->beta2;
     P.eps = prm->eps;
-    P.t = 0;
     P.stop_tol = 0.0;
+    if (P.gexec) {  // the captured steps bake in the optimiser kind and moment buffers
+        cudaGraphExecDestroy(P.gexec);
+        P.gexec = nullptr;
+    }
     if (prm->kind == SOS_OPT_ADAM) {
         if (!(prm->beta1 >= 0.f && prm->beta1 < 1.f && prm->beta2 >= 0.f && prm->beta2 < 1.f))
             return fail(SOS_ERR_ARG, "betas must be in [0,1)");
@@ -378,7 +386,17 @@ int sos_opt_init(sos_plan* pl, const sos_opt_params* prm, void* stream) {
         CK(cudaMemsetAsync(P.d_m, 0, bytes, (cudaStream_t)stream));
         CK(cudaMemsetAsync(P.d_v, 0, bytes, (cudaStream_t)stream));
     }
+    CK(cudaMemsetAsync(P.d_opt, 0, sizeof(DevOpt), (cudaStream_t)stream));  // t = 0
     P.opt_ready = true;
+    return SOS_OK;
+}
+
+// parameters of the optimiser as set on the host -> DevOpt (stream-ordered;
+// t and loss_idx stay device-managed)
+static int upload_opt(Plan& P, cudaStream_t st) {
+    struct { float lr, b1, b2, eps; double stop_tol; } h{P.lr, P.b1, P.b2, P.eps, P.stop_tol};
+    static_assert(sizeof(h) == offsetof(DevOpt, t), "DevOpt host-uploaded prefix");
+    CK(cudaMemcpyAsync(P.d_opt, &h, sizeof(h), cudaMemcpyHostToDevice, st));
     return SOS_OK;
 }
 
@@ -404,12 +422,47 @@ int sos_step(sos_plan* pl, float* V_dev, const float* p_dev, double* loss_dev, v
     cudaStream_t st = (cudaStream_t)stream;
     // loss and residual of the current V, then the backward GEMM whose aux
     // warps apply the optimiser update to V in place, tile by tile
-    int rc = do_loss_grad(P, V_dev, p_dev, loss_dev, nullptr, nullptr, st, true);
+    int rc = upload_opt(P, st);
     if (rc) return rc;
-    P.t += 1;
-    launch_pack_r(P, P.d_res, st, P.stop_tol);
+    rc = do_loss_grad(P, V_dev, p_dev, loss_dev, nullptr, nullptr, st, true);
+    if (rc) return rc;
+    launch_step_begin(P, nullptr, st);
+    launch_pack_r(P, P.d_res, st, 1);
     launch_gemm_bwd_update(P, V_dev, st);
     return check_launch("step");
+}
+
+// one descent step of sos_descend on buffer parity b (see the header)
+struct DescendPtrs {
+    unsigned* vrowx[2];  // exact row maxima of V (current / next)
+    unsigned* urow[2];   // row scales the slices in VQ were written with
+    unsigned* vcol[2];   // exact column maxima of V
+};
+static DescendPtrs descend_ptrs(Plan& P) {
+    DescendPtrs d;
+    d.vrowx[0] = P.d_dbuf;
+    d.vrowx[1] = P.d_dbuf + P.rowsV;
+    d.urow[0] = P.d_dbuf + 2 * P.rowsV;
+    d.urow[1] = P.d_dbuf + 3 * P.rowsV;
+    d.vcol[0] = P.d_dbuf + 4 * P.rowsV;
+    d.vcol[1] = P.d_dbuf + 4 * P.rowsV + P.rowsVT;
+    return d;
+}
+
+static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const float* p, double* losses,
+                        cudaStream_t st) {
+    CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
+    CK(cudaMemsetAsync(P.d_coef, 0, (size_t)P.idx->M * 4, st));
+    launch_gemm_fwd(P, P.d_coef, V, st, d.urow[b], d.vcol[b]);
+    launch_residual(P, P.d_coef, p, P.d_res, st);
+    launch_step_begin(P, losses, st);  // t += 1, losses[k] = L(V_t)
+    launch_pack_r(P, P.d_res, st, 1);
+    CK(cudaMemsetAsync(d.vrowx[b ^ 1], 0, P.rowsV * 4, st));
+    CK(cudaMemsetAsync(d.vcol[b ^ 1], 0, P.rowsVT * 4, st));
+    const DescendBufs db{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1]};
+    launch_gemm_bwd_update(P, V, st, &db);
+    launch_descend_fixup(P, V, d.vrowx[b], d.vrowx[b ^ 1], d.urow[b], d.urow[b ^ 1], d.vcol[b], d.vcol[b ^ 1], st);
+    return check_launch("descend step");
 }
 
 int sos_descend(sos_plan* pl, float* V_dev, const float* p_dev, int64_t steps, double* losses_dev, void* stream) {
@@ -418,30 +471,51 @@ int sos_descend(sos_plan* pl, float* V_dev, const float* p_dev, int64_t steps, d
     if (!P.opt_ready) return fail(SOS_ERR_ARG, "sos_opt_init not called");
     if (steps == 0) return SOS_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    unsigned* vrowx[2] = {P.d_dbuf, P.d_dbuf + P.rowsV};
-    unsigned* urow[2] = {P.d_dbuf + 2 * P.rowsV, P.d_dbuf + 3 * P.rowsV};
-    unsigned* vcol[2] = {P.d_dbuf + 4 * P.rowsV, P.d_dbuf + 4 * P.rowsV + P.rowsVT};
-    // step 0: exact maxima and slices of the caller's V
-    launch_pack_v(P, V_dev, st, vrowx[0], vcol[0]);
-    for (int64_t t = 0; t < steps; ++t) {
-        const int b = (int)(t & 1);
-        const unsigned* ucur = t == 0 ? vrowx[0] : urow[b];
-        CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
-        CK(cudaMemsetAsync(P.d_coef, 0, (size_t)P.idx->M * 4, st));
-        launch_gemm_fwd(P, P.d_coef, V_dev, st, ucur, vcol[b]);
-        launch_residual(P, P.d_coef, p_dev, P.d_res, st);
-        CK(cudaMemcpyAsync(losses_dev + t, &P.d_scal->loss, sizeof(double), cudaMemcpyDeviceToDevice, st));
-        P.t += 1;
-        launch_pack_r(P, P.d_res, st, P.stop_tol);
-        CK(cudaMemsetAsync(vrowx[b ^ 1], 0, P.rowsV * 4, st));
-        CK(cudaMemsetAsync(vcol[b ^ 1], 0, P.rowsVT * 4, st));
-        const DescendBufs db{vrowx[b], vcol[b], vrowx[b ^ 1], vcol[b ^ 1]};
-        launch_gemm_bwd_update(P, V_dev, st, &db);
-        if (t + 1 < steps)
-            launch_descend_fixup(P, V_dev, vrowx[b], vrowx[b ^ 1], ucur, urow[b ^ 1], vcol[b], vcol[b ^ 1], st);
-        int rc = check_launch("descend");
-        if (rc) return rc;
+    const DescendPtrs d = descend_ptrs(P);
+    int rc = upload_opt(P, st);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(&P.d_opt->loss_idx, 0, sizeof(long long), st));
+    // step 0 starts from the exact maxima and slices of the caller's V
+    launch_pack_v(P, V_dev, st, d.vrowx[0], d.vcol[0]);
+    CK(cudaMemcpyAsync(d.urow[0], d.vrowx[0], P.rowsV * 4, cudaMemcpyDeviceToDevice, st));
+    if ((rc = descend_step(P, d, 0, V_dev, p_dev, losses_dev, st))) return rc;
+    int64_t left = steps - 1;
+    const bool timing = P.timing && P.timing->on;  // per-kernel events need plain launches
+    if (left >= 2 && !timing) {
+        // steps 1, 2 (parities 1, 0) captured once as a graph, replayed for every pair
+        const void* key[3] = {V_dev, p_dev, losses_dev};
+        if (!P.gexec || memcmp(key, P.gkey, sizeof(key)) != 0) {
+            if (P.gexec) {
+                cudaGraphExecDestroy(P.gexec);
+                P.gexec = nullptr;
+            }
+            cudaStream_t cs;
+            CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            const int64_t l0 = P.launches;
+            cudaGraph_t graph = nullptr;
+            cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+            int rc1 = e == cudaSuccess ? descend_step(P, d, 1, V_dev, p_dev, losses_dev, cs) : SOS_ERR_CUDA;
+            int rc2 = e == cudaSuccess && !rc1 ? descend_step(P, d, 0, V_dev, p_dev, losses_dev, cs) : SOS_ERR_CUDA;
+            cudaError_t e2 = cudaStreamEndCapture(cs, &graph);
+            P.glaunches = P.launches - l0;
+            P.launches = l0;
+            cudaStreamDestroy(cs);
+            if (e != cudaSuccess || rc1 || rc2 || e2 != cudaSuccess ||
+                cudaGraphInstantiate(&P.gexec, graph, 0) != cudaSuccess) {
+                if (graph) cudaGraphDestroy(graph);
+                P.gexec = nullptr;
+                return fail(SOS_ERR_CUDA, "descend graph capture failed: %s", cudaGetErrorString(cudaGetLastError()));
+            }
+            cudaGraphDestroy(graph);
+            memcpy(P.gkey, key, sizeof(key));
+        }
+        for (; left >= 2; left -= 2) {
+            CK(cudaGraphLaunch(P.gexec, st));
+            P.launches += P.glaunches;
+        }
     }
+    for (int64_t t = steps - left; t < steps; ++t)
+        if ((rc = descend_step(P, d, (int)(t & 1), V_dev, p_dev, losses_dev, st))) return rc;
     return SOS_OK;
 }
 

@@ -58,9 +58,9 @@ struct GemmArgs {
     float* m;
     float* v;
     int adam;
-    float lr, b1, b2, lr_c1, inv_sqrt_c2, eps;
     const Scalars* scal;
-    double stop_tol;  // sos_opt_set_stop rule (0 = off)
+    const DevOpt* opt;  // optimiser parameters, step count t, stopping tolerance
+    int use_stop;       // apply the sos_opt_set_stop rule
     // kModeBwdUpdate inside sos_descend (vq_next != nullptr): the aux warps also
     // write the int8 slices of the updated V (scale kHeadroom * vrow_cur) and the
     // exact row / column maxima of the updated V for the next step
@@ -75,6 +75,11 @@ struct GemmArgs {
     int64_t rowsVT;
     int64_t nkbN;
     const unsigned* vcol;
+};
+
+// Adam / GD constants of this step, formed on the device from DevOpt
+struct OptConsts {
+    float lr, b1, b2, eps, lr_c1, inv_sqrt_c2;
 };
 
 constexpr int kModeFwd = 0;        // Gram tile -> coefficient scatter
@@ -96,7 +101,8 @@ constexpr float kInv65536 = 1.f / 65536.f;
 
 // aux warps: one optimiser step on a finished 128 x 160 gradient tile
 // (coalesced: 64 threads cover consecutive columns of one row per access)
-__device__ __forceinline__ void update_tile(const GemmArgs& a, const float* __restrict__ gt, int64_t row0,
+__device__ __forceinline__ void update_tile(const GemmArgs& a, const OptConsts& o, const float* __restrict__ gt,
+                                            int64_t row0,
                                             int64_t col0, int t) {
 #pragma unroll 1
     for (int rr = 0; rr < 128; ++rr) {
@@ -121,13 +127,13 @@ __device__ __forceinline__ void update_tile(const GemmArgs& a, const float* __re
         for (int e = 0; e < 3; ++e) {
             if (!ok[e]) continue;
             if (a.adam) {
-                mm[e] = a.b1 * mm[e] + (1.f - a.b1) * gv[e];
-                vv[e] = a.b2 * vv[e] + (1.f - a.b2) * gv[e] * gv[e];
+                mm[e] = o.b1 * mm[e] + (1.f - o.b1) * gv[e];
+                vv[e] = o.b2 * vv[e] + (1.f - o.b2) * gv[e] * gv[e];
                 a.m[off[e]] = mm[e];
                 a.v[off[e]] = vv[e];
-                a.V[off[e]] = x[e] - a.lr_c1 * mm[e] / (sqrtf(vv[e]) * a.inv_sqrt_c2 + a.eps);
+                a.V[off[e]] = x[e] - o.lr_c1 * mm[e] / (sqrtf(vv[e]) * o.inv_sqrt_c2 + o.eps);
             } else {
-                a.V[off[e]] = x[e] - a.lr * gv[e];
+                a.V[off[e]] = x[e] - o.lr * gv[e];
             }
         }
     }
@@ -142,7 +148,8 @@ __device__ __forceinline__ void update_tile(const GemmArgs& a, const float* __re
 // row maximum stays in [1/2, 2] of the old one (k_descend_fixup re-slices the
 // rare rows that leave that window, see sos_pointwise.cu).
 constexpr int kQRows = 16;  // rows per staged batch
-__device__ __forceinline__ void update_tile_q(const GemmArgs& a, const float* __restrict__ gt, int64_t row0,
+__device__ __forceinline__ void update_tile_q(const GemmArgs& a, const OptConsts& o, const float* __restrict__ gt,
+                                              int64_t row0,
                                               int64_t col0, int t, float* stage, unsigned* rmax_s) {
     const int lane = t & 31, w = t >> 5;
     float cm[3] = {0.f, 0.f, 0.f};
@@ -179,13 +186,13 @@ __device__ __forceinline__ void update_tile_q(const GemmArgs& a, const float* __
                     float xn = 0.f;
                     if (ok[k][e]) {
                         if (a.adam) {
-                            mm[k][e] = a.b1 * mm[k][e] + (1.f - a.b1) * gv[k][e];
-                            vv[k][e] = a.b2 * vv[k][e] + (1.f - a.b2) * gv[k][e] * gv[k][e];
-                            xn = x[k][e] - a.lr_c1 * mm[k][e] / (sqrtf(vv[k][e]) * a.inv_sqrt_c2 + a.eps);
+                            mm[k][e] = o.b1 * mm[k][e] + (1.f - o.b1) * gv[k][e];
+                            vv[k][e] = o.b2 * vv[k][e] + (1.f - o.b2) * gv[k][e] * gv[k][e];
+                            xn = x[k][e] - o.lr_c1 * mm[k][e] / (sqrtf(vv[k][e]) * o.inv_sqrt_c2 + o.eps);
                             __stcs(a.m + off[k][e], mm[k][e]);
                             __stcs(a.v + off[k][e], vv[k][e]);
                         } else {
-                            xn = x[k][e] - a.lr * gv[k][e];
+                            xn = x[k][e] - o.lr * gv[k][e];
                         }
                         __stcs(a.V + off[k][e], xn);
                     }
@@ -239,7 +246,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     constexpr bool kFwd = kMode == kModeFwd;
     // converged (sos_opt_set_stop): the whole grid leaves before any barrier,
     // TMEM or cluster work, so V and the optimiser state stay as they are
-    if (kMode == kModeBwdUpdate && descent_stopped(args.scal, args.stop_tol)) return;
+    if (kMode == kModeBwdUpdate && descent_stopped(args.scal, args.opt, args.use_stop)) return;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
@@ -471,6 +478,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         // ----------------------------------------------------------- aux --
         // optimiser step on tile t while the tensor cores work on tile t+1
         const int t = threadIdx.x - 32 * (2 + kEpiWarps);  // 0..63
+        OptConsts oc;
+        {
+            const DevOpt o = *args.opt;
+            oc.lr = o.lr;
+            oc.b1 = o.b1;
+            oc.b2 = o.b2;
+            oc.eps = o.eps;
+            const double c1 = 1.0 - pow((double)o.b1, (double)o.t);
+            const double c2 = 1.0 - pow((double)o.b2, (double)o.t);
+            oc.lr_c1 = (float)((double)o.lr / c1);
+            oc.inv_sqrt_c2 = (float)(1.0 / sqrt(c2));
+        }
         int it = 0;
         for (int tile = cid; tile < args.ntiles; tile += ncl, ++it) {
             const TileCoord tc = args.tiles[tile];
@@ -484,9 +503,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     for (int e = t; e < 128; e += 32 * kAuxWarps) rmax_s[e] = 0u;
                     asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
                 }
-                update_tile_q(args, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.b * kTileN, t, stg, rmax_s);
+                update_tile_q(args, oc, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.b * kTileN, t, stg, rmax_s);
             } else {
-                update_tile(args, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.b * kTileN, t);
+                update_tile(args, oc, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.b * kTileN, t);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&gfree[slot]);
@@ -629,19 +648,12 @@ void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBuf
     }
     a.ring = P.d_ring;
     a.V = V;
-    a.stop_tol = P.stop_tol;
-    a.lr = P.lr;
+    a.opt = P.d_opt;
+    a.use_stop = 1;
     a.adam = P.opt_kind == 1;
     if (a.adam) {
-        const double c1 = 1.0 - pow((double)P.b1, (double)P.t);
-        const double c2 = 1.0 - pow((double)P.b2, (double)P.t);
         a.m = P.d_m;
         a.v = P.d_v;
-        a.b1 = P.b1;
-        a.b2 = P.b2;
-        a.eps = P.eps;
-        a.lr_c1 = (float)(P.lr / c1);
-        a.inv_sqrt_c2 = (float)(1.0 / sqrt(c2));
     }
     LaunchScope ls(P, KK_GEMM_BWD, st);
     launchq<kModeBwdUpdate>(P, tm(P.tmap_rq_a), tm(P.tmap_vtq_b), a, st);

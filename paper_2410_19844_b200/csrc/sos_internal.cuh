@@ -79,10 +79,23 @@ struct Scalars {           // device-resident per-step scalars
     double pnorm2;         // sum p^2
 };
 
+// optimiser state on the device, so that a captured step replays unchanged
+// (CUDA graphs in sos_descend): the host uploads the parameters at the start of
+// every sos_step / sos_descend call; k_step_begin advances t once per step
+struct DevOpt {
+    float lr, b1, b2, eps;  // uploaded by the host
+    double stop_tol;        // sos_opt_set_stop (0 = off), uploaded by the host
+    long long t;            // Adam step count (device-managed)
+    long long loss_idx;     // sos_descend: next entry of the caller's loss array (device-managed)
+};
+
 // the device-side stopping rule of sos_step (sos_opt_set_stop), read after
 // the residual kernel completed the loss and |p|^2 reductions
 __device__ __forceinline__ bool descent_stopped(const Scalars* sc, double tol) {
     return tol > 0.0 && sc->loss <= tol * sc->pnorm2;
+}
+__device__ __forceinline__ bool descent_stopped(const Scalars* sc, const DevOpt* opt, int use_stop) {
+    return use_stop && descent_stopped(sc, opt->stop_tol);
 }
 
 struct Index {
@@ -124,8 +137,13 @@ struct Plan {
     alignas(64) uint8_t tmap_vq_b[128];
     alignas(64) uint8_t tmap_vtq_b[128];
     alignas(64) uint8_t tmap_rq_a[128];
-    int opt_kind; float lr, b1, b2, eps; int64_t t; bool opt_ready;
+    int opt_kind; float lr, b1, b2, eps; bool opt_ready;
     double stop_tol;  // sos_opt_set_stop: skip backward + update once loss <= stop_tol * |p|^2
+    DevOpt* d_opt;    // device copy of the optimiser parameters + step counter
+    // sos_descend: a captured pair of steps, replayed with cudaGraphLaunch
+    cudaGraphExec_t gexec;
+    const void* gkey[3];   // (V, p, losses) the graph was captured for
+    int64_t glaunches;     // kernels per replay (launch accounting)
     int64_t launches;
     int num_sms;
     Timing* timing;
@@ -165,9 +183,10 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow = nu
                    unsigned* vcol = nullptr);  // maxima + VQ
 void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
-void launch_rmax(Plan& P, const float* res, cudaStream_t st, double stop_tol);
-void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, double stop_tol);
-void launch_pack_r(Plan& P, const float* res, cudaStream_t st, double stop_tol);  // maxima + RQ
+void launch_step_begin(Plan& P, double* losses, cudaStream_t st);
+void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop);
+void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop);
+void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop);  // maxima + RQ
 // sos_descend: maxima buffers of the current and the next step
 struct DescendBufs {
     const unsigned* vrow_cur;  // exact row maxima of the current V

@@ -168,8 +168,8 @@ __global__ void k_residual(const float* __restrict__ coef, const float* __restri
 // the two half-warps read the 256-byte PT rows (jb, i) and (jb+1, i).
 __global__ void __launch_bounds__(256) k_rmax(const uint32_t* __restrict__ pt, const float* __restrict__ res,
                                               int64_t Np, unsigned* __restrict__ rrow, const Scalars* sc,
-                                              double stop_tol) {
-    if (descent_stopped(sc, stop_tol)) return;
+                                              const DevOpt* opt, int use_stop) {
+    if (descent_stopped(sc, opt, use_stop)) return;
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int64_t njb = Np / kPtW;
@@ -193,8 +193,9 @@ __global__ void __launch_bounds__(256) k_rmax(const uint32_t* __restrict__ pt, c
 // PT, so reads and writes both stream).
 __global__ void __launch_bounds__(256) k_pack_rq(const uint32_t* __restrict__ pt, const float* __restrict__ res,
                                                  int64_t Np, const unsigned* __restrict__ rrow,
-                                                 uint8_t* __restrict__ RQ, const Scalars* sc, double stop_tol) {
-    if (descent_stopped(sc, stop_tol)) return;
+                                                 uint8_t* __restrict__ RQ, const Scalars* sc, const DevOpt* opt,
+                                                 int use_stop) {
+    if (descent_stopped(sc, opt, use_stop)) return;
     const int64_t nkb = Np / kPtW;
     const int64_t total = nkb * Np * 4;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -260,8 +261,8 @@ constexpr int kRThreads = 512;
 __global__ void __launch_bounds__(kRThreads, 2) k_pack_r_rows(const uint32_t* __restrict__ pt,
                                                               const float* __restrict__ res, int64_t Np,
                                                               unsigned* __restrict__ rrow, uint8_t* __restrict__ RQ,
-                                                              const Scalars* sc, double stop_tol) {
-    if (descent_stopped(sc, stop_tol)) return;
+                                                              const Scalars* sc, const DevOpt* opt, int use_stop) {
+    if (descent_stopped(sc, opt, use_stop)) return;
     extern __shared__ float buf[];  // Np floats = the row
     __shared__ float red[kRThreads / 32];
     const int64_t nkb = Np / kPtW;
@@ -314,10 +315,22 @@ void launch_residual(Plan& P, const float* coef, const float* p, float* res, cud
     k_residual<<<grid_for(P, P.idx->M, 256, 4), 256, 0, st>>>(coef, p, res, P.idx->M, P.d_scal);
 }
 
-void launch_rmax(Plan& P, const float* res, cudaStream_t st, double stop_tol) {
+void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     LaunchScope ls(P, KK_ABSMAX_R, st);
     k_rmax<<<grid_for(P, P.idx->Np * 32, 256), 256, 0, st>>>(P.idx->d_pt, res, P.idx->Np, P.d_rrow, P.d_scal,
-                                                             stop_tol);
+                                                             P.d_opt, use_stop);
+}
+
+// one thread: t += 1 (Adam bias correction of this step), and in sos_descend
+// the loss of this step into the caller's array
+__global__ void k_step_begin(DevOpt* opt, const Scalars* sc, double* losses) {
+    opt->t += 1;
+    if (losses) losses[opt->loss_idx++] = sc->loss;
+}
+
+void launch_step_begin(Plan& P, double* losses, cudaStream_t st) {
+    LaunchScope ls(P, KK_RESIDUAL, st);
+    k_step_begin<<<1, 1, 0, st>>>(P.d_opt, P.d_scal, losses);
 }
 
 // rows whose staging buffer fits shared memory take the fused one-pass packers
@@ -334,12 +347,12 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, uns
 
 // row maxima + RQ: one fused gather pass per row when the row fits the staging
 // buffer, else k_rmax followed by k_pack_rq (two gather passes)
-void launch_pack_r(Plan& P, const float* res, cudaStream_t st, double stop_tol) {
+void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     const int64_t Np = P.idx->Np;
     const int64_t row_bytes = Np * 4;
     if (row_bytes > kRowSmemMax) {
-        launch_rmax(P, res, st, stop_tol);
-        launch_pack_rq(P, res, st, stop_tol);
+        launch_rmax(P, res, st, use_stop);
+        launch_pack_rq(P, res, st, use_stop);
         return;
     }
     LaunchScope ls(P, KK_PACK_R, st);
@@ -351,14 +364,14 @@ void launch_pack_r(Plan& P, const float* res, cudaStream_t st, double stop_tol) 
     const int bps = row_bytes <= 100 * 1024 ? 2 : 1;
     const unsigned blocks = (unsigned)std::min<int64_t>(Np, (int64_t)P.num_sms * bps);
     k_pack_r_rows<<<blocks, kRThreads, (size_t)row_bytes, st>>>(P.idx->d_pt, res, Np, P.d_rrow, P.d_rq, P.d_scal,
-                                                                stop_tol);
+                                                                P.d_opt, use_stop);
 }
 
-void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, double stop_tol) {
+void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     const int64_t Np = P.idx->Np;
     LaunchScope ls(P, KK_PACK_R, st);
     k_pack_rq<<<grid_for(P, (Np / kPtW) * Np * 4, 256), 256, 0, st>>>(P.idx->d_pt, res, Np, P.d_rrow, P.d_rq,
-                                                                       P.d_scal, stop_tol);
+                                                                       P.d_scal, P.d_opt, use_stop);
 }
 
 
@@ -378,8 +391,8 @@ __global__ void __launch_bounds__(256) k_descend_fixup(const float* __restrict__
                                                        unsigned* __restrict__ urow_next,
                                                        const unsigned* __restrict__ vcol_cur,
                                                        unsigned* __restrict__ vcol_next, uint8_t* __restrict__ VQ,
-                                                       const Scalars* sc, double stop_tol) {
-    if (descent_stopped(sc, stop_tol)) {
+                                                       const Scalars* sc, const DevOpt* opt) {
+    if (descent_stopped(sc, opt, 1)) {
         const int64_t stride = (int64_t)gridDim.x * blockDim.x;
         for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rowsV; e += stride) {
             vrow_next[e] = vrow_cur[e];
@@ -417,7 +430,7 @@ void launch_descend_fixup(Plan& P, const float* V, const unsigned* vrow_cur, uns
     LaunchScope ls(P, KK_PACK_V, st);
     k_descend_fixup<<<grid_for(P, P.rowsV * 256, 256), 256, 0, st>>>(
         V, P.idx->N, P.r, P.rowsV, P.nkbV, P.rowsVT, vrow_cur, vrow_next, urow_cur, urow_next, vcol_cur, vcol_next,
-        P.d_vq, P.d_scal, P.stop_tol);
+        P.d_vq, P.d_scal, P.d_opt);
 }
 
 }  // namespace sos

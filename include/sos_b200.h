@@ -103,7 +103,7 @@ int64_t sos_plan_launch_count(const sos_plan *plan);
 #define SOS_KERNEL_RMAX 4     /* row maxima of R (only when a row exceeds the fused packer) */
 #define SOS_KERNEL_PACK_R 5   /* R gathered through the pair-rank table: row maxima + int8 slices */
 #define SOS_KERNEL_GEMM_BWD 6 /* 4 R V (tensor cores), in sos_step with the optimiser update */
-#define SOS_KERNEL_UPDATE 7   /* unused: sos_step applies the update inside GEMM_BWD */
+#define SOS_KERNEL_UPDATE 7   /* step bookkeeping (Adam t, loss record); the update itself runs inside GEMM_BWD */
 #define SOS_KERNEL_COUNT 8
 int sos_plan_timing(sos_plan *plan, int enable);
 int sos_plan_timing_read(sos_plan *plan, int kernel, double *total_ms, int64_t *launches);

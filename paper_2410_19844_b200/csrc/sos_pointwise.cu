@@ -329,7 +329,7 @@ __global__ void k_step_begin(DevOpt* opt, const Scalars* sc, double* losses) {
 }
 
 void launch_step_begin(Plan& P, double* losses, cudaStream_t st) {
-    LaunchScope ls(P, KK_RESIDUAL, st);
+    LaunchScope ls(P, KK_UPDATE, st);
     k_step_begin<<<1, 1, 0, st>>>(P.d_opt, P.d_scal, losses);
 }
 

@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "sm100_ptx.cuh"
@@ -52,6 +53,8 @@ struct GemmArgs {
     int64_t r;
     unsigned long long* progress;
     int skew_epoch, skew_lag;  // bounded K-skew (K-blocks per epoch, epochs of lead)
+    int skew_sleep;            // ns between polls of the progress counter
+    unsigned long long* dbg;   // SOS_GEMM_STATS: per-role wait cycles (instrumentation only)
     // kModeBwdUpdate: the optimiser step of PAPER.md:221, applied by the aux warps
     float* ring;  // per-CTA ring of 2 finished gradient tiles (128 x 160 fp32 each)
     float* V;
@@ -309,15 +312,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                         atomicAdd(args.progress, 1ull);
                         if (e >= args.skew_lag) {
                             const unsigned long long need = G * (unsigned long long)(e - args.skew_lag + 1);
+                            const long long c0 = clock64();
                             for (int spin = 0; spin < kSkewMaxSpin && ld_acquire_u64(args.progress) < need; ++spin)
-                                __nanosleep(256);
+                                if (args.skew_sleep) __nanosleep(args.skew_sleep);
+                            if (args.dbg) atomicAdd(args.dbg + 0, (unsigned long long)(clock64() - c0));
                         }
                     }
-                    mbar_wait(&empty[stage], phase ^ 1);
+                    {
+                        const long long c0 = clock64();
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        if (args.dbg) atomicAdd(args.dbg + 1, (unsigned long long)(clock64() - c0));
+                    }
                     uint8_t* sa = smem + stage * kStageBytes;
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
-                    tma_load_3d_2sm(sa, &tmA, &full[stage], 0, (int32_t)(kb * args.a_rows + rowA), 0);
-                    tma_load_3d_2sm(sa + kABytes, &tmB, &full[stage], 0, (int32_t)(kb * args.b_rows + rowB), 0);
+                    // the tensor maps view 4 consecutive 64-byte Q-rows as one 256-byte row
+                    tma_load_3d_2sm(sa, &tmA, &full[stage], 0, (int32_t)((kb * args.a_rows + rowA) >> 2), 0);
+                    tma_load_3d_2sm(sa + kABytes, &tmB, &full[stage], 0, (int32_t)((kb * args.b_rows + rowB) >> 2), 0);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -326,6 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer --
         if (leader && lane == 0) {
+            const long long t_start = clock64();
             constexpr uint32_t idesc = umma_idesc_s8_s32(kPairM, kTileN);
             const uint32_t d0 = tbase, d1 = tbase + kTileN, d2 = tbase + 2 * kTileN;
             int stage = 0;
@@ -334,28 +345,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int tile = cid; tile < args.ntiles; tile += ncl) {
                 for (int kb0 = 0; kb0 < args.num_kb; kb0 += args.seg_kb) {
                     const int kb1 = min(args.num_kb, kb0 + args.seg_kb);
-                    mbar_wait_cluster(tempty, acc_phase ^ 1);
+                    {
+                        const long long c0 = clock64();
+                        mbar_wait_cluster(tempty, acc_phase ^ 1);
+                        if (args.dbg) atomicAdd(args.dbg + 2, (unsigned long long)(clock64() - c0));
+                    }
                     tc_fence_after();
                     for (int kb = kb0; kb < kb1; ++kb) {
-                        mbar_wait(&full[stage], phase);
+                        {
+                            const long long c0 = clock64();
+                            mbar_wait(&full[stage], phase);
+                            if (args.dbg) atomicAdd(args.dbg + 3, (unsigned long long)(clock64() - c0));
+                        }
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(smem + stage * kStageBytes);
                         const uint32_t b0 = a0 + kABytes;
+                        // per 32-wide K step (ks) the MMAs that share an A slice run back to
+                        // back and take A from the tensor core's collector buffer after the
+                        // first read (collector::a fill / use / lastuse): A is read from
+                        // shared memory 3 times instead of 6, which relieves the shared-memory
+                        // bandwidth the MMA reads share with the TMA fills
+                        const bool first = kb == kb0;
+                        const uint64_t a1[2] = {umma_desc_sw64(a0), umma_desc_sw64(a0 + 32)};
+                        const uint64_t a2[2] = {umma_desc_sw64(a0 + kASliceBytes), umma_desc_sw64(a0 + kASliceBytes + 32)};
+                        const uint64_t a3[2] = {umma_desc_sw64(a0 + 2 * kASliceBytes),
+                                                umma_desc_sw64(a0 + 2 * kASliceBytes + 32)};
+                        const uint64_t b1[2] = {umma_desc_sw64(b0), umma_desc_sw64(b0 + 32)};
+                        const uint64_t b2[2] = {umma_desc_sw64(b0 + kBSliceBytes), umma_desc_sw64(b0 + kBSliceBytes + 32)};
+                        const uint64_t b3[2] = {umma_desc_sw64(b0 + 2 * kBSliceBytes),
+                                                umma_desc_sw64(b0 + 2 * kBSliceBytes + 32)};
 #pragma unroll
                         for (int ks = 0; ks < 2; ++ks) {
-                            const uint64_t a1 = umma_desc_sw64(a0 + ks * 32);
-                            const uint64_t a2 = umma_desc_sw64(a0 + kASliceBytes + ks * 32);
-                            const uint64_t a3 = umma_desc_sw64(a0 + 2 * kASliceBytes + ks * 32);
-                            const uint64_t b1 = umma_desc_sw64(b0 + ks * 32);
-                            const uint64_t b2 = umma_desc_sw64(b0 + kBSliceBytes + ks * 32);
-                            const uint64_t b3 = umma_desc_sw64(b0 + 2 * kBSliceBytes + ks * 32);
-                            const uint32_t acc = (kb != kb0 || ks != 0) ? 1u : 0u;
-                            umma_s8_2sm(d0, a1, b1, idesc, acc);
-                            umma_s8_2sm(d1, a1, b2, idesc, acc);
-                            umma_s8_2sm(d1, a2, b1, idesc, 1u);
-                            umma_s8_2sm(d2, a1, b3, idesc, acc);
-                            umma_s8_2sm(d2, a2, b2, idesc, 1u);
-                            umma_s8_2sm(d2, a3, b1, idesc, 1u);
+                            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+                            umma_s8_2sm<1>(d0, a1[ks], b1[ks], idesc, acc);  // a1 read once, kept
+                            umma_s8_2sm<2>(d1, a1[ks], b2[ks], idesc, acc);
+                            umma_s8_2sm<3>(d2, a1[ks], b3[ks], idesc, acc);  // a1 released
+                            umma_s8_2sm<1>(d1, a2[ks], b1[ks], idesc, 1u);   // a2 read once, kept
+                            umma_s8_2sm<3>(d2, a2[ks], b2[ks], idesc, 1u);   // a2 released
+                            umma_s8_2sm<0>(d2, a3[ks], b1[ks], idesc, 1u);
                         }
                         umma_commit_2sm(&empty[stage], 0x3);  // both CTAs' smem slots free
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -364,6 +391,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     acc_phase ^= 1;
                 }
             }
+            if (args.dbg) atomicAdd(args.dbg + 4, (unsigned long long)(clock64() - t_start));
         }
     } else if (warp < 2 + kEpiWarps) {
         // -------------------------------------------------------- epilogue --
@@ -534,15 +562,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// Q-layout viewed as a 3-D byte array [slice][kb * rows_total + row][64]; a box
-// of box_rows x 64 bytes x 3 slices is one pipeline stage of one operand.
+// Q-layout viewed as a 3-D byte array [slice][(kb * rows_total + row) / 4][256]:
+// four consecutive 64-byte Q-rows form one 256-byte TMA row (the data is
+// pre-swizzled, SWIZZLE_NONE copies bytes), so a stage of box_rows Q-rows x 3
+// slices is fetched as 3 * box_rows / 4 wide requests instead of 3 * box_rows
+// 64-byte ones -- the TMA request rate, not bandwidth, limited the 64-byte form.
 bool make_q_tmap(void* map_out, const uint8_t* base, int64_t rows_total, int64_t nkb, int box_rows) {
     CUtensorMap* map = reinterpret_cast<CUtensorMap*>(map_out);
     auto fn = encode_fn();
     if (!fn) return false;
-    cuuint64_t dims[3] = {64, (cuuint64_t)(rows_total * nkb), (cuuint64_t)kSlices};
-    cuuint64_t strides[2] = {64, (cuuint64_t)(rows_total * nkb * 64)};
-    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)kSlices};
+    if ((rows_total * nkb) % 4 || box_rows % 4) return false;
+    cuuint64_t dims[3] = {256, (cuuint64_t)(rows_total * nkb / 4), (cuuint64_t)kSlices};
+    cuuint64_t strides[2] = {256, (cuuint64_t)(rows_total * nkb * 64)};
+    cuuint32_t box[3] = {256, (cuuint32_t)(box_rows / 4), (cuuint32_t)kSlices};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -561,6 +593,13 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
     static const int epoch = env_int("SOS_SKEW_EPOCH", kSkewEpoch), lag = env_int("SOS_SKEW_LAG", kSkewLag);
     a.skew_epoch = epoch > 0 ? epoch : 1 << 30;
     a.skew_lag = lag;
+    static const int sleep_ns = env_int("SOS_SKEW_SLEEP", 256);
+    a.skew_sleep = sleep_ns;
+    static unsigned long long* dbg = nullptr;
+    if (env_int("SOS_GEMM_STATS", 0)) {
+        if (!dbg) cudaMalloc(&dbg, 8 * sizeof(unsigned long long));
+        a.dbg = dbg + (kMode == kModeFwd ? 0 : 0);
+    }
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(k_gemmq<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
@@ -577,7 +616,21 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
     cfg.stream = st;
     cfg.attrs = nullptr;
     cfg.numAttrs = 0;
-    return cudaLaunchKernelEx(&cfg, k_gemmq<kMode>, ma, mb, a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemmq<kMode>, ma, mb, a);
+    if (a.dbg) {  // SOS_GEMM_STATS: wait cycles summed over CTAs, per launch (instrumentation only)
+        unsigned long long h[8];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, a.dbg, sizeof(h), cudaMemcpyDeviceToHost);
+        cudaMemset(a.dbg, 0, sizeof(h));
+        const double mma_total = (double)h[4];
+        fprintf(stderr,
+                "gemm_stats mode=%d grid=%d | per leader CTA (Mcycles): mma_thread_total=%.2f full_wait=%.2f (%.1f%%) "
+                "tempty_wait=%.2f (%.1f%%) | per CTA producer: skew_wait=%.2f empty_wait=%.2f\n",
+                kMode, grid, mma_total / (grid / 2) / 1e6, (double)h[3] / (grid / 2) / 1e6, 100.0 * h[3] / mma_total,
+                (double)h[2] / (grid / 2) / 1e6, 100.0 * h[2] / mma_total, (double)h[0] / grid / 1e6,
+                (double)h[1] / grid / 1e6);
+    }
+    return e;
 }
 
 static const CUtensorMap& tm(const uint8_t* raw) { return *reinterpret_cast<const CUtensorMap*>(raw); }

@@ -3,7 +3,7 @@
 // memory (SWIZZLE_64B K-major, zeros or random bytes), one accumulator per N.
 // Answers: how close to the s8 peak can an N=160 pair MMA run by itself?
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o mma2_bench tools/mma2_bench.cu
-//   ./mma2_bench <N> <random 0/1> <seconds>
+//   ./mma2_bench <N> <random 0/1> <seconds> [pattern: 0 one accumulator, 1 the GEMM's 3-accumulator order]
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
@@ -19,15 +19,15 @@ __device__ __forceinline__ uint64_t desc_sw64(uint32_t a) {
     return d;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma2(int nn, int rnd, long long iters,
-                                                                          unsigned long long* out) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma2(int nn, int rnd, int pattern,
+                                                                          long long iters, unsigned long long* out) {
     extern __shared__ __align__(1024) uint8_t smraw[];
     uint8_t* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
     __shared__ uint64_t bar[2];
     __shared__ uint32_t tslot;
     uint32_t rank;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-    for (int e = threadIdx.x; e < 32768 / 4; e += blockDim.x) {
+    for (int e = threadIdx.x; e < 49152 / 4; e += blockDim.x) {
         uint32_t x = rnd ? (e * 2654435761u + blockIdx.x * 97u) ^ 0x5bd1e995u : 0u;
         x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
         reinterpret_cast<uint32_t*>(sm)[e] = rnd ? x : 0u;
@@ -39,7 +39,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma2(int n
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (threadIdx.x < 32) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tslot)));
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -48,17 +48,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma2(int n
     const uint32_t tmem = tslot;
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nn >> 3) << 17) | ((256u >> 4) << 24);
     if (rank == 0 && threadIdx.x == 0) {
-        const uint32_t a0 = smem_u32(sm), b0 = a0 + 16384;
+        const uint32_t a0 = smem_u32(sm), b0 = a0 + 24576;
         uint32_t ph[2] = {0, 0};
         long long done = 0;
         for (long long it = 0; it < iters; ++it) {
+            if (pattern == 0) {
 #pragma unroll
-            for (int u = 0; u < 32; ++u) {
-                const uint64_t da = desc_sw64(a0 + 32 * (u & 1) + 8192 * ((u >> 1) & 1)), db = desc_sw64(b0 + 32 * (u & 1));
-                const uint32_t acc = u == 0 ? 0u : 1u;
-                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                             "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-                             "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                for (int u = 0; u < 32; ++u) {
+                    const uint64_t da = desc_sw64(a0 + 32 * (u & 1) + 8192 * ((u >> 1) & 1)), db = desc_sw64(b0 + 32 * (u & 1));
+                    const uint32_t acc = u == 0 ? 0u : 1u;
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                                 "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                }
+            } else {
+                // the GEMM's pattern: 3 A slices (8 KB apart) x 3 B slices (5 KB apart), accumulators at
+                // TMEM columns 0 / 160 / 320: per K32 step acc0, acc1, acc1, acc2, acc2, acc2
+                const int pa[6] = {0, 0, 1, 0, 1, 2}, pb[6] = {0, 1, 0, 2, 1, 0}, pd[6] = {0, 1, 1, 2, 2, 2};
+#pragma unroll
+                for (int u = 0; u < 32; ++u) {
+                    const int ks = (u / 6) & 1, m = u % 6;
+                    const uint64_t da = desc_sw64(a0 + 8192 * pa[m] + 32 * ks), db = desc_sw64(b0 + 5120 * pb[m] + 32 * ks);
+                    const uint32_t dt = tmem + (uint32_t)(nn * pd[m]);
+                    const uint32_t acc = u < 6 ? 0u : 1u;
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dt),
+                                 "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                }
             }
             const int s = (int)(it & 1);
             asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
@@ -82,16 +98,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma2(int n
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 int main(int argc, char** argv) {
     const int nn = argc > 1 ? atoi(argv[1]) : 160;
     const int rnd = argc > 2 ? atoi(argv[2]) : 0;
     const double secs = argc > 3 ? atof(argv[3]) : 1.0;
+    const int pattern = argc > 4 ? atoi(argv[4]) : 0;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int smem = 32768 + 1024;
+    const int smem = 49152 + 1024;
     cudaFuncSetAttribute(k_mma2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     unsigned long long* d;
     cudaMalloc(&d, 8);
@@ -103,7 +120,7 @@ int main(int argc, char** argv) {
     for (;;) {
         cudaMemset(d, 0, 8);
         cudaEventRecord(e0);
-        k_mma2<<<sms & ~1, 128, smem>>>(nn, rnd, iters, d);
+        k_mma2<<<sms & ~1, 128, smem>>>(nn, rnd, pattern, iters, d);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
@@ -114,7 +131,7 @@ int main(int argc, char** argv) {
     iters = (long long)(iters * (secs * 1e3 / ms));
     cudaMemset(d, 0, 8);
     cudaEventRecord(e0);
-    k_mma2<<<sms & ~1, 128, smem>>>(nn, rnd, iters, d);
+    k_mma2<<<sms & ~1, 128, smem>>>(nn, rnd, pattern, iters, d);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
@@ -122,7 +139,7 @@ int main(int argc, char** argv) {
     cudaMemcpy(&mm, d, 8, cudaMemcpyDeviceToHost);
     // MACs per pair MMA: 256 x N x 32 ; per SM per cycle at the measured clock is computed by the caller
     const double macs = (double)mm * 256 * nn * 32;
-    printf("{\"N\": %d, \"random\": %d, \"ms\": %.1f, \"pair_mmas\": %llu, \"tops\": %.1f, \"mma_per_us_per_pair\": %.3f}\n",
-           nn, rnd, ms, mm, 2 * macs / (ms * 1e-3) / 1e12, mm / (ms * 1e3) / (sms / 2));
+    printf("{\"pattern\": %d, \"N\": %d, \"random\": %d, \"ms\": %.1f, \"pair_mmas\": %llu, \"tops\": %.1f, \"mma_per_us_per_pair\": %.3f}\n",
+           pattern, nn, rnd, ms, mm, 2 * macs / (ms * 1e-3) / 1e12, mm / (ms * 1e3) / (sms / 2));
     return 0;
 }

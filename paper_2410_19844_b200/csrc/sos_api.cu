@@ -204,7 +204,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     P.rowsV = std::max(Np, colBlocksV * kTileN);
     P.nkbV = (r + kQK - 1) / kQK;
     P.rowsVT = ((r + kTileN - 1) / kTileN) * kTileN;
-    P.nkbN = Np / kQK;
+    P.nkbN = (N + kQK - 1) / kQK;  // K = j runs over the N monomials (rows stay padded to Np)
     std::vector<TileCoord> tf, tb;
     build_tiles(Np / kPairM, colBlocksV, true, tf);
     build_tiles(Np / kPairM, P.rowsVT / kTileN, false, tb);

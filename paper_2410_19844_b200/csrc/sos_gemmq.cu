@@ -605,7 +605,9 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
         cudaFuncSetAttribute(k_gemmq<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         configured = true;
     }
-    int grid = 2 * a.ntiles < P.num_sms ? 2 * a.ntiles : P.num_sms;
+    static const int max_ctas = env_int("SOS_GEMM_CTAS", 0);  // experiment: cap the persistent grid
+    const int sms = max_ctas > 0 && max_ctas < P.num_sms ? max_ctas : P.num_sms;
+    int grid = 2 * a.ntiles < sms ? 2 * a.ntiles : sms;
     grid &= ~1;
     if (grid <= 0) return cudaSuccess;
     cudaMemsetAsync(a.progress, 0, sizeof(unsigned long long), st);

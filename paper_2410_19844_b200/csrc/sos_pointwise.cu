@@ -192,11 +192,10 @@ __global__ void __launch_bounds__(256) k_rmax(const uint32_t* __restrict__ pt, c
 // -> one 16-byte chunk per slice of RQ row i, K-block jb (same [jb][i] order as
 // PT, so reads and writes both stream).
 __global__ void __launch_bounds__(256) k_pack_rq(const uint32_t* __restrict__ pt, const float* __restrict__ res,
-                                                 int64_t Np, const unsigned* __restrict__ rrow,
+                                                 int64_t Np, int64_t nkb, const unsigned* __restrict__ rrow,
                                                  uint8_t* __restrict__ RQ, const Scalars* sc, const DevOpt* opt,
                                                  int use_stop) {
     if (descent_stopped(sc, opt, use_stop)) return;
-    const int64_t nkb = Np / kPtW;
     const int64_t total = nkb * Np * 4;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -259,18 +258,18 @@ __device__ __forceinline__ void slice_row(const float* buf, int64_t nkb, int64_t
 // fall into few 32-byte sectors of res.
 constexpr int kRThreads = 512;
 __global__ void __launch_bounds__(kRThreads, 2) k_pack_r_rows(const uint32_t* __restrict__ pt,
-                                                              const float* __restrict__ res, int64_t Np,
+                                                              const float* __restrict__ res, int64_t Np, int64_t nkb,
                                                               unsigned* __restrict__ rrow, uint8_t* __restrict__ RQ,
                                                               const Scalars* sc, const DevOpt* opt, int use_stop) {
     if (descent_stopped(sc, opt, use_stop)) return;
-    extern __shared__ float buf[];  // Np floats = the row
+    extern __shared__ float buf[];  // nkb * 64 floats = the row (K = j padded to 64)
     __shared__ float red[kRThreads / 32];
-    const int64_t nkb = Np / kPtW;
+    const int64_t K = nkb * kPtW;
     for (int64_t i = blockIdx.x; i < Np; i += gridDim.x) {
         float m = 0.f;
         const uint32_t* prow = pt + i * kPtW;
 #pragma unroll 4
-        for (int64_t j = threadIdx.x; j < Np; j += kRThreads) {
+        for (int64_t j = threadIdx.x; j < K; j += kRThreads) {
             const uint32_t k = __ldg(prow + (j / kPtW) * Np * kPtW + (j % kPtW));
             const float x = k != kInvalidRank ? __ldg(res + k) : 0.f;
             buf[j] = x;
@@ -363,14 +362,14 @@ void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     }
     const int bps = row_bytes <= 100 * 1024 ? 2 : 1;
     const unsigned blocks = (unsigned)std::min<int64_t>(Np, (int64_t)P.num_sms * bps);
-    k_pack_r_rows<<<blocks, kRThreads, (size_t)row_bytes, st>>>(P.idx->d_pt, res, Np, P.d_rrow, P.d_rq, P.d_scal,
-                                                                P.d_opt, use_stop);
+    k_pack_r_rows<<<blocks, kRThreads, (size_t)(P.nkbN * kPtW * 4), st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow,
+                                                                         P.d_rq, P.d_scal, P.d_opt, use_stop);
 }
 
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     const int64_t Np = P.idx->Np;
     LaunchScope ls(P, KK_PACK_R, st);
-    k_pack_rq<<<grid_for(P, (Np / kPtW) * Np * 4, 256), 256, 0, st>>>(P.idx->d_pt, res, Np, P.d_rrow, P.d_rq,
+    k_pack_rq<<<grid_for(P, P.nkbN * Np * 4, 256), 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow, P.d_rq,
                                                                        P.d_scal, P.d_opt, use_stop);
 }
 

@@ -3,7 +3,7 @@
 // memory (SWIZZLE_64B K-major, zeros or random bytes), one accumulator per N.
 // Answers: how close to the s8 peak can an N=160 pair MMA run by itself?
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o mma2_bench tools/mma2_bench.cu
-//   ./mma2_bench <N> <random 0/1> <seconds> [pattern: 0 one accumulator, 1 the GEMM's 3-accumulator order]
+//   ./mma2_bench <N> <random 0/1> <seconds> [pattern: 0 one accumulator, 1 the GEMM's 3-accumulator order] [store warps 0-3]
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
@@ -19,8 +19,10 @@ __device__ __forceinline__ uint64_t desc_sw64(uint32_t a) {
     return d;
 }
 
+__device__ volatile int g_stop;
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma2(int nn, int rnd, int pattern,
-                                                                          long long iters, unsigned long long* out) {
+                                                                          long long iters, unsigned long long* out,
+                                                                          int store_warps, unsigned long long* stores) {
     extern __shared__ __align__(1024) uint8_t smraw[];
     uint8_t* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
     __shared__ uint64_t bar[2];
@@ -47,6 +49,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma2(int n
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tslot;
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nn >> 3) << 17) | ((256u >> 4) << 24);
+    if (threadIdx.x >= 32 && (threadIdx.x >> 5) <= store_warps) {
+        // competing shared-memory writes (16-byte stores into a separate 64 KB region)
+        uint4* scratch = reinterpret_cast<uint4*>(sm + 49152);
+        unsigned long long n = 0;
+        const uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
+        while (!g_stop) {
+#pragma unroll 16
+            for (int u = 0; u < 64; ++u) scratch[((threadIdx.x - 32) + 96 * u) & 4095] = v;
+            n += 64;
+        }
+        atomicAdd(stores, n * 16);
+    }
     if (rank == 0 && threadIdx.x == 0) {
         const uint32_t a0 = smem_u32(sm), b0 = a0 + 24576;
         uint32_t ph[2] = {0, 0};
@@ -95,6 +109,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma2(int n
             asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                          "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(&bar[q])), "r"(ph[q]) : "memory");
         atomicAdd(out, (unsigned long long)done);
+        g_stop = 1;
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -106,9 +121,13 @@ int main(int argc, char** argv) {
     const int rnd = argc > 2 ? atoi(argv[2]) : 0;
     const double secs = argc > 3 ? atof(argv[3]) : 1.0;
     const int pattern = argc > 4 ? atoi(argv[4]) : 0;
+    const int store_warps = argc > 5 ? atoi(argv[5]) : 0;
+    unsigned long long* dst;
+    cudaMalloc(&dst, 8);
+    int zero = 0;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int smem = 49152 + 1024;
+    const int smem = 49152 + 65536 + 1024;
     cudaFuncSetAttribute(k_mma2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     unsigned long long* d;
     cudaMalloc(&d, 8);
@@ -119,8 +138,9 @@ int main(int argc, char** argv) {
     float ms = 0;
     for (;;) {
         cudaMemset(d, 0, 8);
+        cudaMemcpyToSymbol(g_stop, &zero, 4);
         cudaEventRecord(e0);
-        k_mma2<<<sms & ~1, 128, smem>>>(nn, rnd, pattern, iters, d);
+        k_mma2<<<sms & ~1, 128, smem>>>(nn, rnd, pattern, iters, d, store_warps, dst);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
@@ -130,16 +150,19 @@ int main(int argc, char** argv) {
     }
     iters = (long long)(iters * (secs * 1e3 / ms));
     cudaMemset(d, 0, 8);
+    cudaMemset(dst, 0, 8);
+    cudaMemcpyToSymbol(g_stop, &zero, 4);
     cudaEventRecord(e0);
-    k_mma2<<<sms & ~1, 128, smem>>>(nn, rnd, pattern, iters, d);
+    k_mma2<<<sms & ~1, 128, smem>>>(nn, rnd, pattern, iters, d, store_warps, dst);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
-    unsigned long long mm = 0;
+    unsigned long long mm = 0, sb = 0;
     cudaMemcpy(&mm, d, 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&sb, dst, 8, cudaMemcpyDeviceToHost);
     // MACs per pair MMA: 256 x N x 32 ; per SM per cycle at the measured clock is computed by the caller
     const double macs = (double)mm * 256 * nn * 32;
-    printf("{\"pattern\": %d, \"N\": %d, \"random\": %d, \"ms\": %.1f, \"pair_mmas\": %llu, \"tops\": %.1f, \"mma_per_us_per_pair\": %.3f}\n",
-           pattern, nn, rnd, ms, mm, 2 * macs / (ms * 1e-3) / 1e12, mm / (ms * 1e3) / (sms / 2));
+    printf("{\"pattern\": %d, \"N\": %d, \"random\": %d, \"store_warps\": %d, \"ms\": %.1f, \"pair_mmas\": %llu, \"tops\": %.1f, \"smem_store_GBps_per_SM\": %.1f}\n",
+           pattern, nn, rnd, store_warps, ms, mm, 2 * macs / (ms * 1e-3) / 1e12, sb / (ms * 1e-3) / sms / 1e9);
     return 0;
 }

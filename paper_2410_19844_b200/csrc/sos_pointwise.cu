@@ -268,12 +268,36 @@ __global__ void __launch_bounds__(kRThreads, 2) k_pack_r_rows(const uint32_t* __
     for (int64_t i = blockIdx.x; i < Np; i += gridDim.x) {
         float m = 0.f;
         const uint32_t* prow = pt + i * kPtW;
-#pragma unroll 4
-        for (int64_t j = threadIdx.x; j < K; j += kRThreads) {
-            const uint32_t k = __ldg(prow + (j / kPtW) * Np * kPtW + (j % kPtW));
-            const float x = k != kInvalidRank ? __ldg(res + k) : 0.f;
-            buf[j] = x;
-            m = fmaxf(m, fabsf(x));
+        // batches of kRB columns per thread; the ranks of batch b+1 are loaded
+        // while the residuals of batch b are gathered (PT latency hidden)
+        constexpr int kRB = 8;
+        const int64_t step = (int64_t)kRThreads * kRB;
+        uint32_t kn[kRB];
+#pragma unroll
+        for (int u = 0; u < kRB; ++u) {
+            const int64_t j = threadIdx.x + (int64_t)u * kRThreads;
+            kn[u] = j < K ? __ldg(prow + (j / kPtW) * Np * kPtW + (j % kPtW)) : kInvalidRank;
+        }
+        for (int64_t j0 = 0; j0 < K; j0 += step) {
+            uint32_t kc[kRB];
+#pragma unroll
+            for (int u = 0; u < kRB; ++u) kc[u] = kn[u];
+            if (j0 + step < K) {
+#pragma unroll
+                for (int u = 0; u < kRB; ++u) {
+                    const int64_t j = j0 + step + threadIdx.x + (int64_t)u * kRThreads;
+                    kn[u] = j < K ? __ldg(prow + (j / kPtW) * Np * kPtW + (j % kPtW)) : kInvalidRank;
+                }
+            }
+            float x[kRB];
+#pragma unroll
+            for (int u = 0; u < kRB; ++u) x[u] = kc[u] != kInvalidRank ? __ldg(res + kc[u]) : 0.f;
+#pragma unroll
+            for (int u = 0; u < kRB; ++u) {
+                const int64_t j = j0 + threadIdx.x + (int64_t)u * kRThreads;
+                if (j < K) buf[j] = x[u];
+                m = fmaxf(m, fabsf(x[u]));
+            }
         }
         m = block_max(m, red, kRThreads);
         if (threadIdx.x == 0) rrow[i] = __float_as_uint(m);

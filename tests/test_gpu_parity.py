@@ -487,18 +487,19 @@ def test_zero_rows_and_columns(sos):
 
 # -------------------------------------------------------------- sos_descend --
 
-@pytest.mark.parametrize("kind,lr", [("adam", 1e-3), ("gd", 5e-3)])
-def test_descend_matches_steps(sos, kind, lr):
+@pytest.mark.parametrize("kind,lr,r", [("adam", 1e-3, 330), ("gd", 5e-3, 330), ("adam", 1e-3, 336)])
+def test_descend_matches_steps(sos, kind, lr, r):
     """sos_descend (slices of V_{t+1} written by the update of step t) follows
     the same iteration as repeated sos_step calls, to the slice precision.
     Row 5 of V0 is zero, so its first update leaves the headroom window and is
-    re-sliced by the fixup kernel."""
+    re-sliced by the fixup kernel.  r = 336 (a multiple of 4) takes the
+    vectorised update path, r = 330 the scalar one."""
     c = si.CONFIGS["c1_n8_2d8"]
     o = oracle(c.n, c.d)
     ix = sos.SosIndex(c.n, c.d)
-    plan = sos.SosPlan(ix, c.r)
+    plan = sos.SosPlan(ix, r)
     p = torch.from_numpy(o.forward(si.planted_w(o.N, c.r_star, 0)).astype(np.float32)).cuda()
-    V0 = si.v0(o.N, c.r, 0)
+    V0 = si.v0(o.N, r, 0)
     V0[5] = 0.0
     steps = 30
     plan.opt_init(kind, lr)

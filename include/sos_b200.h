@@ -180,8 +180,10 @@ int sos_descend(sos_plan *plan, float *V_dev, const float *p_dev, int64_t steps,
 
 /* Host-buffer entry point: copies p_host (M) and V_host (N x r) to the device,
  * runs sos_descend for `steps` steps, copies V back to V_host and the per-step
- * losses (steps values, fp64) to losses_host.  Synchronous.  Uses the plan's
- * optimiser settings (sos_opt_init must have been called). */
+ * losses (steps values, fp64) to losses_host.  Synchronous (legacy default
+ * stream).  Uses the plan's optimiser settings (sos_opt_init must have been
+ * called).  The device staging buffers (4*N*r + 4*M + 8*steps bytes) are kept by
+ * the plan between calls; page-locked host buffers give full copy bandwidth. */
 int sos_solve_host(sos_plan *plan, float *V_host, const float *p_host, int64_t steps,
                    double *losses_host);
 

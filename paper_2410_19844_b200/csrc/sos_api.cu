@@ -266,6 +266,9 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_rrow);
     cudaFree(P.d_dbuf);
     cudaFree(P.d_opt);
+    cudaFree(P.d_hV);
+    cudaFree(P.d_hp);
+    cudaFree(P.d_hl);
     if (P.gexec) cudaGraphExecDestroy(P.gexec);
     cudaFree(P.d_coef);
     cudaFree(P.d_res);
@@ -523,27 +526,27 @@ int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t ste
     if (!pl || !V_host || !p_host || steps < 0 || (steps > 0 && !losses_host)) return fail(SOS_ERR_ARG, "bad argument");
     Plan& P = pl->P;
     const size_t vb = (size_t)P.idx->N * P.r * 4, pb = (size_t)P.idx->M * 4;
-    float *dV = nullptr, *dp = nullptr;
-    double* dl = nullptr;
     int rc;
-    if ((rc = dalloc(&dV, vb)) || (rc = dalloc(&dp, pb)) || (rc = dalloc(&dl, sizeof(double) * (steps > 0 ? steps : 1)))) {
-        cudaFree(dV);
-        cudaFree(dp);
-        return rc;
+    // device staging buffers live with the plan (no per-call cudaMalloc / cudaFree)
+    if (!P.d_hV && ((rc = dalloc(&P.d_hV, vb)) || (rc = dalloc(&P.d_hp, pb)))) return rc;
+    if (P.hl_cap < steps) {
+        cudaFree(P.d_hl);
+        P.d_hl = nullptr;
+        P.hl_cap = 0;
+        if ((rc = dalloc(&P.d_hl, sizeof(double) * steps))) return rc;
+        P.hl_cap = steps;
     }
     cudaStream_t st = 0;
     rc = SOS_OK;
-    if (cudaMemcpyAsync(dV, V_host, vb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaMemcpyAsync(dp, p_host, pb, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    if (cudaMemcpyAsync(P.d_hV, V_host, vb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(P.d_hp, p_host, pb, cudaMemcpyHostToDevice, st) != cudaSuccess)
         rc = fail(SOS_ERR_CUDA, "H2D copy");
-    if (!rc) rc = sos_descend(pl, dV, dp, steps, dl, st);
-    if (!rc && (cudaMemcpyAsync(V_host, dV, vb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-                (steps > 0 && cudaMemcpyAsync(losses_host, dl, sizeof(double) * steps, cudaMemcpyDeviceToHost, st) != cudaSuccess) ||
+    if (!rc) rc = sos_descend(pl, P.d_hV, P.d_hp, steps, P.d_hl, st);
+    if (!rc && (cudaMemcpyAsync(V_host, P.d_hV, vb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                (steps > 0 && cudaMemcpyAsync(losses_host, P.d_hl, sizeof(double) * steps, cudaMemcpyDeviceToHost, st) !=
+                                  cudaSuccess) ||
                 cudaStreamSynchronize(st) != cudaSuccess))
         rc = fail(SOS_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
-    cudaFree(dV);
-    cudaFree(dp);
-    cudaFree(dl);
     return rc;
 }
 

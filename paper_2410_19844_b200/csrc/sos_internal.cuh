@@ -144,6 +144,11 @@ struct Plan {
     cudaGraphExec_t gexec;
     const void* gkey[3];   // (V, p, losses) the graph was captured for
     int64_t glaunches;     // kernels per replay (launch accounting)
+    // sos_solve_host: device staging of the caller's host buffers (lazy)
+    float* d_hV;
+    float* d_hp;
+    double* d_hl;
+    int64_t hl_cap;
     int64_t launches;
     int num_sms;
     Timing* timing;

@@ -3,7 +3,9 @@
 // cycles a 4-deep ring of 24 KB stages over a private 2 MB region of an
 // L2-resident buffer.  mode 0: one 3-D tensor box {256 B, 32 rows, 3 planes}
 // (the GEMM's A stage); mode 1: three 2-D boxes {256 B, 32 rows}; mode 2: three
-// 8 KB cp.async.bulk (non-tensor) copies.
+// 8 KB cp.async.bulk (non-tensor) copies; mode 3: 256 threads issue 16-byte
+// cp.async (LDGSTS) copies of the same stages; mode 4: 256 threads load 16-byte
+// vectors into registers (raw L2 -> SM read rate, no shared-memory write).
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tma_bench tools/tma_bench.cu -lcuda
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -62,6 +64,37 @@ __global__ void __launch_bounds__(32, 1) k_tma(const __grid_constant__ CUtensorM
     atomicAdd(cyc, (unsigned long long)(clock64() - c0));
 }
 
+__global__ void __launch_bounds__(256, 1) k_lsu(const uint8_t* src, int mode, long long iters,
+                                                unsigned long long* cyc, unsigned long long* sink) {
+    extern __shared__ __align__(1024) uint8_t smraw[];
+    uint8_t* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
+    const long long c0 = clock64();
+    const int64_t region = (int64_t)blockIdx.x * (2 << 20);
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (long long it = 0; it < iters; ++it) {
+        const int s = (int)(it & 3);
+        const int64_t off = region + (it % 85) * 24576;
+        if (mode == 3) {
+            for (int c = threadIdx.x; c < 24576 / 16; c += 256) {
+                const uint32_t d = smem_u32(sm + s * 24576 + 16 * c);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + off + 16 * c) : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group 3;" ::: "memory");
+        } else {
+#pragma unroll 6
+            for (int c = threadIdx.x; c < 24576 / 16; c += 256) {
+                const uint4 v = __ldcg(reinterpret_cast<const uint4*>(src + off) + c);
+                acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(cyc, (unsigned long long)(clock64() - c0));
+    if (acc.x == 0x12345678u) atomicAdd(sink, 1ull);
+}
+
 int main(int argc, char** argv) {
     const int mode = argc > 1 ? atoi(argv[1]) : 0;
     int sms = 0;
@@ -88,13 +121,17 @@ int main(int argc, char** argv) {
     unsigned long long* cyc;
     cudaMalloc(&cyc, 8);
     const long long iters = 40000;
+    cudaFuncSetAttribute(k_lsu, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    unsigned long long* sink;
+    cudaMalloc(&sink, 8);
     for (int rep = 0; rep < 2; ++rep) {
         cudaMemset(cyc, 0, 8);
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        k_tma<<<sms, 32, smem>>>(m3, m2, buf, mode, iters, cyc);
+        if (mode <= 2) k_tma<<<sms, 32, smem>>>(m3, m2, buf, mode, iters, cyc);
+        else k_lsu<<<sms, 256, smem>>>(buf, mode, iters, cyc, sink);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;

@@ -546,3 +546,36 @@ def test_descend_reaches_1e8_config2_and_stops(sos):
     lo, _, _, _ = o.loss_grad(V.cpu().numpy(), pf, want_grad=False)
     print(f"descend config2: stop at step {hit[0]}, oracle eps_rel {lo / pn:.3e}")
     assert lo / pn <= 1e-8
+
+
+def test_large_n_sampled(sos):
+    """Beyond the BASELINE sizes: n=20, 2d=10 (N = 42,504 monomials, M =
+    20,030,010 coefficients, r = N; R rows of 171 KB still take the fused R
+    packer, K = 42,752 stays below the exact-s32 segment bound).  Sampled
+    coefficients and gradient rows against the oracle, and the
+    point-evaluation identity on the full coefficient vector."""
+    n, d = 20, 5
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    assert (ix.N, ix.M) == (o.N, o.M) == (42504, 20030010)
+    r = ix.N
+    plan = sos.SosPlan(ix, r)
+    V = si.v0(ix.N, r, seed=5)
+    Vd = torch.from_numpy(V).cuda()
+    coef = plan.forward(Vd).cpu().numpy().astype(np.float64)
+    rng = np.random.default_rng(7)
+    betas = np.concatenate([[0, 1, o.M - 1], rng.integers(0, o.M, 20)])
+    assert rel_l2(coef[betas], o.coef_sample(V, betas)) <= REL_TOL
+    res = si.residual_probe(o.M, seed=8)
+    g = plan.backward(Vd, torch.from_numpy(res).cuda())
+    rows = np.array([3, o.N - 2], dtype=np.int64)
+    got = g[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert rel_l2(got, o.grad_rows(V, res, rows)) <= REL_TOL
+    x = si.points(1, n, seed=9)[0] * 0.5
+    B = o.beta().astype(np.float64)
+    lhs = coef @ np.prod(x[None, :] ** B, axis=1)
+    A = o.alpha().astype(np.float64)
+    rhs = np.sum((np.prod(x[None, :] ** A, axis=1) @ V.astype(np.float64)) ** 2)
+    assert abs(lhs - rhs) <= REL_TOL * abs(rhs)
+    plan.close()
+    ix.close()

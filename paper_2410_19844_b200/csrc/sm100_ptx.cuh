@@ -102,6 +102,19 @@ __host__ __device__ constexpr uint32_t umma_idesc_s8_s32(int M, int N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// one lane of the (fully active) warp: the issue slot for single-thread
+// tcgen05 / TMA instructions whose operands the whole warp computed uniformly
+// (keeps them in uniform registers instead of per-issue R2UR round trips)
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // ------------------------------------------------------ clusters / CTA pairs --
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;

@@ -335,10 +335,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer --
-        if (leader && lane == 0) {
+        // the whole warp runs the loop (waits, descriptor arithmetic: warp-uniform
+        // values in uniform registers); one elected lane issues the MMAs and
+        // commits.  A single-lane loop spent ~15 % of the tensor pipe on issue.
+        if (leader) {
             const long long t_start = clock64();
             constexpr uint32_t idesc = umma_idesc_s8_s32(kPairM, kTileN);
             const uint32_t d0 = tbase, d1 = tbase + kTileN, d2 = tbase + 2 * kTileN;
+            // descriptor of stage 0, slice 0; other operands differ only in the
+            // start-address field (bits 0-13, 16-byte units)
+            const uint64_t desc0 = umma_desc_sw64(smem_u32(smem));
             int stage = 0;
             uint32_t phase = 0;
             uint32_t acc_phase = 0;
@@ -348,50 +354,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     {
                         const long long c0 = clock64();
                         mbar_wait_cluster(tempty, acc_phase ^ 1);
-                        if (args.dbg) atomicAdd(args.dbg + 2, (unsigned long long)(clock64() - c0));
+                        if (args.dbg && lane == 0) atomicAdd(args.dbg + 2, (unsigned long long)(clock64() - c0));
                     }
                     tc_fence_after();
                     for (int kb = kb0; kb < kb1; ++kb) {
                         {
                             const long long c0 = clock64();
                             mbar_wait(&full[stage], phase);
-                            if (args.dbg) atomicAdd(args.dbg + 3, (unsigned long long)(clock64() - c0));
+                            if (args.dbg && lane == 0) atomicAdd(args.dbg + 3, (unsigned long long)(clock64() - c0));
                         }
                         tc_fence_after();
-                        const uint32_t a0 = smem_u32(smem + stage * kStageBytes);
-                        const uint32_t b0 = a0 + kABytes;
-                        // per 32-wide K step (ks) the MMAs that share an A slice run back to
-                        // back and take A from the tensor core's collector buffer after the
-                        // first read (collector::a fill / use / lastuse): A is read from
-                        // shared memory 3 times instead of 6, which relieves the shared-memory
-                        // bandwidth the MMA reads share with the TMA fills
+                        const uint64_t sd = desc0 + (uint64_t)((stage * kStageBytes) >> 4);
+                        const uint64_t bd = sd + (kABytes >> 4);
                         const bool first = kb == kb0;
-                        const uint64_t a1[2] = {umma_desc_sw64(a0), umma_desc_sw64(a0 + 32)};
-                        const uint64_t a2[2] = {umma_desc_sw64(a0 + kASliceBytes), umma_desc_sw64(a0 + kASliceBytes + 32)};
-                        const uint64_t a3[2] = {umma_desc_sw64(a0 + 2 * kASliceBytes),
-                                                umma_desc_sw64(a0 + 2 * kASliceBytes + 32)};
-                        const uint64_t b1[2] = {umma_desc_sw64(b0), umma_desc_sw64(b0 + 32)};
-                        const uint64_t b2[2] = {umma_desc_sw64(b0 + kBSliceBytes), umma_desc_sw64(b0 + kBSliceBytes + 32)};
-                        const uint64_t b3[2] = {umma_desc_sw64(b0 + 2 * kBSliceBytes),
-                                                umma_desc_sw64(b0 + 2 * kBSliceBytes + 32)};
+                        if (elect_one()) {
+                            // per 32-wide K step (ks) the MMAs that share an A slice run back
+                            // to back and take A from the tensor core's collector buffer after
+                            // the first read (collector::a fill / use / lastuse)
 #pragma unroll
-                        for (int ks = 0; ks < 2; ++ks) {
-                            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-                            umma_s8_2sm<1>(d0, a1[ks], b1[ks], idesc, acc);  // a1 read once, kept
-                            umma_s8_2sm<2>(d1, a1[ks], b2[ks], idesc, acc);
-                            umma_s8_2sm<3>(d2, a1[ks], b3[ks], idesc, acc);  // a1 released
-                            umma_s8_2sm<1>(d1, a2[ks], b1[ks], idesc, 1u);   // a2 read once, kept
-                            umma_s8_2sm<3>(d2, a2[ks], b2[ks], idesc, 1u);   // a2 released
-                            umma_s8_2sm<0>(d2, a3[ks], b1[ks], idesc, 1u);
+                            for (int ks = 0; ks < 2; ++ks) {
+                                const uint64_t k2 = (uint64_t)(ks * 2);  // +32 bytes
+                                const uint64_t a1 = sd + k2, a2 = sd + (kASliceBytes >> 4) + k2,
+                                               a3 = sd + (2 * kASliceBytes >> 4) + k2;
+                                const uint64_t b1 = bd + k2, b2 = bd + (kBSliceBytes >> 4) + k2,
+                                               b3 = bd + (2 * kBSliceBytes >> 4) + k2;
+                                const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+                                umma_s8_2sm<1>(d0, a1, b1, idesc, acc);  // a1 read once, kept
+                                umma_s8_2sm<2>(d1, a1, b2, idesc, acc);
+                                umma_s8_2sm<3>(d2, a1, b3, idesc, acc);  // a1 released
+                                umma_s8_2sm<1>(d1, a2, b1, idesc, 1u);   // a2 read once, kept
+                                umma_s8_2sm<3>(d2, a2, b2, idesc, 1u);   // a2 released
+                                umma_s8_2sm<0>(d2, a3, b1, idesc, 1u);
+                            }
+                            umma_commit_2sm(&empty[stage], 0x3);  // both CTAs' smem slots free
                         }
-                        umma_commit_2sm(&empty[stage], 0x3);  // both CTAs' smem slots free
+                        __syncwarp();
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
-                    umma_commit_2sm(tfull, 0x3);  // both CTAs' epilogues may drain
+                    if (elect_one()) umma_commit_2sm(tfull, 0x3);  // both CTAs' epilogues may drain
+                    __syncwarp();
                     acc_phase ^= 1;
                 }
             }
-            if (args.dbg) atomicAdd(args.dbg + 4, (unsigned long long)(clock64() - t_start));
+            if (args.dbg && lane == 0) atomicAdd(args.dbg + 4, (unsigned long long)(clock64() - t_start));
         }
     } else if (warp < 2 + kEpiWarps) {
         // -------------------------------------------------------- epilogue --

@@ -7,6 +7,7 @@
 // cp.async (LDGSTS) copies of the same stages; mode 4: 256 threads load 16-byte
 // vectors into registers (raw L2 -> SM read rate, no shared-memory write).
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tma_bench tools/tma_bench.cu -lcuda
+//   ./tma_bench <mode> [CTAs]
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
@@ -99,6 +100,7 @@ int main(int argc, char** argv) {
     const int mode = argc > 1 ? atoi(argv[1]) : 0;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    if (argc > 2 && atoi(argv[2]) > 0 && atoi(argv[2]) < sms) sms = atoi(argv[2]);  // CTAs (one per SM)
     const size_t bytes = (size_t)sms * (2 << 20) + (1 << 20);
     uint8_t* buf;
     cudaMalloc(&buf, bytes);

@@ -293,7 +293,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 
     if (warp == 0) {
         // ------------------------------------------------------- producer --
-        if (lane == 0) {
+        // whole warp (warp-uniform loop state), one elected lane issues
+        {
             int stage = 0;
             uint32_t phase = 0;
             int64_t g = 0;
@@ -309,29 +310,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     // their shared panels through L2 instead of whole panels.
                     if (g % args.skew_epoch == 0 && g > 0) {
                         const int64_t e = g / args.skew_epoch;
-                        atomicAdd(args.progress, 1ull);
+                        if (lane == 0) atomicAdd(args.progress, 1ull);
                         if (e >= args.skew_lag) {
                             const unsigned long long need = G * (unsigned long long)(e - args.skew_lag + 1);
                             const long long c0 = clock64();
-                            for (int spin = 0; spin < kSkewMaxSpin && ld_acquire_u64(args.progress) < need; ++spin)
-                                if (args.skew_sleep) __nanosleep(args.skew_sleep);
-                            if (args.dbg) atomicAdd(args.dbg + 0, (unsigned long long)(clock64() - c0));
+                            if (lane == 0)
+                                for (int spin = 0; spin < kSkewMaxSpin && ld_acquire_u64(args.progress) < need; ++spin)
+                                    if (args.skew_sleep) __nanosleep(args.skew_sleep);
+                            __syncwarp();
+                            if (args.dbg && lane == 0) atomicAdd(args.dbg + 0, (unsigned long long)(clock64() - c0));
                         }
                     }
                     {
                         const long long c0 = clock64();
                         mbar_wait(&empty[stage], phase ^ 1);
-                        if (args.dbg) atomicAdd(args.dbg + 1, (unsigned long long)(clock64() - c0));
+                        if (args.dbg && lane == 0) atomicAdd(args.dbg + 1, (unsigned long long)(clock64() - c0));
                     }
-                    uint8_t* sa = smem + stage * kStageBytes;
-                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
-                    // the tensor maps view 4 consecutive 64-byte Q-rows as one 256-byte row
-                    tma_load_3d_2sm(sa, &tmA, &full[stage], 0, (int32_t)((kb * args.a_rows + rowA) >> 2), 0);
-                    tma_load_3d_2sm(sa + kABytes, &tmB, &full[stage], 0, (int32_t)((kb * args.b_rows + rowB) >> 2), 0);
+                    if (elect_one()) {
+                        uint8_t* sa = smem + stage * kStageBytes;
+                        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+                        // the tensor maps view 4 consecutive 64-byte Q-rows as one 256-byte row
+                        tma_load_3d_2sm(sa, &tmA, &full[stage], 0, (int32_t)((kb * args.a_rows + rowA) >> 2), 0);
+                        tma_load_3d_2sm(sa + kABytes, &tmB, &full[stage], 0, (int32_t)((kb * args.b_rows + rowB) >> 2), 0);
+                    }
+                    __syncwarp();
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
-            atomicAdd(args.progress, 1ull << 32);
+            if (lane == 0) atomicAdd(args.progress, 1ull << 32);
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer --

@@ -38,6 +38,9 @@ METRIC = "SOS grad steps/sec and effective TFLOP/s (% tensor roofline) at N mono
 # (a1b1, a1b2, a2b1, a1b3, a2b2, a3b1) on the s8 tensor path
 N_PRODUCTS = 6
 I8_OVER_BF16 = 2.0  # nominal dense s8 / bf16 rate on B200 (4.5 POPS / 2.25 PFLOP/s)
+# context only: our own s8 MMA microbenchmark under the power cap (operands in
+# shared memory, random data), per fp32-equivalent flop: 3751 TOPS / 6 products
+PEAK_S8_MICROBENCH = 3751.0 / N_PRODUCTS
 
 
 def parse():
@@ -337,7 +340,11 @@ def run_ours(args):
                      "peak_source": f"{peak_src} bf16_tflops_sustained {peaks['bf16_tflops_sustained']} x "
                                     f"{I8_OVER_BF16} (nominal s8/bf16 ratio) / {N_PRODUCTS} s8 slice products "
                                     f"per fp32-equivalent multiply-add",
-                     "flops_per_launch": flops["bwd"]},
+                     "flops_per_launch": flops["bwd"],
+                     "peak_s8_microbench": PEAK_S8_MICROBENCH,
+                     "frac_of_s8_microbench": achieved_bwd / PEAK_S8_MICROBENCH,
+                     "peak_s8_microbench_source": "profiles/r1_mma_power.md: s8 MMAs on random operands under the "
+                                                  "1 kW cap, 3751 TOPS / 6 slice products"},
         "kernels": {k: {"ms_per_launch": (v[0] / v[1] if v[1] else None), "launches": v[1],
                         "share": (v[0] / total_kernel_ms if total_kernel_ms else None)} for k, v in kt.items()},
         "fwd_gemm_tflops": achieved_fwd,

@@ -171,6 +171,13 @@ int sos_index_pair_ranks(const sos_index* h, const int64_t* i_dev, const int64_t
     return check_launch("pair lookup");
 }
 
+// scratch of the lattice DP for the R row maxima: degrees d+1 .. 2d-1
+static size_t rlev_floats(const Index& ix) {
+    size_t s = 0;
+    for (int D = ix.d + 1; D <= 2 * ix.d - 1; ++D) s += (size_t)rmax_level_count(ix.n, D);
+    return s;
+}
+
 // ------------------------------------------------------------------- plan --
 // CTA-pair tiles: a = 256-row block, b = 160-col block, grouped raster (8 row
 // blocks per group) so a wave of CTAs shares A and B panels in L2
@@ -218,6 +225,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         (rc = dalloc(&P.d_rrow, (size_t)Np * 4)) || (rc = dalloc(&P.d_coef, (size_t)M * 4)) ||
         (rc = dalloc(&P.d_dbuf, (size_t)(4 * P.rowsV + 2 * P.rowsVT) * 4)) ||
         (rc = dalloc(&P.d_opt, sizeof(DevOpt))) ||
+        (rc = dalloc(&P.d_rlev, std::max<size_t>(1, rlev_floats(h->ix)) * sizeof(float))) ||
         (rc = dalloc(&P.d_res, (size_t)M * 4)) || (rc = dalloc(&P.d_scal, sizeof(Scalars))) ||
         (rc = dalloc(&P.d_ring, (size_t)sms * 2 * 128 * kTileN * 4)) ||
         (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) ||
@@ -266,6 +274,7 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_rrow);
     cudaFree(P.d_dbuf);
     cudaFree(P.d_opt);
+    cudaFree(P.d_rlev);
     cudaFree(P.d_hV);
     cudaFree(P.d_hp);
     cudaFree(P.d_hl);

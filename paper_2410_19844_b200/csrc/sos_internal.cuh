@@ -123,6 +123,7 @@ struct Plan {
     unsigned* d_vrow; // max_k |V_ik| (float bits), rowsV
     unsigned* d_vcol; // max_j |V_jk| (float bits), rowsVT
     unsigned* d_rrow; // max_j |R_ij| (float bits), Np
+    float* d_rlev;    // lattice-DP levels for the R row maxima
     unsigned* d_dbuf; // sos_descend: [2][rowsV] exact row maxima, [2][rowsV] used row scales, [2][rowsVT] column maxima
     float* d_coef;    // M
     float* d_res;     // M
@@ -182,6 +183,16 @@ void launch_index_build(Index& ix, cudaStream_t st);
 void launch_beta_table(const Index& ix, uint8_t* beta, cudaStream_t st);
 void launch_pair_lookup(const Index& ix, const int64_t* i, const int64_t* j, int64_t cnt, uint32_t* out,
                         cudaStream_t st);
+// number of degree-D monomials in n variables, C(n+D-1, D)
+inline int64_t rmax_level_count(int n, int D) {
+    long double c = 1;
+    for (int t = 1; t <= D; ++t) c = c * (n + D - t) / t;
+    return (int64_t)(c + 0.5L);
+}
+// R row maxima through the monomial lattice (sos_index.cu); scratch holds the
+// levels strictly between degree 2d and degree d
+void launch_rmax_dp(const Index& ix, const float* res, float* scratch, unsigned* rrow, cudaStream_t st,
+                    const Scalars* sc, const DevOpt* opt, int use_stop);
 
 void launch_vmax(Plan& P, const float* V, cudaStream_t st, unsigned* vrow = nullptr, unsigned* vcol = nullptr);
 void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow = nullptr,

@@ -5,6 +5,7 @@
 // GEMM (sos_gemmq.cu).  All kernels are coalesced and sized as a multiple of
 // the SM count (grid-stride).
 #include <algorithm>
+#include <cstdlib>
 
 #include "sos_internal.cuh"
 #include "sos_slice.cuh"
@@ -188,35 +189,39 @@ __global__ void __launch_bounds__(256) k_rmax(const uint32_t* __restrict__ pt, c
 }
 
 // --------------------------------------------------------------- pack RQ ----
-// thread = (jb, i, chunk c): 16 ranks (64 B of PT) -> 16 gathered residuals
-// -> one 16-byte chunk per slice of RQ row i, K-block jb (same [jb][i] order as
-// PT, so reads and writes both stream).
+// Row maxima known (rrow): a warp packs 8 rows x one 64-wide K-block.  Lanes
+// gather consecutive j (for a fixed row, consecutive j give nearby ranks in
+// colex order, so a warp's 32 gathers touch few 32-byte sectors of res) into a
+// per-warp shared-memory tile; then lane (row r, chunk c) slices 16 values and
+// the 32 lanes write 8 consecutive 64-byte Q-rows per slice.
 __global__ void __launch_bounds__(256) k_pack_rq(const uint32_t* __restrict__ pt, const float* __restrict__ res,
                                                  int64_t Np, int64_t nkb, const unsigned* __restrict__ rrow,
                                                  uint8_t* __restrict__ RQ, const Scalars* sc, const DevOpt* opt,
                                                  int use_stop) {
     if (descent_stopped(sc, opt, use_stop)) return;
-    const int64_t total = nkb * Np * 4;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(t & 3);
-        const int64_t rest = t >> 2;  // = jb * Np + i
-        const int64_t jb = rest / Np, i = rest - jb * Np;
-        const uint4* p4 = reinterpret_cast<const uint4*>(pt + rest * kPtW + c * 16);
+    __shared__ float tile[8][8][kPtW + 4];  // [warp][row][j], padded
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t groups = Np / 8;
+    const int64_t tasks = nkb * groups;  // (jb, 8-row group)
+    for (int64_t task = blockIdx.x * 8 + w; task < tasks; task += (int64_t)gridDim.x * 8) {
+        const int64_t jb = task / groups, i0 = (task - jb * groups) * 8;
+        const uint32_t* p0 = pt + (jb * Np + i0) * kPtW;  // 8 rows x 64 ranks, contiguous
+        uint32_t k[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) k[u] = __ldg(p0 + u * 32 + lane);  // row u/2, column (u%2)*32 + lane
+#pragma unroll
+        for (int u = 0; u < 16; ++u) tile[w][u >> 1][(u & 1) * 32 + lane] = k[u] != kInvalidRank ? __ldg(res + k[u]) : 0.f;
+        __syncwarp();
+        const int r = lane >> 2, c = lane & 3;
         float x[16];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint4 k = __ldg(p4 + u);
-            const uint32_t kk[4] = {k.x, k.y, k.z, k.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) x[4 * u + e] = kk[e] != kInvalidRank ? __ldg(res + kk[e]) : 0.f;
-        }
+        for (int e = 0; e < 16; ++e) x[e] = tile[w][r][c * 16 + e];
         uint4 q[3];
-        slice16(x, slice_scale(__ldg(rrow + i)), q);
-        store_q16(RQ, jb, i, c, nkb, Np, q);
+        slice16(x, slice_scale(__ldg(rrow + i0 + r)), q);
+        store_q16(RQ, jb, i0 + r, c, nkb, Np, q);
+        __syncwarp();
     }
 }
-
 
 // ----------------------------------------------------- fused row packers ----
 // One pass per row: a block stages a whole row in shared memory (contiguous
@@ -368,13 +373,23 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, uns
     k_pack_vq<<<grid_for(P, work, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.rowsV, P.nkbV, vrow, P.d_vq);
 }
 
-// row maxima + RQ: one fused gather pass per row when the row fits the staging
-// buffer, else k_rmax followed by k_pack_rq (two gather passes)
+// row maxima + RQ: the row maxima come from the lattice DP (sos_index.cu, a
+// few tens of millions of lookups instead of N^2 gathers), then one streaming
+// pass gathers and slices R.  SOS_RPACK_FUSED=1 selects the one-pass fused
+// packer (row staged in shared memory), SOS_RPACK_TWOPASS=1 the gathered maxima.
 void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     const int64_t Np = P.idx->Np;
     const int64_t row_bytes = Np * 4;
-    if (row_bytes > kRowSmemMax) {
-        launch_rmax(P, res, st, use_stop);
+    static const bool fused = getenv("SOS_RPACK_FUSED") && atoi(getenv("SOS_RPACK_FUSED"));
+    static const bool two_pass = getenv("SOS_RPACK_TWOPASS") && atoi(getenv("SOS_RPACK_TWOPASS"));
+    if (!fused || row_bytes > kRowSmemMax) {
+        if (two_pass) {
+            launch_rmax(P, res, st, use_stop);
+        } else {
+            LaunchScope ls(P, KK_ABSMAX_R, st);
+            launch_rmax_dp(*P.idx, res, P.d_rlev, P.d_rrow, st, P.d_scal, P.d_opt, use_stop);
+            P.launches += P.idx->d - 1;  // one kernel per lattice level (the scope counts one)
+        }
         launch_pack_rq(P, res, st, use_stop);
         return;
     }
@@ -393,7 +408,7 @@ void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop) {
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     const int64_t Np = P.idx->Np;
     LaunchScope ls(P, KK_PACK_R, st);
-    k_pack_rq<<<grid_for(P, P.nkbN * Np * 4, 256), 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow, P.d_rq,
+    k_pack_rq<<<grid_for(P, P.nkbN * (Np / 8) * 32, 256), 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow, P.d_rq,
                                                                        P.d_scal, P.d_opt, use_stop);
 }
 

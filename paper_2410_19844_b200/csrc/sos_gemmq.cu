@@ -19,11 +19,15 @@
 // scales: value = u_i u_j (acc0 + acc1/256 + acc2/65536).
 //
 // Warp roles (384 threads per CTA, 1 CTA per SM, persistent over a static tile list):
-//   warp 0      one lane issues the 2-SM TMA loads, completion on the leader's barrier
-//   warp 1      allocates 512 TMEM columns (pair-wide); the leader's lane 0 issues MMAs
+//   warp 0      producer: the 2-SM TMA loads (completion on the leader's barrier)
+//   warp 1      allocates 512 TMEM columns (pair-wide); in the leader CTA it issues
+//               the MMAs.  Both run as whole warps over warp-uniform state and issue
+//               from one elect.sync lane (a single-lane loop cost ~15 % of the
+//               tensor pipe in R2UR / BRA.U.ANY sequences)
 //   warps 2..9  epilogue: TMEM lane quarter (warp & 3) x column half (80 columns)
 //   warps 10,11 aux: forward -> pack V^T slices for the backward that follows;
-//               backward in sos_step -> optimiser update from the gradient-tile ring
+//               backward in sos_step / sos_descend -> optimiser update from the
+//               gradient-tile ring (and, in sos_descend, the next step's V slices)
 #include <cuda.h>
 #include <cudaTypedefs.h>
 

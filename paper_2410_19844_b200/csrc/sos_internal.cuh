@@ -65,7 +65,7 @@ constexpr int kPtW = 64;          // pair-rank table chunk width (columns j per 
 // bounded K-skew between the CTAs of a GEMM (see the producer in sos_gemmq.cu)
 constexpr int kSkewEpoch = 4;     // K-blocks (of 64) per progress epoch (tools/gpu_tune2.sh)
 constexpr int kSkewLag = 2;       // epochs a CTA may run ahead of the slowest
-constexpr int kSkewMaxSpin = 8192;  // bounded wait (x 256 ns): a locality hint, never a deadlock
+constexpr int kSkewMaxSpin = 8192;  // bounded wait (polls): a locality hint, never a deadlock
 constexpr uint32_t kInvalidRank = 0xFFFFFFFFu;
 constexpr int kMaxVars = 255;     // n + 2d <= 255 (variable indices are uint8)
 constexpr int kMaxDeg2 = 64;

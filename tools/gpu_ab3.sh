@@ -1,5 +1,5 @@
 cd paper_2410_19844_b200
-for rep in 1 2; do for v in s5 s4; do
+for rep in 1; do for v in s5 s4 s5 s4; do
   cp libsos_$v.so libsos_b200.so
   (cd .. && timeout 200 python bench.py --steps 12 --warmup 3 --no-e2e --no-cpu-baseline > /tmp/b.json 2>/dev/null)
   python3 -c "

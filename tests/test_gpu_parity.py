@@ -579,3 +579,26 @@ def test_large_n_sampled(sos):
     assert abs(lhs - rhs) <= REL_TOL * abs(rhs)
     plan.close()
     ix.close()
+
+
+# tile-boundary shapes: N just above 160 (B-tile width) and 256 (pair tile
+# height), r around the 64-wide K-block and the 160-wide column block
+BOUNDARY = [
+    (9, 3, 63), (9, 3, 64), (9, 3, 65),          # N = 165
+    (11, 3, 159), (11, 3, 160), (11, 3, 161),    # N = 286
+    (4, 8, 255), (4, 8, 256), (4, 8, 257),       # N = 165, high degree
+    (7, 4, 1), (7, 4, 321),                      # N = 210
+]
+
+
+@pytest.mark.parametrize("n,d,r", BOUNDARY)
+def test_boundary_shapes_forward_backward(sos, n, d, r):
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    V = si.v0(o.N, r, seed=100 + r)
+    Vd = torch.from_numpy(V).cuda()
+    assert rel_l2(plan.forward(Vd).cpu().numpy(), o.forward(V)) <= REL_TOL
+    res = si.residual_probe(o.M, seed=200 + r)
+    g = plan.backward(Vd, torch.from_numpy(res).cuda()).cpu().numpy()
+    assert rel_l2(g, o.grad_rows(V, res, np.arange(o.N))) <= REL_TOL

@@ -59,6 +59,8 @@ struct GemmArgs {
     int skew_epoch, skew_lag;  // bounded K-skew (K-blocks per epoch, epochs of lead)
     int skew_sleep;            // ns between polls of the progress counter
     unsigned long long* dbg;   // SOS_GEMM_STATS: per-role wait cycles (instrumentation only)
+    int kserp;                 // walk K backwards on odd local tiles (L2 reuse across waves)
+    int probe;                 // SOS_GEMM_PROBE (experiment, wrong results): 1 = K-blocks mod 8, 2 = also tile 0, 4 = 2 with B loaded only on the first ring pass
     // kModeBwdUpdate: the optimiser step of PAPER.md:221, applied by the aux warps
     float* ring;  // per-CTA ring of 2 finished gradient tiles (128 x 160 fp32 each)
     float* V;
@@ -303,8 +305,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             uint32_t phase = 0;
             int64_t g = 0;
             const unsigned long long G = gridDim.x;
-            for (int tile = cid; tile < args.ntiles; tile += ncl) {
+            int it = 0;
+            for (int tile = cid; tile < args.ntiles; tile += ncl, ++it) {
                 const TileCoord tc = args.tiles[tile];
+                // serpentine K: consecutive waves share their A panels (grouped raster), so
+                // every other tile walks K backwards and starts on the slabs the previous
+                // wave loaded last, still in L2 (-1.4 % step time, profiles/r1_l2_probes.md)
+                const bool rev = args.kserp && (it & 1);
                 const int32_t rowA = tc.a * kPairM + (int)rank * 128;
                 const int32_t rowB = tc.b * kTileN + (int)rank * kHalfN;
                 for (int kb = 0; kb < args.num_kb; ++kb, ++g) {
@@ -332,10 +339,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     }
                     if (elect_one()) {
                         uint8_t* sa = smem + stage * kStageBytes;
-                        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+                        const bool skipB = args.probe == 4 && g >= kStages;
+                        if (leader) mbar_arrive_expect_tx(&full[stage], skipB ? 2 * kABytes : 2 * kStageBytes);
                         // the tensor maps view 4 consecutive 64-byte Q-rows as one 256-byte row
-                        tma_load_3d_2sm(sa, &tmA, &full[stage], 0, (int32_t)((kb * args.a_rows + rowA) >> 2), 0);
-                        tma_load_3d_2sm(sa + kABytes, &tmB, &full[stage], 0, (int32_t)((kb * args.b_rows + rowB) >> 2), 0);
+                        const int kq = args.probe ? (kb & 7) : rev ? args.num_kb - 1 - kb : kb;
+                        const int32_t ra = args.probe >= 2 ? (int32_t)rank * 128 : rowA;
+                        const int32_t rb = args.probe >= 2 ? (int32_t)rank * kHalfN : rowB;
+                        tma_load_3d_2sm(sa, &tmA, &full[stage], 0, (int32_t)((kq * args.a_rows + ra) >> 2), 0);
+                        if (!skipB)
+                            tma_load_3d_2sm(sa + kABytes, &tmB, &full[stage], 0, (int32_t)((kq * args.b_rows + rb) >> 2), 0);
                     }
                     __syncwarp();
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -610,6 +622,10 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
     a.skew_lag = lag;
     static const int sleep_ns = env_int("SOS_SKEW_SLEEP", 256);
     a.skew_sleep = sleep_ns;
+    static const int probe = env_int("SOS_GEMM_PROBE", 0);
+    a.probe = probe;
+    static const int kserp = env_int("SOS_KSERP", 1);
+    a.kserp = kserp;
     static unsigned long long* dbg = nullptr;
     if (env_int("SOS_GEMM_STATS", 0)) {
         if (!dbg) cudaMalloc(&dbg, 8 * sizeof(unsigned long long));

@@ -183,7 +183,11 @@ int sos_descend(sos_plan *plan, float *V_dev, const float *p_dev, int64_t steps,
  * losses (steps values, fp64) to losses_host.  Synchronous (legacy default
  * stream).  Uses the plan's optimiser settings (sos_opt_init must have been
  * called).  The device staging buffers (4*N*r + 4*M + 8*steps bytes) are kept by
- * the plan between calls; page-locked host buffers give full copy bandwidth. */
+ * the plan between calls; page-locked host buffers give full copy bandwidth.
+ * V comes back in row chunks (one per 8 x 256-row tile group) on a second
+ * stream while the last step's backward is still updating later rows: the
+ * update releases a chunk (device counter + cuStreamWaitValue32) once all its
+ * tiles are stored; without stream memory operations, one copy at the end. */
 int sos_solve_host(sos_plan *plan, float *V_host, const float *p_host, int64_t steps,
                    double *losses_host);
 

@@ -2,6 +2,7 @@
 // Argument checking, device memory ownership, launch sequencing.  Every
 // arithmetic step of the path runs in the kernels of sos_index.cu,
 // sos_pointwise.cu and sos_gemmq.cu; there is no host or CPU fallback.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -181,9 +182,12 @@ static size_t rlev_floats(const Index& ix) {
 // ------------------------------------------------------------------- plan --
 // CTA-pair tiles: a = 256-row block, b = 160-col block, grouped raster (8 row
 // blocks per group) so a wave of CTAs shares A and B panels in L2
-static void build_tiles(int64_t row_blocks, int64_t col_blocks, bool upper, std::vector<TileCoord>& out) {
+static int64_t tile_group() {
     const char* ga = getenv("SOS_TILE_GROUP");
-    const int64_t GA = ga && atoi(ga) > 0 ? atoi(ga) : 8;
+    return ga && atoi(ga) > 0 ? atoi(ga) : 8;
+}
+static void build_tiles(int64_t row_blocks, int64_t col_blocks, bool upper, std::vector<TileCoord>& out) {
+    const int64_t GA = tile_group();
     for (int64_t g0 = 0; g0 < row_blocks; g0 += GA) {
         const int64_t g1 = std::min(row_blocks, g0 + GA);
         for (int64_t b = 0; b < col_blocks; ++b)
@@ -217,6 +221,10 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     build_tiles(Np / kPairM, P.rowsVT / kTileN, false, tb);
     P.ntiles_fwd = (int)tf.size();
     P.ntiles_bwd = (int)tb.size();
+    // row chunks of the last step's V release = the raster's row groups
+    P.sig_blocks = (int)tile_group();
+    P.sig_expect.assign((size_t)((Np / kPairM + P.sig_blocks - 1) / P.sig_blocks), 0u);
+    for (const TileCoord& t : tb) P.sig_expect[t.a / P.sig_blocks] += 2;  // one per CTA of the pair
 
     if ((rc = dalloc(&P.d_vq, (size_t)kSlices * P.nkbV * P.rowsV * 64)) ||
         (rc = dalloc(&P.d_vtq, (size_t)kSlices * P.nkbN * P.rowsVT * 64)) ||
@@ -230,7 +238,8 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         (rc = dalloc(&P.d_ring, (size_t)sms * 2 * 128 * kTileN * 4)) ||
         (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) ||
         (rc = dalloc(&P.d_tiles_fwd, std::max<size_t>(1, tf.size()) * sizeof(TileCoord))) ||
-        (rc = dalloc(&P.d_tiles_bwd, std::max<size_t>(1, tb.size()) * sizeof(TileCoord)))) {
+        (rc = dalloc(&P.d_tiles_bwd, std::max<size_t>(1, tb.size()) * sizeof(TileCoord))) ||
+        (rc = dalloc(&P.d_rowsig, std::max<size_t>(1, P.sig_expect.size()) * sizeof(unsigned)))) {
         sos_plan_destroy(pl);
         return rc;
     }
@@ -288,6 +297,9 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_progress);
     cudaFree(P.d_tiles_fwd);
     cudaFree(P.d_tiles_bwd);
+    cudaFree(P.d_rowsig);
+    if (P.copy_st) cudaStreamDestroy(P.copy_st);
+    if (P.sig_ev) cudaEventDestroy(P.sig_ev);
     if (P.timing) {
         for (cudaEvent_t e : P.timing->pool) cudaEventDestroy(e);
         delete P.timing;
@@ -477,23 +489,33 @@ static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const fl
     return check_launch("descend step");
 }
 
-int sos_descend(sos_plan* pl, float* V_dev, const float* p_dev, int64_t steps, double* losses_dev, void* stream) {
-    if (!pl || !V_dev || !p_dev || steps < 0 || (steps > 0 && !losses_dev)) return fail(SOS_ERR_ARG, "bad argument");
-    Plan& P = pl->P;
-    if (!P.opt_ready) return fail(SOS_ERR_ARG, "sos_opt_init not called");
-    if (steps == 0) return SOS_OK;
-    cudaStream_t st = (cudaStream_t)stream;
+// K descent steps; with sig_last the final step runs outside the graph with the
+// row-chunk release of V on (P.d_rowsig zeroed, then P.sig_ev recorded, on st)
+static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps, double* losses_dev, cudaStream_t st,
+                        bool sig_last) {
     const DescendPtrs d = descend_ptrs(P);
+    auto plain_step = [&](int64_t t) -> int {
+        const bool sig = sig_last && t == steps - 1;
+        if (sig) {
+            CK(cudaMemsetAsync(P.d_rowsig, 0, P.sig_expect.size() * sizeof(unsigned), st));
+            CK(cudaEventRecord(P.sig_ev, st));
+        }
+        P.sig_on = sig;
+        const int r = descend_step(P, d, (int)(t & 1), V_dev, p_dev, losses_dev, st);
+        P.sig_on = false;
+        return r;
+    };
     int rc = upload_opt(P, st);
     if (rc) return rc;
     CK(cudaMemsetAsync(&P.d_opt->loss_idx, 0, sizeof(long long), st));
     // step 0 starts from the exact maxima and slices of the caller's V
     launch_pack_v(P, V_dev, st, d.vrowx[0], d.vcol[0]);
     CK(cudaMemcpyAsync(d.urow[0], d.vrowx[0], P.rowsV * 4, cudaMemcpyDeviceToDevice, st));
-    if ((rc = descend_step(P, d, 0, V_dev, p_dev, losses_dev, st))) return rc;
+    if ((rc = plain_step(0))) return rc;
     int64_t left = steps - 1;
     const bool timing = P.timing && P.timing->on;  // per-kernel events need plain launches
-    if (left >= 2 && !timing) {
+    const int64_t keep_plain = sig_last ? 1 : 0;      // the signalling step is never replayed
+    if (left >= 2 + keep_plain && !timing) {
         // steps 1, 2 (parities 1, 0) captured once as a graph, replayed for every pair
         const void* key[3] = {V_dev, p_dev, losses_dev};
         if (!P.gexec || memcmp(key, P.gkey, sizeof(key)) != 0) {
@@ -521,14 +543,38 @@ int sos_descend(sos_plan* pl, float* V_dev, const float* p_dev, int64_t steps, d
             cudaGraphDestroy(graph);
             memcpy(P.gkey, key, sizeof(key));
         }
-        for (; left >= 2; left -= 2) {
+        for (; left >= 2 + keep_plain; left -= 2) {
             CK(cudaGraphLaunch(P.gexec, st));
             P.launches += P.glaunches;
         }
     }
     for (int64_t t = steps - left; t < steps; ++t)
-        if ((rc = descend_step(P, d, (int)(t & 1), V_dev, p_dev, losses_dev, st))) return rc;
+        if ((rc = plain_step(t))) return rc;
     return SOS_OK;
+}
+
+int sos_descend(sos_plan* pl, float* V_dev, const float* p_dev, int64_t steps, double* losses_dev, void* stream) {
+    if (!pl || !V_dev || !p_dev || steps < 0 || (steps > 0 && !losses_dev)) return fail(SOS_ERR_ARG, "bad argument");
+    Plan& P = pl->P;
+    if (!P.opt_ready) return fail(SOS_ERR_ARG, "sos_opt_init not called");
+    if (steps == 0) return SOS_OK;
+    return descend_impl(P, V_dev, p_dev, steps, losses_dev, (cudaStream_t)stream, false);
+}
+
+// cuStreamWaitValue32 through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*PFN_wait_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_wait_value32 wait_value_fn() {
+    static PFN_wait_value32 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_wait_value32>(p);
+    }
+    return fn;
 }
 
 int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t steps, double* losses_host) {
@@ -545,18 +591,42 @@ int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t ste
         if ((rc = dalloc(&P.d_hl, sizeof(double) * steps))) return rc;
         P.hl_cap = steps;
     }
+    if (steps > 0 && !P.opt_ready) return fail(SOS_ERR_ARG, "sos_opt_init not called");
     cudaStream_t st = 0;
     rc = SOS_OK;
     if (cudaMemcpyAsync(P.d_hV, V_host, vb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
         cudaMemcpyAsync(P.d_hp, p_host, pb, cudaMemcpyHostToDevice, st) != cudaSuccess)
-        rc = fail(SOS_ERR_CUDA, "H2D copy");
-    if (!rc) rc = sos_descend(pl, P.d_hV, P.d_hp, steps, P.d_hl, st);
-    if (!rc && (cudaMemcpyAsync(V_host, P.d_hV, vb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-                (steps > 0 && cudaMemcpyAsync(losses_host, P.d_hl, sizeof(double) * steps, cudaMemcpyDeviceToHost, st) !=
-                                  cudaSuccess) ||
-                cudaStreamSynchronize(st) != cudaSuccess))
-        rc = fail(SOS_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
-    return rc;
+        return fail(SOS_ERR_CUDA, "H2D copy");
+    // ship V back in row chunks while the last step's backward still runs (needs
+    // stream memory operations; otherwise one copy after the last step)
+    const PFN_wait_value32 wait = steps > 0 ? wait_value_fn() : nullptr;
+    bool overlap = wait != nullptr;
+    if (overlap && !P.copy_st)
+        overlap = cudaStreamCreateWithFlags(&P.copy_st, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&P.sig_ev, cudaEventDisableTiming) == cudaSuccess;
+    if (steps > 0 && (rc = descend_impl(P, P.d_hV, P.d_hp, steps, P.d_hl, st, overlap))) return rc;
+    const int64_t N = P.idx->N, chunk_rows = (int64_t)P.sig_blocks * kPairM;
+    if (overlap) {
+        if (cudaStreamWaitEvent(P.copy_st, P.sig_ev, 0) != cudaSuccess)
+            return fail(SOS_ERR_CUDA, "copy stream wait");
+        for (size_t c = 0; c < P.sig_expect.size(); ++c) {
+            const int64_t r0 = (int64_t)c * chunk_rows, r1 = std::min(N, r0 + chunk_rows);
+            if (r1 <= r0) break;
+            if (wait(P.copy_st, (CUdeviceptr)(P.d_rowsig + c), P.sig_expect[c], CU_STREAM_WAIT_VALUE_GEQ) !=
+                    CUDA_SUCCESS ||
+                cudaMemcpyAsync(V_host + r0 * P.r, P.d_hV + r0 * P.r, (size_t)(r1 - r0) * P.r * 4,
+                                cudaMemcpyDeviceToHost, P.copy_st) != cudaSuccess)
+                return fail(SOS_ERR_CUDA, "chunked D2H of V");
+        }
+        // the fixup after the last update reads V only; the losses follow on st
+    } else if (cudaMemcpyAsync(V_host, P.d_hV, vb, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+        return fail(SOS_ERR_CUDA, "D2H copy");
+    }
+    if ((steps > 0 &&
+         cudaMemcpyAsync(losses_host, P.d_hl, sizeof(double) * steps, cudaMemcpyDeviceToHost, st) != cudaSuccess) ||
+        cudaStreamSynchronize(st) != cudaSuccess || (overlap && cudaStreamSynchronize(P.copy_st) != cudaSuccess))
+        return fail(SOS_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
+    return SOS_OK;
 }
 
 }  // extern "C"

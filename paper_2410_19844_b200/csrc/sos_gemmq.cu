@@ -84,6 +84,12 @@ struct GemmArgs {
     int64_t rowsVT;
     int64_t nkbN;
     const unsigned* vcol;
+    // kModeBwdUpdate, last step of sos_solve_host: after the update of a tile is
+    // stored, both CTAs of the pair add 1 to rowsig[tile.a / sig_blocks] (system
+    // scope) so a copy stream can ship finished row chunks of V while the rest runs
+    unsigned* rowsig;
+    int sig_blocks;
+    int sig_chunks;
 };
 
 // Adam / GD constants of this step, formed on the device from DevOpt
@@ -255,7 +261,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     constexpr bool kFwd = kMode == kModeFwd;
     // converged (sos_opt_set_stop): the whole grid leaves before any barrier,
     // TMEM or cluster work, so V and the optimiser state stay as they are
-    if (kMode == kModeBwdUpdate && descent_stopped(args.scal, args.opt, args.use_stop)) return;
+    if (kMode == kModeBwdUpdate && descent_stopped(args.scal, args.opt, args.use_stop)) {
+        if (args.rowsig && blockIdx.x == 0)  // nothing changes: release every chunk at once
+            for (int c = threadIdx.x; c < args.sig_chunks; c += blockDim.x) atomicExch(args.rowsig + c, kSigReleased);
+        return;
+    }
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
@@ -564,6 +574,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&gfree[slot]);
+            if (args.rowsig) {
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));  // both aux warps stored the tile
+                if (t == 0) {
+                    __threadfence_system();
+                    atomicAdd(args.rowsig + tc.a / args.sig_blocks, 1u);
+                }
+            }
         }
     }
 
@@ -740,6 +757,11 @@ void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBuf
     if (a.adam) {
         a.m = P.d_m;
         a.v = P.d_v;
+    }
+    if (P.sig_on) {
+        a.rowsig = P.d_rowsig;
+        a.sig_blocks = P.sig_blocks;
+        a.sig_chunks = (int)P.sig_expect.size();
     }
     LaunchScope ls(P, KK_GEMM_BWD, st);
     launchq<kModeBwdUpdate>(P, tm(P.tmap_rq_a), tm(P.tmap_vtq_b), a, st);

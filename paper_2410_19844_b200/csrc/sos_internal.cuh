@@ -108,7 +108,9 @@ struct Index {
     uint32_t* d_pt;            // pair-rank table PT (Np*Np)
 };
 
-struct TileCoord { int a; int b; };  // a: 256-row block (CTA pair), b: 160-col block
+struct TileCoord { int a; int b; };
+// rowsig value that satisfies every chunk's wait (cyclic >= compare of stream waits)
+constexpr unsigned kSigReleased = 0x40000000u;  // a: 256-row block (CTA pair), b: 160-col block
 
 struct Plan {
     const Index* idx;
@@ -150,6 +152,15 @@ struct Plan {
     float* d_hp;
     double* d_hl;
     int64_t hl_cap;
+    // sos_solve_host: the last step's update releases finished row chunks of V
+    // (rowsig[c] counts tile halves stored; chunk c = row blocks [c, c+1) x sig_blocks)
+    // and a copy stream ships each chunk to the host while the rest still runs
+    unsigned* d_rowsig;
+    int sig_blocks;
+    std::vector<uint32_t> sig_expect;
+    bool sig_on;
+    cudaStream_t copy_st;
+    cudaEvent_t sig_ev;
     int64_t launches;
     int num_sms;
     Timing* timing;

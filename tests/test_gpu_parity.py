@@ -198,6 +198,45 @@ def test_solve_host_matches_device_steps(sos):
     assert np.all(np.isfinite(losses)) and losses[-1] < losses[0]
 
 
+@pytest.mark.parametrize("steps", [1, 2, 3, 6])
+def test_solve_host_chunked_copy_matches_descend(sos, steps):
+    # N = 8855 rows -> 5 row chunks of V shipped by the copy stream during the
+    # last step's backward; steps 1..3 cover the graph / plain-step boundaries
+    n, d, r = 20, 4, 96
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    V0 = si.v0(ix.N, r, seed=3)
+    W = np.zeros((ix.N, r), np.float32)
+    W[:, :48] = si.planted_w(ix.N, 48, 4)  # zero columns leave coef(W W^T) unchanged
+    Wd = torch.from_numpy(W).cuda()
+    p = plan.forward(Wd).cpu().numpy()
+    plan.opt_init("adam", 1e-3)
+    Vh = V0.copy()
+    lh = plan.solve_host(Vh, p, steps)
+    plan.opt_init("adam", 1e-3)
+    Vd = torch.from_numpy(V0.copy()).cuda()
+    ld = plan.descend(Vd, torch.from_numpy(p).cuda(), steps).cpu().numpy()
+    assert not np.array_equal(Vh, V0)
+    assert rel_l2(Vh, Vd.cpu().numpy()) <= 1e-6
+    assert np.allclose(lh, ld, rtol=1e-5)
+
+
+def test_solve_host_stopped_releases_copy(sos):
+    # stopping rule already met: the update never runs, the copy stream must
+    # still be released (no hang) and V comes back unchanged
+    n, d, r = 20, 4, 96
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    V0 = si.v0(ix.N, r, seed=5)
+    p = plan.forward(torch.from_numpy(V0).cuda()).cpu().numpy() * 1.001
+    plan.opt_init("adam", 1e-3)
+    plan.set_stop(1e-2)
+    Vh = V0.copy()
+    losses = plan.solve_host(Vh, p, 4)
+    assert np.array_equal(Vh, V0)
+    assert np.all(np.isfinite(losses))
+
+
 # ---------------------------------------------------------------- full size --
 
 @pytest.fixture(scope="module", params=["c3_n12_2d12", si.BENCH_CONFIG])

@@ -252,6 +252,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     if (cudaMemset(P.d_vrow, 0, (size_t)P.rowsV * 4) != cudaSuccess ||
         cudaMemset(P.d_vcol, 0, (size_t)P.rowsVT * 4) != cudaSuccess ||
         cudaMemset(P.d_rrow, 0, (size_t)Np * 4) != cudaSuccess ||
+        cudaMemset(P.d_rq, 0, (size_t)kSlices * P.nkbN * Np * 64) != cudaSuccess ||  // padding rows stay 0
         cudaMemset(P.d_dbuf, 0, (size_t)(4 * P.rowsV + 2 * P.rowsVT) * 4) != cudaSuccess ||
         cudaMemset(P.d_opt, 0, sizeof(DevOpt)) != cudaSuccess) {
         sos_plan_destroy(pl);

@@ -223,6 +223,54 @@ __global__ void __launch_bounds__(256) k_pack_rq(const uint32_t* __restrict__ pt
     }
 }
 
+// R is symmetric (R_ij = res[rank(alpha_i + alpha_j)] = R_ji): one 64 x 64 block of
+// PT is read per unordered block pair {I <= J} and both RQ blocks -- rows of I at
+// K-block J and rows of J at K-block I (the transposed tile) -- are written from
+// it, so PT and the res gathers are read once for two blocks.  RQ rows at or
+// beyond nkb * 64 (padding of Np) are never written: zeroed at plan creation.
+__global__ void __launch_bounds__(256) k_pack_rq_sym(const uint32_t* __restrict__ pt, const float* __restrict__ res,
+                                                     int64_t Np, int64_t nkb, const unsigned* __restrict__ rrow,
+                                                     uint8_t* __restrict__ RQ, const Scalars* sc, const DevOpt* opt,
+                                                     int use_stop) {
+    if (descent_stopped(sc, opt, use_stop)) return;
+    __shared__ float tile[kPtW][kPtW + 1];  // [row in I][j in J], padded
+    const int t = threadIdx.x;
+    const int64_t npairs = nkb * (nkb + 1) / 2;
+    for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+        // pr enumerates the upper triangle column by column: J, then I = 0..J
+        int64_t J = (int64_t)((sqrt(8.0 * (double)pr + 1.0) - 1.0) * 0.5);
+        while (J * (J + 1) / 2 > pr) --J;
+        while ((J + 1) * (J + 2) / 2 <= pr) ++J;
+        const int64_t I = pr - J * (J + 1) / 2;
+        const uint32_t* p0 = pt + (J * Np + I * kPtW) * kPtW;  // 64 rows x 64 ranks, contiguous
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = (u * 256 + t) * 4;
+            const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + e));
+            float* d = &tile[e >> 6][e & 63];
+            d[0] = k.x != kInvalidRank ? __ldg(res + k.x) : 0.f;
+            d[1] = k.y != kInvalidRank ? __ldg(res + k.y) : 0.f;
+            d[2] = k.z != kInvalidRank ? __ldg(res + k.z) : 0.f;
+            d[3] = k.w != kInvalidRank ? __ldg(res + k.w) : 0.f;
+        }
+        __syncthreads();
+        const int r = t >> 2, c = t & 3;
+        float x[16];
+        uint4 q[3];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[e] = tile[r][c * 16 + e];
+        slice16(x, slice_scale(__ldg(rrow + I * kPtW + r)), q);
+        store_q16(RQ, J, I * kPtW + r, c, nkb, Np, q);
+        if (I != J) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = tile[c * 16 + e][r];
+            slice16(x, slice_scale(__ldg(rrow + J * kPtW + r)), q);
+            store_q16(RQ, I, J * kPtW + r, c, nkb, Np, q);
+        }
+        __syncthreads();
+    }
+}
+
 // ----------------------------------------------------- fused row packers ----
 // One pass per row: a block stages a whole row in shared memory (contiguous
 // loads for V, gathers through PT for R), reduces the row maximum, then slices
@@ -408,6 +456,14 @@ void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop) {
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     const int64_t Np = P.idx->Np;
     LaunchScope ls(P, KK_PACK_R, st);
+    static const bool sym = !getenv("SOS_RPACK_SYM") || atoi(getenv("SOS_RPACK_SYM"));
+    if (sym) {
+        const int64_t npairs = P.nkbN * (P.nkbN + 1) / 2;
+        const unsigned blocks = (unsigned)std::min<int64_t>(npairs, (int64_t)P.num_sms * 8);
+        k_pack_rq_sym<<<blocks, 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow, P.d_rq, P.d_scal, P.d_opt,
+                                              use_stop);
+        return;
+    }
     k_pack_rq<<<grid_for(P, P.nkbN * (Np / 8) * 32, 256), 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow, P.d_rq,
                                                                        P.d_scal, P.d_opt, use_stop);
 }

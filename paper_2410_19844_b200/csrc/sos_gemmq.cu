@@ -324,7 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 const bool rev = args.kserp && (it & 1);
                 const int32_t rowA = tc.a * kPairM + (int)rank * 128;
                 const int32_t rowB = tc.b * kTileN + (int)rank * kHalfN;
-                for (int kb = 0; kb < args.num_kb; ++kb, ++g) {
+                for (int kb = tc.kb0; kb < tc.kb1; ++kb, ++g) {
                     // Bounded K-skew: every kSkewEpoch K-blocks the producer publishes its
                     // progress and waits (bounded) while it is more than kSkewLag epochs
                     // ahead of the grid, so the CTAs of a wave stream the same K-slabs of
@@ -352,7 +352,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                         const bool skipB = args.probe == 4 && g >= kStages;
                         if (leader) mbar_arrive_expect_tx(&full[stage], skipB ? 2 * kABytes : 2 * kStageBytes);
                         // the tensor maps view 4 consecutive 64-byte Q-rows as one 256-byte row
-                        const int kq = args.probe ? (kb & 7) : rev ? args.num_kb - 1 - kb : kb;
+                        const int kq = args.probe ? (kb & 7) : rev ? tc.kb0 + tc.kb1 - 1 - kb : kb;
                         const int32_t ra = args.probe >= 2 ? (int32_t)rank * 128 : rowA;
                         const int32_t rb = args.probe >= 2 ? (int32_t)rank * kHalfN : rowB;
                         tma_load_3d_2sm(sa, &tmA, &full[stage], 0, (int32_t)((kq * args.a_rows + ra) >> 2), 0);
@@ -381,8 +381,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             uint32_t phase = 0;
             uint32_t acc_phase = 0;
             for (int tile = cid; tile < args.ntiles; tile += ncl) {
-                for (int kb0 = 0; kb0 < args.num_kb; kb0 += args.seg_kb) {
-                    const int kb1 = min(args.num_kb, kb0 + args.seg_kb);
+                const TileCoord tc = args.tiles[tile];
+                for (int kb0 = tc.kb0; kb0 < tc.kb1; kb0 += args.seg_kb) {
+                    const int kb1 = min(tc.kb1, kb0 + args.seg_kb);
                     {
                         const long long c0 = clock64();
                         mbar_wait_cluster(tempty, acc_phase ^ 1);
@@ -442,7 +443,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             float sum[kEpiCols];
 #pragma unroll
             for (int t = 0; t < kEpiCols; ++t) sum[t] = 0.f;
-            for (int kb0 = 0; kb0 < args.num_kb; kb0 += args.seg_kb) {
+            for (int kb0 = tc.kb0; kb0 < tc.kb1; kb0 += args.seg_kb) {
                 mbar_wait(tfull, acc_phase);
                 tc_fence_after();
                 const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + h * kEpiCols;

@@ -108,7 +108,9 @@ struct Index {
     uint32_t* d_pt;            // pair-rank table PT (Np*Np)
 };
 
-struct TileCoord { int a; int b; };
+// a: 256-row block (CTA pair), b: 160-col block, K-blocks [kb0, kb1) of the tile
+// (shorter than the whole K only in the forward's split last wave)
+struct TileCoord { int a; int b; int kb0; int kb1; };
 // rowsig value that satisfies every chunk's wait (cyclic >= compare of stream waits)
 constexpr unsigned kSigReleased = 0x40000000u;  // a: 256-row block (CTA pair), b: 160-col block
 

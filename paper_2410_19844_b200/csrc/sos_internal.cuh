@@ -63,8 +63,8 @@ constexpr int kAuxWarps = 2;      // optimiser-update / V^T-pack warps of the GE
 constexpr int kGemmThreads = 64 + 32 * (kEpiWarps + kAuxWarps);  // producer, MMA, epilogue, aux
 constexpr int kPtW = 64;          // pair-rank table chunk width (columns j per [jb][i] row)
 // bounded K-skew between the CTAs of a GEMM (see the producer in sos_gemmq.cu)
-constexpr int kSkewEpoch = 4;     // K-blocks (of 64) per progress epoch (tools/gpu_tune2.sh)
-constexpr int kSkewLag = 2;       // epochs a CTA may run ahead of the slowest
+constexpr int kSkewEpoch = 8;     // K-blocks (of 64) per progress epoch (tools/gpu_skew2.sh)
+constexpr int kSkewLag = 1;       // epochs a CTA may run ahead of the slowest
 constexpr int kSkewMaxSpin = 8192;  // bounded wait (polls): a locality hint, never a deadlock
 constexpr uint32_t kInvalidRank = 0xFFFFFFFFu;
 constexpr int kMaxVars = 255;     // n + 2d <= 255 (variable indices are uint8)

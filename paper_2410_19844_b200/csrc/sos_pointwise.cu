@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(256) k_pack_rq(const uint32_t* __restrict__ pt
 // K-block J and rows of J at K-block I (the transposed tile) -- are written from
 // it, so PT and the res gathers are read once for two blocks.  RQ rows at or
 // beyond nkb * 64 (padding of Np) are never written: zeroed at plan creation.
-__global__ void __launch_bounds__(256) k_pack_rq_sym(const uint32_t* __restrict__ pt, const float* __restrict__ res,
+__global__ void __launch_bounds__(256, 6) k_pack_rq_sym(const uint32_t* __restrict__ pt, const float* __restrict__ res,
                                                      int64_t Np, int64_t nkb, const unsigned* __restrict__ rrow,
                                                      uint8_t* __restrict__ RQ, const Scalars* sc, const DevOpt* opt,
                                                      int use_stop) {

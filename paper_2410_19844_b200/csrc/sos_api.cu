@@ -199,23 +199,6 @@ static void build_tiles(int64_t row_blocks, int64_t col_blocks, bool upper, std:
     }
 }
 
-// The persistent GEMM hands tile k to CTA pair k mod pairs.  When the forward's
-// last wave is at most half full, its tiles are split into s K-ranges (the
-// epilogue adds partial Gram sums into coef with atomics, so the split is exact
-// up to fp32 summation order): the wave then takes 1/s of a tile time.
-static void split_last_wave(std::vector<TileCoord>& t, int pairs, int nkb) {
-    const char* e = getenv("SOS_FWD_SPLIT");
-    if ((e && !atoi(e)) || pairs <= 0) return;
-    const int64_t n = (int64_t)t.size(), rem = n % pairs;
-    if (n <= pairs || rem == 0 || 2 * rem > pairs) return;
-    const int s = (int)std::min<int64_t>(std::min<int64_t>(pairs / rem, 4), nkb);
-    if (s < 2) return;
-    std::vector<TileCoord> tail(t.end() - rem, t.end());
-    t.resize(n - rem);
-    for (const TileCoord& c : tail)
-        for (int p = 0; p < s; ++p) t.push_back(TileCoord{c.a, c.b, (int)((int64_t)nkb * p / s), (int)((int64_t)nkb * (p + 1) / s)});
-}
-
 int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     if (!h || !out || r < 1) return fail(SOS_ERR_ARG, "bad argument");
     *out = nullptr;
@@ -238,7 +221,6 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     build_tiles(Np / kPairM, P.rowsVT / kTileN, false, tb);
     for (TileCoord& t : tf) t.kb1 = (int)P.nkbV;
     for (TileCoord& t : tb) t.kb1 = (int)P.nkbN;
-    split_last_wave(tf, sms / 2, (int)P.nkbV);
     P.ntiles_fwd = (int)tf.size();
     P.ntiles_bwd = (int)tb.size();
     // row chunks of the last step's V release = the raster's row groups

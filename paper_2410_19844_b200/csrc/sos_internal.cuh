@@ -109,7 +109,8 @@ struct Index {
 };
 
 // a: 256-row block (CTA pair), b: 160-col block, K-blocks [kb0, kb1) of the tile
-// (shorter than the whole K only in the forward's split last wave)
+// (the whole K today; splitting half-empty last waves in K measured no gain
+// under the power cap, profiles/r1_fwd_split_ab.log)
 struct TileCoord { int a; int b; int kb0; int kb1; };
 // rowsig value that satisfies every chunk's wait (cyclic >= compare of stream waits)
 constexpr unsigned kSigReleased = 0x40000000u;  // a: 256-row block (CTA pair), b: 160-col block

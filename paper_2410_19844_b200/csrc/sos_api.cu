@@ -186,15 +186,26 @@ static int64_t tile_group() {
     const char* ga = getenv("SOS_TILE_GROUP");
     return ga && atoi(ga) > 0 ? atoi(ga) : 8;
 }
-static void build_tiles(int64_t row_blocks, int64_t col_blocks, bool upper, std::vector<TileCoord>& out) {
+static int round_up32(int64_t x) { return (int)std::max<int64_t>(32, (x + 31) / 32 * 32); }
+
+// forward: upper triangle of the Gram matrix (columns j >= rows' block start);
+// backward: all of R V.  Columns tiled on the 160 grid; see TileCoord for the
+// narrow tiles
+static void build_tiles(int64_t row_blocks, int64_t ncols, bool upper, std::vector<TileCoord>& out) {
     const int64_t GA = tile_group();
+    const int64_t col_blocks = (ncols + kTileN - 1) / kTileN;
+    static const bool narrow = !getenv("SOS_NARROW_TILES") || atoi(getenv("SOS_NARROW_TILES"));
     for (int64_t g0 = 0; g0 < row_blocks; g0 += GA) {
         const int64_t g1 = std::min(row_blocks, g0 + GA);
         for (int64_t b = 0; b < col_blocks; ++b)
             for (int64_t a = g0; a < g1; ++a) {
-                // forward: keep the tile iff it holds some (i, j) with j >= i
-                if (upper && b * kTileN + kTileN - 1 < a * kPairM) continue;
-                out.push_back(TileCoord{(int)a, (int)b, 0, 0});
+                int64_t c_start = b * kTileN, c_end = std::min(ncols, c_start + kTileN);
+                if (upper) {
+                    if (c_end <= a * kPairM) continue;              // wholly below the diagonal block
+                    c_start = std::max(c_start, a * kPairM);        // skip columns left of it
+                }
+                if (!narrow) c_start = b * kTileN, c_end = c_start + kTileN;  // A/B: full 160-wide grid tiles
+                out.push_back(TileCoord{(int)a, (int)c_start, round_up32(c_end - c_start), 0});
             }
     }
 }
@@ -217,10 +228,8 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     P.rowsVT = ((r + kTileN - 1) / kTileN) * kTileN;
     P.nkbN = (N + kQK - 1) / kQK;  // K = j runs over the N monomials (rows stay padded to Np)
     std::vector<TileCoord> tf, tb;
-    build_tiles(Np / kPairM, colBlocksV, true, tf);
-    build_tiles(Np / kPairM, P.rowsVT / kTileN, false, tb);
-    for (TileCoord& t : tf) t.kb1 = (int)P.nkbV;
-    for (TileCoord& t : tb) t.kb1 = (int)P.nkbN;
+    build_tiles(Np / kPairM, N, true, tf);
+    build_tiles(Np / kPairM, r, false, tb);
     P.ntiles_fwd = (int)tf.size();
     P.ntiles_bwd = (int)tb.size();
     // row chunks of the last step's V release = the raster's row groups

@@ -323,8 +323,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 // wave loaded last, still in L2 (-1.4 % step time, profiles/r1_l2_probes.md)
                 const bool rev = args.kserp && (it & 1);
                 const int32_t rowA = tc.a * kPairM + (int)rank * 128;
-                const int32_t rowB = tc.b * kTileN + (int)rank * kHalfN;
-                for (int kb = tc.kb0; kb < tc.kb1; ++kb, ++g) {
+                const int32_t rowB = tc.c0 + (int)rank * (tc.nb >> 1);  // each CTA supplies nb/2 B rows
+                for (int kb = 0; kb < args.num_kb; ++kb, ++g) {
                     // Bounded K-skew: every kSkewEpoch K-blocks the producer publishes its
                     // progress and waits (bounded) while it is more than kSkewLag epochs
                     // ahead of the grid, so the CTAs of a wave stream the same K-slabs of
@@ -352,7 +352,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                         const bool skipB = args.probe == 4 && g >= kStages;
                         if (leader) mbar_arrive_expect_tx(&full[stage], skipB ? 2 * kABytes : 2 * kStageBytes);
                         // the tensor maps view 4 consecutive 64-byte Q-rows as one 256-byte row
-                        const int kq = args.probe ? (kb & 7) : rev ? tc.kb0 + tc.kb1 - 1 - kb : kb;
+                        const int kq = args.probe ? (kb & 7) : rev ? args.num_kb - 1 - kb : kb;
                         const int32_t ra = args.probe >= 2 ? (int32_t)rank * 128 : rowA;
                         const int32_t rb = args.probe >= 2 ? (int32_t)rank * kHalfN : rowB;
                         tma_load_3d_2sm(sa, &tmA, &full[stage], 0, (int32_t)((kq * args.a_rows + ra) >> 2), 0);
@@ -372,7 +372,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         // commits.  A single-lane loop spent ~15 % of the tensor pipe on issue.
         if (leader) {
             const long long t_start = clock64();
-            constexpr uint32_t idesc = umma_idesc_s8_s32(kPairM, kTileN);
             const uint32_t d0 = tbase, d1 = tbase + kTileN, d2 = tbase + 2 * kTileN;
             // descriptor of stage 0, slice 0; other operands differ only in the
             // start-address field (bits 0-13, 16-byte units)
@@ -381,9 +380,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             uint32_t phase = 0;
             uint32_t acc_phase = 0;
             for (int tile = cid; tile < args.ntiles; tile += ncl) {
-                const TileCoord tc = args.tiles[tile];
-                for (int kb0 = tc.kb0; kb0 < tc.kb1; kb0 += args.seg_kb) {
-                    const int kb1 = min(tc.kb1, kb0 + args.seg_kb);
+                const uint32_t idesc = umma_idesc_s8_s32(kPairM, args.tiles[tile].nb);
+                for (int kb0 = 0; kb0 < args.num_kb; kb0 += args.seg_kb) {
+                    const int kb1 = min(args.num_kb, kb0 + args.seg_kb);
                     {
                         const long long c0 = clock64();
                         mbar_wait_cluster(tempty, acc_phase ^ 1);
@@ -443,12 +442,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             float sum[kEpiCols];
 #pragma unroll
             for (int t = 0; t < kEpiCols; ++t) sum[t] = 0.f;
-            for (int kb0 = tc.kb0; kb0 < tc.kb1; kb0 += args.seg_kb) {
+            const int ncol = min(kEpiCols, tc.nb - h * kEpiCols);  // this warp's live columns (<= 0: none)
+            for (int kb0 = 0; kb0 < args.num_kb; kb0 += args.seg_kb) {
                 mbar_wait(tfull, acc_phase);
                 tc_fence_after();
                 const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + h * kEpiCols;
 #pragma unroll
                 for (int ch = 0; ch < kEpiCols / 16; ++ch) {
+                    if (ch * 16 >= ncol) break;  // warp-uniform
                     uint32_t v0[16], v1[16], v2[16];
                     tmem_ld16(tq + ch * 16, v0);
                     tmem_ld16(tq + kTileN + ch * 16, v1);
@@ -464,16 +465,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 if (lane == 0) mbar_arrive_cluster(tempty, 0);
                 acc_phase ^= 1;
             }
-            const int64_t cbase = (int64_t)tc.b * kTileN + h * kEpiCols;
+            const int64_t cbase = (int64_t)tc.c0 + h * kEpiCols;
             const float ui = slice_unit(__ldg(args.umaxA + i));
             if (kFwd) {
-                // rows [256a, 256a+256) vs cols [160b, 160b+160): all above the diagonal iff 160b >= 256a + 256
-                const bool strictly_upper = (int64_t)tc.b * kTileN >= (int64_t)tc.a * kPairM + kPairM;
+                // rows [256a, 256a+256) vs cols [c0, c0+nb): all above the diagonal iff c0 >= 256a + 256
+                const bool strictly_upper = (int64_t)tc.c0 >= (int64_t)tc.a * kPairM + kPairM;
                 if (i < args.N) {
 #pragma unroll
                     for (int ch = 0; ch < kEpiCols / 16; ++ch) {
                         const int64_t c0 = cbase + ch * 16;
-                        if (c0 >= args.N) break;
+                        if (ch * 16 >= ncol || c0 >= args.N) break;
                         const uint4* prow = reinterpret_cast<const uint4*>(
                             args.pt + ((c0 / kPtW) * args.Np + i) * kPtW + (c0 % kPtW));
                         const uint4* pu = reinterpret_cast<const uint4*>(args.umaxB + c0);
@@ -515,6 +516,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 const float s4 = 4.f * ui;
 #pragma unroll
                 for (int u = 0; u < kEpiCols / 4; ++u) {
+                    if (4 * u >= ncol) break;
                     const int64_t c0 = cbase + 4 * u;
                     const uint4 ub = __ldg(reinterpret_cast<const uint4*>(args.umaxB + cbase) + u);
                     const float o[4] = {s4 * slice_unit(ub.x) * sum[4 * u], s4 * slice_unit(ub.y) * sum[4 * u + 1],
@@ -569,9 +571,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     for (int e = t; e < 128; e += 32 * kAuxWarps) rmax_s[e] = 0u;
                     asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
                 }
-                update_tile_q(args, oc, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.b * kTileN, t, stg, rmax_s);
+                update_tile_q(args, oc, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.c0, t, stg, rmax_s);
             } else {
-                update_tile(args, oc, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.b * kTileN, t);
+                update_tile(args, oc, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.c0, t);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&gfree[slot]);

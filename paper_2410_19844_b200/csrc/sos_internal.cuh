@@ -108,10 +108,13 @@ struct Index {
     uint32_t* d_pt;            // pair-rank table PT (Np*Np)
 };
 
-// a: 256-row block (CTA pair), b: 160-col block, K-blocks [kb0, kb1) of the tile
-// (the whole K today; splitting half-empty last waves in K measured no gain
-// under the power cap, profiles/r1_fwd_split_ab.log)
-struct TileCoord { int a; int b; int kb0; int kb1; };
+// One CTA-pair output tile: rows [256a, 256a + 256) x columns [c0, c0 + nb).
+// nb = 160 except where a narrower tile (multiple of 32) stops the MMAs from
+// computing columns nobody needs: the last column block (r or N not a multiple
+// of 160) and, in the forward, the diagonal tile of each row block (c0 = 256a
+// instead of the 160-grid line below it).  The MMA N and the B rows each CTA
+// supplies (nb / 2) follow nb; the epilogue ignores accumulator columns >= nb.
+struct TileCoord { int a; int c0; int nb; int pad; };
 // rowsig value that satisfies every chunk's wait (cyclic >= compare of stream waits)
 constexpr unsigned kSigReleased = 0x40000000u;  // a: 256-row block (CTA pair), b: 160-col block
 

@@ -1,0 +1,28 @@
+"""Device time per descent step for an arbitrary (n, d, r) (planted target, Adam):
+python tools/time_shape.py n d r [steps]"""
+import os, sys
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import seeded_inputs as si
+import paper_2410_19844_b200 as sos
+
+n, d, r = (int(x) for x in sys.argv[1:4])
+steps = int(sys.argv[4]) if len(sys.argv) > 4 else 20
+ix = sos.SosIndex(n, d)
+plan = sos.SosPlan(ix, r)
+rs = max(1, ix.N // 2)
+W = torch.zeros(ix.N, r, device="cuda")
+W[:, : min(r, rs)] = torch.from_numpy(si.planted_w(ix.N, min(r, rs), 1)).cuda()
+p = plan.forward(W)
+V = torch.from_numpy(si.v0(ix.N, r, 0)).cuda()
+plan.opt_init("adam", 1e-4)
+plan.descend(V, p, 4)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+plan.descend(V, p, steps)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / steps
+print(f"n={n} d={d} N={ix.N} r={r} ms/step={ms:.3f} steps/s={1e3 / ms:.3f}")

@@ -45,7 +45,7 @@ struct GemmArgs {
     int64_t b_rows;   // rows_total of the B Q-layout
     int num_kb;       // K-blocks of 64
     int seg_kb;       // K-blocks per exact s32 TMEM segment
-    const TileCoord* tiles;  // (256-row block, 160-col block)
+    const TileCoord* tiles;  // 256 rows x nb (<= 160) columns each
     int ntiles;
     const unsigned* umaxA;  // row maxima (float bits) of the A operand rows
     const unsigned* umaxB;  // row maxima of the B operand rows

@@ -14,7 +14,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
     "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
-]
+] + os.environ.get("SOS_NVCC_EXTRA", "").split()  # experiments only (e.g. -DSOS_UROWS=2)
 
 
 def _stale() -> bool:

@@ -163,6 +163,10 @@ __device__ __forceinline__ void update_tile(const GemmArgs& a, const OptConsts& 
 // row maximum stays in [1/2, 2] of the old one (k_descend_fixup re-slices the
 // rare rows that leave that window, see sos_pointwise.cu).
 constexpr int kQRows = 16;  // rows per staged batch
+#ifndef SOS_UROWS
+#define SOS_UROWS 4
+#endif
+constexpr int kURows = SOS_UROWS;  // rows whose loads are in flight together (latency-bound loop)
 __device__ __forceinline__ void update_tile_q(const GemmArgs& a, const OptConsts& o, const float* __restrict__ gt,
                                               int64_t row0,
                                               int64_t col0, int t, float* stage, unsigned* rmax_s) {
@@ -173,12 +177,12 @@ __device__ __forceinline__ void update_tile_q(const GemmArgs& a, const OptConsts
         if (row0 + rb >= a.N) break;
         // (A) update, thread = column
 #pragma unroll 1
-        for (int rr = rb; rr < rb + kQRows; rr += 2) {
-            float gv[2][3], x[2][3], mm[2][3], vv[2][3];
-            int64_t off[2][3];
-            bool ok[2][3];
+        for (int rr = rb; rr < rb + kQRows; rr += kURows) {
+            float gv[kURows][3], x[kURows][3], mm[kURows][3], vv[kURows][3];
+            int64_t off[kURows][3];
+            bool ok[kURows][3];
 #pragma unroll
-            for (int k = 0; k < 2; ++k)
+            for (int k = 0; k < kURows; ++k)
 #pragma unroll
                 for (int e = 0; e < 3; ++e) {
                     const int c = t + 64 * e;
@@ -193,7 +197,7 @@ __device__ __forceinline__ void update_tile_q(const GemmArgs& a, const OptConsts
                     }
                 }
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
+            for (int k = 0; k < kURows; ++k) {
                 float m = 0.f;
 #pragma unroll
                 for (int e = 0; e < 3; ++e) {

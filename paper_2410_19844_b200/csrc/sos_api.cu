@@ -246,7 +246,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         (rc = dalloc(&P.d_opt, sizeof(DevOpt))) ||
         (rc = dalloc(&P.d_rlev, std::max<size_t>(1, rlev_floats(h->ix)) * sizeof(float))) ||
         (rc = dalloc(&P.d_res, (size_t)M * 4)) || (rc = dalloc(&P.d_scal, sizeof(Scalars))) ||
-        (rc = dalloc(&P.d_ring, (size_t)sms * 2 * 128 * kTileN * 4)) ||
+        (rc = dalloc(&P.d_ring, (size_t)sms * 128 * kTileN * 4)) ||
         (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) ||
         (rc = dalloc(&P.d_tiles_fwd, std::max<size_t>(1, tf.size()) * sizeof(TileCoord))) ||
         (rc = dalloc(&P.d_tiles_bwd, std::max<size_t>(1, tb.size()) * sizeof(TileCoord))) ||

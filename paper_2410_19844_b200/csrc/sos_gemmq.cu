@@ -24,13 +24,15 @@
 //               the MMAs.  Both run as whole warps over warp-uniform state and issue
 //               from one elect.sync lane (a single-lane loop cost ~15 % of the
 //               tensor pipe in R2UR / BRA.U.ANY sequences)
-//   warps 2..9  epilogue: TMEM lane quarter (warp & 3) x column half (80 columns)
-//   warps 10,11 aux: forward -> pack V^T slices for the backward that follows;
-//               backward in sos_step / sos_descend -> optimiser update from the
-//               gradient-tile ring (and, in sos_descend, the next step's V slices)
+//   warps 2..9  epilogue: TMEM lane quarter (warp & 3) x column half (80 columns);
+//               in sos_step / sos_descend they also apply the optimiser update to
+//               the drained tile (and write the next step's V slices) while the
+//               tensor cores work on the next tile
+//   warps 10,11 aux: forward -> pack V^T slices for the backward that follows
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -62,7 +64,7 @@ struct GemmArgs {
     int kserp;                 // walk K backwards on odd local tiles (L2 reuse across waves)
     int probe;                 // SOS_GEMM_PROBE (experiment, wrong results): 1 = K-blocks mod 8, 2 = also tile 0, 4 = 2 with B loaded only on the first ring pass
     // kModeBwdUpdate: the optimiser step of PAPER.md:221, applied by the aux warps
-    float* ring;  // per-CTA ring of 2 finished gradient tiles (128 x 160 fp32 each)
+    float* ring;  // per-CTA staging of the finished gradient tile (128 x 160 fp32, L2-resident)
     float* V;
     float* m;
     float* v;
@@ -114,149 +116,122 @@ constexpr uint32_t kSmemBytes = kStages * kStageBytes + kBarBytes + kAuxSmemByte
 constexpr float kInv256 = 1.f / 256.f;
 constexpr float kInv65536 = 1.f / 65536.f;
 
-// aux warps: one optimiser step on a finished 128 x 160 gradient tile
-// (coalesced: 64 threads cover consecutive columns of one row per access)
-__device__ __forceinline__ void update_tile(const GemmArgs& a, const OptConsts& o, const float* __restrict__ gt,
-                                            int64_t row0,
-                                            int64_t col0, int t) {
-#pragma unroll 1
-    for (int rr = 0; rr < 128; ++rr) {
-        const int64_t i = row0 + rr;
-        if (i >= a.N) break;
-        float gv[3], x[3], mm[3], vv[3];
-        int64_t off[3];
-        bool ok[3];
-#pragma unroll
-        for (int e = 0; e < 3; ++e) {
-            const int c = t + 64 * e;
-            ok[e] = c < kTileN && col0 + c < a.r;
-            off[e] = i * a.r + col0 + c;
-            gv[e] = ok[e] ? __ldcg(gt + rr * kTileN + c) : 0.f;
-            x[e] = ok[e] ? a.V[off[e]] : 0.f;
-            if (a.adam) {
-                mm[e] = ok[e] ? a.m[off[e]] : 0.f;
-                vv[e] = ok[e] ? a.v[off[e]] : 0.f;
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < 3; ++e) {
-            if (!ok[e]) continue;
-            if (a.adam) {
-                mm[e] = o.b1 * mm[e] + (1.f - o.b1) * gv[e];
-                vv[e] = o.b2 * vv[e] + (1.f - o.b2) * gv[e] * gv[e];
-                a.m[off[e]] = mm[e];
-                a.v[off[e]] = vv[e];
-                a.V[off[e]] = x[e] - o.lr_c1 * mm[e] / (sqrtf(vv[e]) * o.inv_sqrt_c2 + o.eps);
-            } else {
-                a.V[off[e]] = x[e] - o.lr * gv[e];
-            }
-        }
-    }
-}
+constexpr int kQRows = 16;  // rows per staged batch of the update
 
-// aux warps inside sos_descend: the optimiser step on a finished 128 x 160
-// gradient tile, plus the next step's V slices and maxima.  Batches of 16 rows:
-// (A) the update itself with thread = column (coalesced, as update_tile), the
-// new values staged in shared memory, column maxima in registers, row maxima
-// warp-reduced; (B) the staged rows sliced 16 columns at a time into VQ.  The
-// slices use the scale kHeadroom * max|row of the current V|, valid while the
-// row maximum stays in [1/2, 2] of the old one (k_descend_fixup re-slices the
-// rare rows that leave that window, see sos_pointwise.cu).
-constexpr int kQRows = 16;  // rows per staged batch
-#ifndef SOS_UROWS
-#define SOS_UROWS 4
-#endif
-constexpr int kURows = SOS_UROWS;  // rows whose loads are in flight together (latency-bound loop)
-__device__ __forceinline__ void update_tile_q(const GemmArgs& a, const OptConsts& o, const float* __restrict__ gt,
-                                              int64_t row0,
-                                              int64_t col0, int t, float* stage, unsigned* rmax_s) {
-    const int lane = t & 31, w = t >> 5;
-    float cm[3] = {0.f, 0.f, 0.f};
+// The optimiser step on a finished 128 x 160 gradient tile (ring slot gt) by the
+// 8 epilogue warps, right after they drained it (the tensor cores already work
+// on the next tile).  Batches of 16 rows: warp w owns rows 2w, 2w+1 of a batch,
+// lane l the columns l + 32e (e < 5): every access is a coalesced row segment,
+// all 40 loads of a thread are in flight together, and a thread keeps the same
+// 5 columns for the whole tile (column maxima in registers).  Inside
+// sos_descend (vq_next) the new rows are staged in shared memory and sliced
+// into the next step's VQ with the scale kHeadroom * max|row of the current V|,
+// valid while the row maximum stays in [1/2, 2] of the old one (k_descend_fixup
+// re-slices the rare rows that leave that window, see sos_pointwise.cu).
+constexpr int kEpiThreads = 32 * kEpiWarps;
+__device__ __forceinline__ void update_tile_epi(const GemmArgs& a, const OptConsts& o, const float* __restrict__ gt,
+                                                int64_t row0, int64_t col0, int w, int lane, float* stage) {
+    constexpr int kE = kTileN / 32;  // columns per lane
+    const bool q = a.vq_next != nullptr;
+    float cm[kE];
+#pragma unroll
+    for (int e = 0; e < kE; ++e) cm[e] = 0.f;
 #pragma unroll 1
     for (int rb = 0; rb < 128; rb += kQRows) {
         if (row0 + rb >= a.N) break;
-        // (A) update, thread = column
-#pragma unroll 1
-        for (int rr = rb; rr < rb + kQRows; rr += kURows) {
-            float gv[kURows][3], x[kURows][3], mm[kURows][3], vv[kURows][3];
-            int64_t off[kURows][3];
-            bool ok[kURows][3];
+        float gv[2][kE], x[2][kE], mm[2][kE], vv[2][kE];
+        int64_t off[2][kE];
+        bool ok[2][kE];
 #pragma unroll
-            for (int k = 0; k < kURows; ++k)
+        for (int k = 0; k < 2; ++k)
 #pragma unroll
-                for (int e = 0; e < 3; ++e) {
-                    const int c = t + 64 * e;
-                    const int64_t i = row0 + rr + k;
-                    ok[k][e] = c < kTileN && col0 + c < a.r && i < a.N;
-                    off[k][e] = i * a.r + col0 + c;
-                    gv[k][e] = ok[k][e] ? __ldcg(gt + (rr + k) * kTileN + c) : 0.f;
-                    x[k][e] = ok[k][e] ? __ldcs(a.V + off[k][e]) : 0.f;
-                    if (a.adam) {
-                        mm[k][e] = ok[k][e] ? __ldcs(a.m + off[k][e]) : 0.f;
-                        vv[k][e] = ok[k][e] ? __ldcs(a.v + off[k][e]) : 0.f;
-                    }
+            for (int e = 0; e < kE; ++e) {
+                const int c = lane + 32 * e, rr = rb + 2 * w + k;
+                const int64_t i = row0 + rr;
+                ok[k][e] = col0 + c < a.r && i < a.N;
+                off[k][e] = i * a.r + col0 + c;
+                gv[k][e] = ok[k][e] ? __ldcg(gt + rr * kTileN + c) : 0.f;
+                x[k][e] = ok[k][e] ? __ldcs(a.V + off[k][e]) : 0.f;
+                if (a.adam) {
+                    mm[k][e] = ok[k][e] ? __ldcs(a.m + off[k][e]) : 0.f;
+                    vv[k][e] = ok[k][e] ? __ldcs(a.v + off[k][e]) : 0.f;
                 }
+            }
 #pragma unroll
-            for (int k = 0; k < kURows; ++k) {
-                float m = 0.f;
+        for (int k = 0; k < 2; ++k) {
+            float m = 0.f;
 #pragma unroll
-                for (int e = 0; e < 3; ++e) {
-                    const int c = t + 64 * e;
-                    float xn = 0.f;
-                    if (ok[k][e]) {
-                        if (a.adam) {
-                            mm[k][e] = o.b1 * mm[k][e] + (1.f - o.b1) * gv[k][e];
-                            vv[k][e] = o.b2 * vv[k][e] + (1.f - o.b2) * gv[k][e] * gv[k][e];
-                            xn = x[k][e] - o.lr_c1 * mm[k][e] / (sqrtf(vv[k][e]) * o.inv_sqrt_c2 + o.eps);
-                            __stcs(a.m + off[k][e], mm[k][e]);
-                            __stcs(a.v + off[k][e], vv[k][e]);
-                        } else {
-                            xn = x[k][e] - o.lr * gv[k][e];
-                        }
-                        __stcs(a.V + off[k][e], xn);
+            for (int e = 0; e < kE; ++e) {
+                float xn = 0.f;
+                if (ok[k][e]) {
+                    if (a.adam) {
+                        mm[k][e] = o.b1 * mm[k][e] + (1.f - o.b1) * gv[k][e];
+                        vv[k][e] = o.b2 * vv[k][e] + (1.f - o.b2) * gv[k][e] * gv[k][e];
+                        xn = x[k][e] - o.lr_c1 * mm[k][e] / (sqrtf(vv[k][e]) * o.inv_sqrt_c2 + o.eps);
+                        __stcs(a.m + off[k][e], mm[k][e]);
+                        __stcs(a.v + off[k][e], vv[k][e]);
+                    } else {
+                        xn = x[k][e] - o.lr * gv[k][e];
                     }
-                    if (c < kTileN) stage[(rr + k - rb) * kTileN + c] = xn;
+                    __stcs(a.V + off[k][e], xn);
+                }
+                if (q) {
+                    stage[(2 * w + k) * kTileN + lane + 32 * e] = xn;
                     const float ax = fabsf(xn);
                     m = fmaxf(m, ax);
                     cm[e] = fmaxf(cm[e], ax);
                 }
+            }
+            if (q) {
 #pragma unroll
-                for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-                if (lane == 0) atomicMax(rmax_s + rr + k, __float_as_uint(m));
+                for (int s = 16; s; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
+                const int64_t i = row0 + rb + 2 * w + k;
+                if (lane == 0 && i < a.N && m > 0.f) atomicMax(a.vrow_next + i, __float_as_uint(m));
             }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
-        // (B) slices of the staged rows: task = (row, 16-column chunk)
-        for (int task = t; task < kQRows * (kTileN / 16); task += 32 * kAuxWarps) {
-            const int rr = task / (kTileN / 16), cq = task - rr * (kTileN / 16);
+        if (!q) continue;
+        asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));  // batch staged
+        const int t = w * 32 + lane;
+        if (t < kQRows * (kTileN / 16)) {  // task = (row, 16-column chunk)
+            const int rr = t / (kTileN / 16), cq = t - rr * (kTileN / 16);
             const int64_t i = row0 + rb + rr, k0 = col0 + 16 * cq;
-            if (i >= a.N || k0 >= a.r) continue;
-            float xs[16];
-            const float4* s4 = reinterpret_cast<const float4*>(stage + rr * kTileN + 16 * cq);
+            if (i < a.N && k0 < a.r) {
+                float xs[16];
+                const float4* s4 = reinterpret_cast<const float4*>(stage + rr * kTileN + 16 * cq);
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-                const float4 f = s4[q4];
-                xs[4 * q4] = f.x; xs[4 * q4 + 1] = f.y; xs[4 * q4 + 2] = f.z; xs[4 * q4 + 3] = f.w;
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const float4 f = s4[q4];
+                    xs[4 * q4] = f.x; xs[4 * q4 + 1] = f.y; xs[4 * q4 + 2] = f.z; xs[4 * q4 + 3] = f.w;
+                }
+                const float um = kHeadroom * __uint_as_float(__ldg(a.vrow_cur + i));
+                uint4 qq[3];
+                slice16(xs, slice_scale(__float_as_uint(um)), qq);
+                store_q16(a.vq_next, k0 >> 6, i, (int)((k0 >> 4) & 3), a.nkbV, a.rowsV, qq);
             }
-            const float um = kHeadroom * __uint_as_float(__ldg(a.vrow_cur + i));
-            uint4 q[3];
-            slice16(xs, slice_scale(__float_as_uint(um)), q);
-            store_q16(a.vq_next, k0 >> 6, i, (int)((k0 >> 4) & 3), a.nkbV, a.rowsV, q);
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
+        asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));  // stage free
     }
-    // tile maxima -> global (row maxima were combined in shared memory)
+    if (q) {
 #pragma unroll
-    for (int e = 0; e < 3; ++e) {
-        const int c = t + 64 * e;
-        if (c < kTileN && col0 + c < a.r && cm[e] > 0.f) atomicMax(a.vcol_next + col0 + c, __float_as_uint(cm[e]));
+        for (int e = 0; e < kE; ++e) {
+            const int c = lane + 32 * e;
+            if (col0 + c < a.r && cm[e] > 0.f) atomicMax(a.vcol_next + col0 + c, __float_as_uint(cm[e]));
+        }
     }
-    for (int e = t; e < 128; e += 32 * kAuxWarps) {
-        const unsigned v = rmax_s[e];
-        if (row0 + e < a.N && v) atomicMax(a.vrow_next + row0 + e, v);
-        rmax_s[e] = 0u;  // ready for the next tile
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
+}
+
+__device__ __forceinline__ OptConsts opt_consts(const DevOpt* p) {
+    const DevOpt o = *p;
+    OptConsts oc;
+    oc.lr = o.lr;
+    oc.b1 = o.b1;
+    oc.b2 = o.b2;
+    oc.eps = o.eps;
+    const double c1 = 1.0 - pow((double)o.b1, (double)o.t);
+    const double c2 = 1.0 - pow((double)o.b2, (double)o.t);
+    oc.lr_c1 = (float)((double)o.lr / c1);
+    oc.inv_sqrt_c2 = (float)(1.0 / sqrt(c2));
+    return oc;
 }
 
 template <int kMode>
@@ -277,9 +252,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint64_t* empty = full + kStages;
     uint64_t* tfull = empty + kStages;
     uint64_t* tempty = tfull + 1;
-    uint64_t* gready = tempty + 1;  // ring slot holds a finished gradient tile
-    uint64_t* gfree = gready + 2;   // ring slot consumed by the aux warps
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(gfree + 2);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
     float(*auxbuf)[65] = reinterpret_cast<float(*)[65]>(smem + kStages * kStageBytes + kBarBytes);
 
     const int warp = threadIdx.x >> 5;
@@ -295,10 +268,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
         mbar_init(tfull, 1);
         mbar_init(tempty, 2 * kEpiWarps);  // epilogue warps of both CTAs
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(&gready[a], kEpiWarps);
-            mbar_init(&gfree[a], kAuxWarps);
-        }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -438,9 +407,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         // -------------------------------------------------------- epilogue --
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
+        OptConsts oc{};
+        if (kMode == kModeBwdUpdate) oc = opt_consts(args.opt);
         uint32_t acc_phase = 0;
-        int it = 0;
-        for (int tile = cid; tile < args.ntiles; tile += ncl, ++it) {
+        for (int tile = cid; tile < args.ntiles; tile += ncl) {
             const TileCoord tc = args.tiles[tile];
             const int64_t i = (int64_t)tc.a * kPairM + rank * 128 + q * 32 + lane;
             float sum[kEpiCols];
@@ -501,10 +471,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     }
                 }
             } else if (kMode == kModeBwdUpdate) {
-                // hand the finished tile to the aux warps through the per-CTA ring
-                const int slot = it & 1;
-                mbar_wait(&gfree[slot], ((it >> 1) & 1) ^ 1);
-                float4* gr = reinterpret_cast<float4*>(args.ring + ((int64_t)blockIdx.x * 2 + slot) * kRingTile +
+                // stage the finished tile (thread = row) in the ring, then update it
+                // coalesced (thread = column) with all 8 epilogue warps
+                float4* gr = reinterpret_cast<float4*>(args.ring + (int64_t)blockIdx.x * kRingTile +
                                                        (q * 32 + lane) * kTileN + h * kEpiCols);
                 const float s4 = 4.f * ui;
 #pragma unroll
@@ -514,8 +483,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                                         s4 * slice_unit(ub.z) * sum[4 * u + 2], s4 * slice_unit(ub.w) * sum[4 * u + 3]);
                 }
                 __threadfence_block();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&gready[slot]);
+                asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));  // whole tile in the ring
+                update_tile_epi(args, oc, args.ring + (int64_t)blockIdx.x * kRingTile,
+                                (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.c0, warp - 2, lane,
+                                reinterpret_cast<float*>(auxbuf));
+                asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));  // ring consumed
+                if (args.rowsig && warp == 2 && lane == 0) {
+                    __threadfence_system();
+                    atomicAdd(args.rowsig + tc.a / args.sig_blocks, 1u);
+                }
             } else if (i < args.N) {
                 const float s4 = 4.f * ui;
 #pragma unroll
@@ -545,49 +521,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int64_t b = blockIdx.x; b < args.nkbN * nkt; b += gridDim.x)
                 pack_vtq_tile(args.Vsrc, args.N, args.r, args.rowsVT, args.nkbN, args.vcol, args.vtq, b / nkt,
                               (b % nkt) * 64, auxbuf, t, 32 * kAuxWarps);
-        }
-    } else if (kMode == kModeBwdUpdate) {
-        // ----------------------------------------------------------- aux --
-        // optimiser step on tile t while the tensor cores work on tile t+1
-        const int t = threadIdx.x - 32 * (2 + kEpiWarps);  // 0..63
-        OptConsts oc;
-        {
-            const DevOpt o = *args.opt;
-            oc.lr = o.lr;
-            oc.b1 = o.b1;
-            oc.b2 = o.b2;
-            oc.eps = o.eps;
-            const double c1 = 1.0 - pow((double)o.b1, (double)o.t);
-            const double c2 = 1.0 - pow((double)o.b2, (double)o.t);
-            oc.lr_c1 = (float)((double)o.lr / c1);
-            oc.inv_sqrt_c2 = (float)(1.0 / sqrt(c2));
-        }
-        int it = 0;
-        for (int tile = cid; tile < args.ntiles; tile += ncl, ++it) {
-            const TileCoord tc = args.tiles[tile];
-            const int slot = it & 1;
-            mbar_wait(&gready[slot], (it >> 1) & 1);
-            const float* gt = args.ring + ((int64_t)blockIdx.x * 2 + slot) * kRingTile;
-            if (args.vq_next) {
-                float* stg = reinterpret_cast<float*>(auxbuf);
-                unsigned* rmax_s = reinterpret_cast<unsigned*>(stg + kQRows * kTileN);
-                if (it == 0) {
-                    for (int e = t; e < 128; e += 32 * kAuxWarps) rmax_s[e] = 0u;
-                    asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));
-                }
-                update_tile_q(args, oc, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.c0, t, stg, rmax_s);
-            } else {
-                update_tile(args, oc, gt, (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.c0, t);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&gfree[slot]);
-            if (args.rowsig) {
-                asm volatile("bar.sync 1, %0;" ::"n"(32 * kAuxWarps));  // both aux warps stored the tile
-                if (t == 0) {
-                    __threadfence_system();
-                    atomicAdd(args.rowsig + tc.a / args.sig_blocks, 1u);
-                }
-            }
         }
     }
 
@@ -692,8 +625,25 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
 
 static const CUtensorMap& tm(const uint8_t* raw) { return *reinterpret_cast<const CUtensorMap*>(raw); }
 
+// The V^T slices for the backward come from the forward's two aux warps when
+// the forward is long enough to hide them (elements per aux thread vs K-blocks
+// per CTA pair: ~2.5 elements fit under one K-block's MMAs), else from the
+// all-SM k_pack_vtq before the GEMM (small / mid-size problems).
+static bool vtq_in_aux(const Plan& P) {
+    static const int force = env_int("SOS_VTQ_AUX", -1);
+    if (force >= 0) return force != 0;
+    const double pairs = P.num_sms / 2, grid_threads = P.num_sms * 64.0;
+    const double elems_per_thread = (double)P.idx->N * P.r / grid_threads;
+    const double kblocks_per_pair = std::ceil(P.ntiles_fwd / pairs) * P.nkbV;
+    return elems_per_thread <= 2.5 * kblocks_per_pair;
+}
+
 void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st, const unsigned* urow,
                      const unsigned* vcol) {
+    if (V_for_vtq && !vtq_in_aux(P)) {
+        launch_pack_vtq(P, V_for_vtq, st, vcol);
+        V_for_vtq = nullptr;
+    }
     GemmArgs a{};
     a.Vsrc = V_for_vtq;
     a.vtq = P.d_vtq;

@@ -138,7 +138,7 @@ struct Plan {
     float* d_m;       // Adam moments (lazy)
     float* d_v;
     Scalars* d_scal;
-    float* d_ring;    // per-CTA gradient tile ring of the fused backward + update
+    float* d_ring;    // per-CTA staging of a finished gradient tile (fused backward + update)
     unsigned long long* d_progress;  // [2] K-skew counters (fwd, bwd)
     TileCoord* d_tiles_fwd; int ntiles_fwd;
     TileCoord* d_tiles_bwd; int ntiles_bwd;
@@ -214,7 +214,7 @@ void launch_rmax_dp(const Index& ix, const float* res, float* scratch, unsigned*
 void launch_vmax(Plan& P, const float* V, cudaStream_t st, unsigned* vrow = nullptr, unsigned* vcol = nullptr);
 void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow = nullptr,
                    unsigned* vcol = nullptr);  // maxima + VQ
-void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st);
+void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st, const unsigned* vcol = nullptr);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
 void launch_step_begin(Plan& P, double* losses, cudaStream_t st);
 void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop);

@@ -379,11 +379,11 @@ void launch_vmax(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, unsig
     k_vmax<<<grid_for(P, tiles * 256, 256), 256, 0, st>>>(V, N, P.r, vrow, vcol);
 }
 
-void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st) {
+void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st, const unsigned* vcol) {
     LaunchScope ls(P, KK_PACK_V, st);
     const int64_t blocks = P.nkbN * ((P.rowsVT + 63) / 64);
-    k_pack_vtq<<<grid_for(P, blocks * 256, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.rowsVT, P.nkbN, P.d_vcol,
-                                                               P.d_vtq);
+    k_pack_vtq<<<grid_for(P, blocks * 256, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.rowsVT, P.nkbN,
+                                                               vcol ? vcol : P.d_vcol, P.d_vtq);
 }
 
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st) {

@@ -26,3 +26,9 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / steps
 print(f"n={n} d={d} N={ix.N} r={r} ms/step={ms:.3f} steps/s={1e3 / ms:.3f}")
+if "--kernels" in sys.argv:  # per-kernel split (plain launches with events, a few extra us each)
+    plan.timing(True)
+    plan.descend(V, p, 10)
+    torch.cuda.synchronize()
+    plan.timing(False)
+    print("  per launch (us):", {k: round(ms / max(1, c) * 1e3, 1) for k, (ms, c) in plan.timing_read().items() if c})

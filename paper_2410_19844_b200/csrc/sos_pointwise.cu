@@ -425,13 +425,26 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, uns
 // few tens of millions of lookups instead of N^2 gathers), then one streaming
 // pass gathers and slices R.  SOS_RPACK_FUSED=1 selects the one-pass fused
 // packer (row staged in shared memory), SOS_RPACK_TWOPASS=1 the gathered maxima.
+// R row maxima: the lattice DP costs ~d launches plus sum_D C(n+D-1, D) * n
+// lookups; the direct gather over PT (k_rmax) one launch plus N^2 lookups.
+// Small problems and many variables favour the direct pass (config 2: 60 -> 15
+// us; N = 5050 quartic: 110 -> 44 us); configs 3 and 4 the DP (0.18 / 0.33 ms vs
+// 0.22 / ~0.6 ms).  Rates fitted to those measurements.
+static bool rmax_direct_is_cheaper(const Index& ix) {
+    double lookups = 0;
+    for (int D = ix.d; D <= 2 * ix.d - 1; ++D) lookups += (double)rmax_level_count(ix.n, D) * ix.n;
+    const double dp_us = 12.0 * ix.d + lookups / 2e5;
+    const double direct_us = 10.0 + (double)ix.N * ix.N / 7e5;
+    return direct_us < dp_us;
+}
+
 void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     const int64_t Np = P.idx->Np;
     const int64_t row_bytes = Np * 4;
     static const bool fused = getenv("SOS_RPACK_FUSED") && atoi(getenv("SOS_RPACK_FUSED"));
-    static const bool two_pass = getenv("SOS_RPACK_TWOPASS") && atoi(getenv("SOS_RPACK_TWOPASS"));
+    static const char* tp_env = getenv("SOS_RPACK_TWOPASS");
     if (!fused || row_bytes > kRowSmemMax) {
-        if (two_pass) {
+        if (tp_env ? atoi(tp_env) != 0 : rmax_direct_is_cheaper(*P.idx)) {
             launch_rmax(P, res, st, use_stop);
         } else {
             LaunchScope ls(P, KK_ABSMAX_R, st);

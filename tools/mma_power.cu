@@ -13,6 +13,7 @@
 //   ./mma_power <mode> <seconds> [N]
 // modes: 0 f16 gaussian   1 f16 "lo" split residues   2 f16 zeros   3 bf16 gaussian
 //        4 s8 uniform [-127,127]   5 s8 zeros   6 e4m3 gaussian   7 s8 small [-8,8]
+//        8 s8 uniform [-64,63]   9 s8 uniform [-32,31]
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -70,6 +71,10 @@ __global__ void __launch_bounds__(128, 1) k_mma(int mode, int nn, long long iter
             case 6: { __nv_fp8_e4m3 a(g), b(gauss(key + 77777777u)); v = (uint16_t)a.__x | ((uint16_t)b.__x << 8); } break;
             case 7: { uint32_t h = hash32(key * 7 + 3); int8_t a = (int8_t)((int)(h % 17) - 8), b = (int8_t)((int)((h >> 8) % 17) - 8);
                       v = (uint16_t)(uint8_t)a | ((uint16_t)(uint8_t)b << 8); } break;
+            case 8: { uint32_t h = hash32(key * 7 + 3); int8_t a = (int8_t)((int)(h % 128) - 64), b = (int8_t)((int)((h >> 8) % 128) - 64);
+                      v = (uint16_t)(uint8_t)a | ((uint16_t)(uint8_t)b << 8); } break;
+            case 9: { uint32_t h = hash32(key * 7 + 3); int8_t a = (int8_t)((int)(h % 64) - 32), b = (int8_t)((int)((h >> 8) % 64) - 32);
+                      v = (uint16_t)(uint8_t)a | ((uint16_t)(uint8_t)b << 8); } break;
         }
         reinterpret_cast<uint16_t*>(sm)[e] = v;
     }
@@ -88,7 +93,7 @@ __global__ void __launch_bounds__(128, 1) k_mma(int mode, int nn, long long iter
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tslot;
     uint32_t idesc;
-    const bool i8 = mode == 4 || mode == 5 || mode == 7;
+    const bool i8 = mode == 4 || mode == 5 || mode >= 7;
     const bool f8 = mode == 6;
     if (i8) idesc = (2u << 4) | (1u << 7) | (1u << 10);   // S32 <- S8 x S8
     else if (f8) idesc = (1u << 4);                        // F32 <- E4M3 x E4M3

@@ -232,6 +232,13 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     build_tiles(Np / kPairM, r, false, tb);
     P.ntiles_fwd = (int)tf.size();
     P.ntiles_bwd = (int)tb.size();
+    {
+        // sos_descend: the update can write the next step's V^T slices when its
+        // extra slicing work hides under a tile's MMAs (long K); for short K it
+        // would lengthen the update-bound backward (profiles/r1_vtq_next_ab.log)
+        const char* e = getenv("SOS_VTQ_UPDATE");
+        P.vtq_from_update = e ? atoi(e) != 0 : P.nkbN >= 128;
+    }
     // row chunks of the last step's V release = the raster's row groups
     P.sig_blocks = (int)tile_group();
     P.sig_expect.assign((size_t)((Np / kPairM + P.sig_blocks - 1) / P.sig_blocks), 0u);
@@ -242,7 +249,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         (rc = dalloc(&P.d_rq, (size_t)kSlices * P.nkbN * Np * 64)) ||
         (rc = dalloc(&P.d_vrow, (size_t)P.rowsV * 4)) || (rc = dalloc(&P.d_vcol, (size_t)P.rowsVT * 4)) ||
         (rc = dalloc(&P.d_rrow, (size_t)Np * 4)) || (rc = dalloc(&P.d_coef, (size_t)M * 4)) ||
-        (rc = dalloc(&P.d_dbuf, (size_t)(4 * P.rowsV + 2 * P.rowsVT) * 4)) ||
+        (rc = dalloc(&P.d_dbuf, (size_t)(4 * P.rowsV + 4 * P.rowsVT) * 4)) ||
         (rc = dalloc(&P.d_opt, sizeof(DevOpt))) ||
         (rc = dalloc(&P.d_rlev, std::max<size_t>(1, rlev_floats(h->ix)) * sizeof(float))) ||
         (rc = dalloc(&P.d_res, (size_t)M * 4)) || (rc = dalloc(&P.d_scal, sizeof(Scalars))) ||
@@ -264,7 +271,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         cudaMemset(P.d_vcol, 0, (size_t)P.rowsVT * 4) != cudaSuccess ||
         cudaMemset(P.d_rrow, 0, (size_t)Np * 4) != cudaSuccess ||
         cudaMemset(P.d_rq, 0, (size_t)kSlices * P.nkbN * Np * 64) != cudaSuccess ||  // padding rows stay 0
-        cudaMemset(P.d_dbuf, 0, (size_t)(4 * P.rowsV + 2 * P.rowsVT) * 4) != cudaSuccess ||
+        cudaMemset(P.d_dbuf, 0, (size_t)(4 * P.rowsV + 4 * P.rowsVT) * 4) != cudaSuccess ||
         cudaMemset(P.d_opt, 0, sizeof(DevOpt)) != cudaSuccess) {
         sos_plan_destroy(pl);
         return fail(SOS_ERR_CUDA, "workspace init");
@@ -289,6 +296,7 @@ int sos_plan_destroy(sos_plan* pl) {
     Plan& P = pl->P;
     cudaFree(P.d_vq);
     cudaFree(P.d_vtq);
+    cudaFree(P.d_vtq2);
     cudaFree(P.d_rq);
     cudaFree(P.d_vrow);
     cudaFree(P.d_vcol);
@@ -473,6 +481,9 @@ struct DescendPtrs {
     unsigned* vrowx[2];  // exact row maxima of V (current / next)
     unsigned* urow[2];   // row scales the slices in VQ were written with
     unsigned* vcol[2];   // exact column maxima of V
+    unsigned* ucol[2];   // column scales the slices in VTQ[b] were written with
+    uint8_t* vtq[2];     // VTQ buffers (step parity b reads vtq[b], its update writes vtq[b ^ 1])
+    const uint8_t* tmap_vtq[2];
 };
 static DescendPtrs descend_ptrs(Plan& P) {
     DescendPtrs d;
@@ -482,22 +493,50 @@ static DescendPtrs descend_ptrs(Plan& P) {
     d.urow[1] = P.d_dbuf + 3 * P.rowsV;
     d.vcol[0] = P.d_dbuf + 4 * P.rowsV;
     d.vcol[1] = P.d_dbuf + 4 * P.rowsV + P.rowsVT;
+    d.ucol[0] = P.d_dbuf + 4 * P.rowsV + 2 * P.rowsVT;
+    d.ucol[1] = P.d_dbuf + 4 * P.rowsV + 3 * P.rowsVT;
+    d.vtq[0] = P.d_vtq;
+    d.vtq[1] = P.d_vtq2;
+    d.tmap_vtq[0] = P.tmap_vtq_b;
+    d.tmap_vtq[1] = P.tmap_vtq2_b;
     return d;
+}
+
+// the second VTQ buffer of sos_descend, allocated on first use (zeroed: its
+// K-padding rows j >= N are never written and must read as 0)
+static int ensure_vtq2(Plan& P) {
+    if (P.d_vtq2) return SOS_OK;
+    const size_t bytes = (size_t)kSlices * P.nkbN * P.rowsVT * 64;
+    int rc = dalloc(&P.d_vtq2, bytes);
+    if (rc) return rc;
+    if (cudaMemset(P.d_vtq2, 0, bytes) != cudaSuccess ||
+        !make_q_tmap(P.tmap_vtq2_b, P.d_vtq2, P.rowsVT, P.nkbN, kHalfN)) {
+        cudaFree(P.d_vtq2);
+        P.d_vtq2 = nullptr;
+        return fail(SOS_ERR_CUDA, "second VTQ buffer");
+    }
+    return SOS_OK;
 }
 
 static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const float* p, double* losses,
                         cudaStream_t st) {
     CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
     CK(cudaMemsetAsync(P.d_coef, 0, (size_t)P.idx->M * 4, st));
-    launch_gemm_fwd(P, P.d_coef, V, st, d.urow[b], d.vcol[b]);
+    const bool vu = P.vtq_from_update;
+    // VTQ[b] came from the previous update (or the prologue); else the forward packs it
+    launch_gemm_fwd(P, P.d_coef, vu ? nullptr : V, st, d.urow[b], d.vcol[b]);
     launch_residual(P, P.d_coef, p, P.d_res, st);
     launch_step_begin(P, losses, st);  // t += 1, losses[k] = L(V_t)
     launch_pack_r(P, P.d_res, st, 1);
     CK(cudaMemsetAsync(d.vrowx[b ^ 1], 0, P.rowsV * 4, st));
     CK(cudaMemsetAsync(d.vcol[b ^ 1], 0, P.rowsVT * 4, st));
-    const DescendBufs db{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1]};
+    const DescendBufs db = vu ? DescendBufs{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1], d.ucol[b],
+                                            d.tmap_vtq[b], d.vtq[b ^ 1]}
+                              : DescendBufs{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1], d.vcol[b],
+                                            P.tmap_vtq_b, nullptr};
     launch_gemm_bwd_update(P, V, st, &db);
     launch_descend_fixup(P, V, d.vrowx[b], d.vrowx[b ^ 1], d.urow[b], d.urow[b ^ 1], d.vcol[b], d.vcol[b ^ 1], st);
+    if (vu) launch_descend_fixup_cols(P, V, d.vcol[b], d.vcol[b ^ 1], d.ucol[b ^ 1], d.vtq[b ^ 1], st);
     return check_launch("descend step");
 }
 
@@ -505,6 +544,10 @@ static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const fl
 // row-chunk release of V on (P.d_rowsig zeroed, then P.sig_ev recorded, on st)
 static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps, double* losses_dev, cudaStream_t st,
                         bool sig_last) {
+    if (P.vtq_from_update) {
+        const int rc0 = ensure_vtq2(P);
+        if (rc0) return rc0;
+    }
     const DescendPtrs d = descend_ptrs(P);
     auto plain_step = [&](int64_t t) -> int {
         const bool sig = sig_last && t == steps - 1;
@@ -523,6 +566,10 @@ static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps
     // step 0 starts from the exact maxima and slices of the caller's V
     launch_pack_v(P, V_dev, st, d.vrowx[0], d.vcol[0]);
     CK(cudaMemcpyAsync(d.urow[0], d.vrowx[0], P.rowsV * 4, cudaMemcpyDeviceToDevice, st));
+    if (P.vtq_from_update) {
+        launch_pack_vtq(P, V_dev, st, d.vcol[0]);
+        CK(cudaMemcpyAsync(d.ucol[0], d.vcol[0], P.rowsVT * 4, cudaMemcpyDeviceToDevice, st));
+    }
     if ((rc = plain_step(0))) return rc;
     int64_t left = steps - 1;
     const bool timing = P.timing && P.timing->on;  // per-kernel events need plain launches

@@ -80,7 +80,9 @@ struct GemmArgs {
     const unsigned* vrow_cur;
     unsigned* vrow_next;
     unsigned* vcol_next;
-    // kModeFwd with Vsrc != nullptr: the aux warps pack V^T slices meanwhile
+    // kModeFwd with Vsrc != nullptr: the aux warps pack V^T slices meanwhile;
+    // kModeBwdUpdate with vtq != nullptr: the update writes the next step's
+    // V^T slices (column scale kHeadroom * vcol)
     const float* Vsrc;
     uint8_t* vtq;
     int64_t rowsVT;
@@ -129,6 +131,7 @@ constexpr int kQRows = 16;  // rows per staged batch of the update
 // valid while the row maximum stays in [1/2, 2] of the old one (k_descend_fixup
 // re-slices the rare rows that leave that window, see sos_pointwise.cu).
 constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kStageLd = kTileN + 4;  // staged row pitch (floats): column reads hit distinct banks
 __device__ __forceinline__ void update_tile_epi(const GemmArgs& a, const OptConsts& o, const float* __restrict__ gt,
                                                 int64_t row0, int64_t col0, int w, int lane, float* stage) {
     constexpr int kE = kTileN / 32;  // columns per lane
@@ -176,7 +179,7 @@ __device__ __forceinline__ void update_tile_epi(const GemmArgs& a, const OptCons
                     __stcs(a.V + off[k][e], xn);
                 }
                 if (q) {
-                    stage[(2 * w + k) * kTileN + lane + 32 * e] = xn;
+                    stage[(2 * w + k) * kStageLd + lane + 32 * e] = xn;
                     const float ax = fabsf(xn);
                     m = fmaxf(m, ax);
                     cm[e] = fmaxf(cm[e], ax);
@@ -197,7 +200,7 @@ __device__ __forceinline__ void update_tile_epi(const GemmArgs& a, const OptCons
             const int64_t i = row0 + rb + rr, k0 = col0 + 16 * cq;
             if (i < a.N && k0 < a.r) {
                 float xs[16];
-                const float4* s4 = reinterpret_cast<const float4*>(stage + rr * kTileN + 16 * cq);
+                const float4* s4 = reinterpret_cast<const float4*>(stage + rr * kStageLd + 16 * cq);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
                     const float4 f = s4[q4];
@@ -208,6 +211,18 @@ __device__ __forceinline__ void update_tile_epi(const GemmArgs& a, const OptCons
                 slice16(xs, slice_scale(__float_as_uint(um)), qq);
                 store_q16(a.vq_next, k0 >> 6, i, (int)((k0 >> 4) & 3), a.nkbV, a.rowsV, qq);
             }
+        }
+        const int tv = kEpiThreads - 1 - t;  // VTQ task of this thread (threads 96.. ; 160 tasks)
+        if (a.vtq && tv < kTileN && col0 + tv < a.r) {
+            // VTQ row k = col0 + tv: the batch's 16 rows are one 16-value K-chunk of it
+            const int64_t k = col0 + tv, i0 = row0 + rb;
+            float xs[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) xs[e] = stage[e * kStageLd + tv];
+            const float uc = kHeadroom * __uint_as_float(__ldg(a.vcol + k));
+            uint4 qq[3];
+            slice16(xs, slice_scale(__float_as_uint(uc)), qq);
+            store_q16(a.vtq, i0 >> 6, k, (int)((i0 >> 4) & 3), a.nkbN, a.rowsVT, qq);
         }
         asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));  // stage free
     }
@@ -697,7 +712,7 @@ void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st) {
 // optimiser step (GD or Adam): the gradient never makes an HBM round trip.  The
 // GEMM reads the packed copy VTQ, never V, so updating V in place is safe.
 void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBufs* db) {
-    GemmArgs a = bwd_args(P, db ? db->vcol_cur : nullptr);
+    GemmArgs a = bwd_args(P, db ? db->ucol_cur : nullptr);
     if (db) {
         a.vq_next = P.d_vq;
         a.rowsV = P.rowsV;
@@ -705,6 +720,11 @@ void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBuf
         a.vrow_cur = db->vrow_cur;
         a.vrow_next = db->vrow_next;
         a.vcol_next = db->vcol_next;
+        // the next step's V^T slices (scale kHeadroom x the current column maximum)
+        a.vtq = db->vtq_next;
+        a.vcol = db->vcol_cur;
+        a.rowsVT = P.rowsVT;
+        a.nkbN = P.nkbN;
     }
     a.ring = P.d_ring;
     a.V = V;
@@ -721,7 +741,7 @@ void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBuf
         a.sig_chunks = (int)P.sig_expect.size();
     }
     LaunchScope ls(P, KK_GEMM_BWD, st);
-    launchq<kModeBwdUpdate>(P, tm(P.tmap_rq_a), tm(P.tmap_vtq_b), a, st);
+    launchq<kModeBwdUpdate>(P, tm(P.tmap_rq_a), tm(db ? db->tmap_vtq_cur : P.tmap_vtq_b), a, st);
 }
 
 }  // namespace sos

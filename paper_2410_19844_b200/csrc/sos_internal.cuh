@@ -127,12 +127,15 @@ struct Plan {
     int64_t nkbN;     // VTQ / RQ K-blocks: Np / 64
     uint8_t* d_vq;    // VQ
     uint8_t* d_vtq;   // VTQ
+    uint8_t* d_vtq2;  // sos_descend: second VTQ buffer (the update writes step t+1's while step t's is read)
+    bool vtq_from_update;  // sos_descend: the backward's update writes the next VTQ (long K only)
     uint8_t* d_rq;    // RQ
     unsigned* d_vrow; // max_k |V_ik| (float bits), rowsV
     unsigned* d_vcol; // max_j |V_jk| (float bits), rowsVT
     unsigned* d_rrow; // max_j |R_ij| (float bits), Np
     float* d_rlev;    // lattice-DP levels for the R row maxima
-    unsigned* d_dbuf; // sos_descend: [2][rowsV] exact row maxima, [2][rowsV] used row scales, [2][rowsVT] column maxima
+    unsigned* d_dbuf; // sos_descend: [2][rowsV] exact row maxima, [2][rowsV] used row scales, [2][rowsVT] column
+                      // maxima, [2][rowsVT] used column scales
     float* d_coef;    // M
     float* d_res;     // M
     float* d_m;       // Adam moments (lazy)
@@ -145,6 +148,7 @@ struct Plan {
     alignas(64) uint8_t tmap_vq_a[128];   // CUtensorMaps (3-D: 64 B x rows x slice planes)
     alignas(64) uint8_t tmap_vq_b[128];
     alignas(64) uint8_t tmap_vtq_b[128];
+    alignas(64) uint8_t tmap_vtq2_b[128];
     alignas(64) uint8_t tmap_rq_a[128];
     int opt_kind; float lr, b1, b2, eps; bool opt_ready;
     double stop_tol;  // sos_opt_set_stop: skip backward + update once loss <= stop_tol * |p|^2
@@ -226,6 +230,9 @@ struct DescendBufs {
     const unsigned* vcol_cur;  // exact column maxima of the current V
     unsigned* vrow_next;       // exact row maxima of the updated V (atomicMax, zeroed before)
     unsigned* vcol_next;       // exact column maxima of the updated V
+    const unsigned* ucol_cur;  // column scales the current VTQ was written with (backward B unscale)
+    const uint8_t* tmap_vtq_cur;  // tensor map of the current VTQ buffer
+    uint8_t* vtq_next;         // VTQ buffer the update writes for the next step
 };
 // slices written by the update use kHeadroom x the current row maximum
 constexpr float kHeadroom = 2.f;
@@ -234,6 +241,8 @@ void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t 
                      const unsigned* vcol = nullptr);
 void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st);
 void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBufs* db = nullptr);
+void launch_descend_fixup_cols(Plan& P, const float* V, const unsigned* vcol_cur, const unsigned* vcol_next,
+                               unsigned* ucol_next, uint8_t* vtq_next, cudaStream_t st);
 void launch_descend_fixup(Plan& P, const float* V, const unsigned* vrow_cur, unsigned* vrow_next,
                           const unsigned* urow_cur, unsigned* urow_next, const unsigned* vcol_cur, unsigned* vcol_next,
                           cudaStream_t st);

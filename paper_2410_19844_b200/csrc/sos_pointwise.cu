@@ -531,6 +531,47 @@ __global__ void __launch_bounds__(256) k_descend_fixup(const float* __restrict__
     }
 }
 
+// The same for the V^T slices the update wrote for step t+1 (scale kHeadroom x
+// the old column maximum): a column whose new maximum left [u/4, u] is
+// re-sliced from V with its exact maximum (strided reads: rare); ucol_next
+// receives the scale the backward must unscale each VTQ row with.
+__global__ void __launch_bounds__(256) k_descend_fixup_cols(const float* __restrict__ V, int64_t N, int64_t r,
+                                                            int64_t nkbN, int64_t rowsVT,
+                                                            const unsigned* __restrict__ vcol_cur,
+                                                            const unsigned* __restrict__ vcol_next,
+                                                            unsigned* __restrict__ ucol_next, uint8_t* __restrict__ VTQ,
+                                                            const Scalars* sc, const DevOpt* opt) {
+    if (descent_stopped(sc, opt, 1)) return;  // no update ran: the next step reads nothing new
+    for (int64_t k = blockIdx.x; k < r; k += gridDim.x) {
+        const float u = kHeadroom * __uint_as_float(vcol_cur[k]);
+        const unsigned mb = vcol_next[k];
+        const float mx = __uint_as_float(mb);
+        if (mx <= u && mx >= 0.25f * u) {
+            if (threadIdx.x == 0) ucol_next[k] = __float_as_uint(u);
+            continue;
+        }
+        if (threadIdx.x == 0) ucol_next[k] = mb;
+        const float c = slice_scale(mb);
+        for (int64_t cc = threadIdx.x; cc < nkbN * 4; cc += blockDim.x) {
+            const int64_t j0 = cc * 16;
+            float x[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = j0 + e < N ? V[(j0 + e) * r + k] : 0.f;
+            uint4 q[3];
+            slice16(x, c, q);
+            store_q16(VTQ, cc >> 2, k, (int)(cc & 3), nkbN, rowsVT, q);
+        }
+    }
+}
+
+void launch_descend_fixup_cols(Plan& P, const float* V, const unsigned* vcol_cur, const unsigned* vcol_next,
+                               unsigned* ucol_next, uint8_t* vtq_next, cudaStream_t st) {
+    LaunchScope ls(P, KK_PACK_V, st);
+    k_descend_fixup_cols<<<grid_for(P, P.r * 256, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.nkbN, P.rowsVT, vcol_cur,
+                                                                        vcol_next, ucol_next, vtq_next, P.d_scal,
+                                                                        P.d_opt);
+}
+
 void launch_descend_fixup(Plan& P, const float* V, const unsigned* vrow_cur, unsigned* vrow_next,
                           const unsigned* urow_cur, unsigned* urow_next, const unsigned* vcol_cur, unsigned* vcol_next,
                           cudaStream_t st) {

@@ -526,13 +526,17 @@ def test_zero_rows_and_columns(sos):
 
 # -------------------------------------------------------------- sos_descend --
 
+@pytest.mark.parametrize("vtq_update", ["0", "1"])
 @pytest.mark.parametrize("kind,lr,r", [("adam", 1e-3, 330), ("gd", 5e-3, 330), ("adam", 1e-3, 336)])
-def test_descend_matches_steps(sos, kind, lr, r):
+def test_descend_matches_steps(sos, kind, lr, r, vtq_update, monkeypatch):
     """sos_descend (slices of V_{t+1} written by the update of step t) follows
     the same iteration as repeated sos_step calls, to the slice precision.
-    Row 5 of V0 is zero, so its first update leaves the headroom window and is
-    re-sliced by the fixup kernel.  r = 336 (a multiple of 4) takes the
-    vectorised update path, r = 330 the scalar one."""
+    Row 5 and column 9 of V0 are zero, so their first update leaves the
+    headroom window and is re-sliced by the fixup kernels (VQ row, VTQ row).
+    r = 336 (a multiple of 4) and r = 330 (rows not 16-byte aligned).
+    vtq_update = 1 forces the path where the update also writes the next
+    step's V^T slices (the default only for long K)."""
+    monkeypatch.setenv("SOS_VTQ_UPDATE", vtq_update)  # read at plan creation
     c = si.CONFIGS["c1_n8_2d8"]
     o = oracle(c.n, c.d)
     ix = sos.SosIndex(c.n, c.d)
@@ -540,6 +544,7 @@ def test_descend_matches_steps(sos, kind, lr, r):
     p = torch.from_numpy(o.forward(si.planted_w(o.N, c.r_star, 0)).astype(np.float32)).cuda()
     V0 = si.v0(o.N, r, 0)
     V0[5] = 0.0
+    V0[:, 9] = 0.0
     steps = 30
     plan.opt_init(kind, lr)
     Vs = torch.from_numpy(V0.copy()).cuda()

@@ -63,7 +63,7 @@ struct GemmArgs {
     unsigned long long* dbg;   // SOS_GEMM_STATS: per-role wait cycles (instrumentation only)
     int kserp;                 // walk K backwards on odd local tiles (L2 reuse across waves)
     int probe;                 // SOS_GEMM_PROBE (experiment, wrong results): 1 = K-blocks mod 8, 2 = also tile 0, 4 = 2 with B loaded only on the first ring pass
-    // kModeBwdUpdate: the optimiser step of PAPER.md:221, applied by the aux warps
+    // kModeBwdUpdate(Vtq): the optimiser step of PAPER.md:221, applied by the epilogue warps
     float* ring;  // per-CTA staging of the finished gradient tile (128 x 160 fp32, L2-resident)
     float* V;
     float* m;
@@ -72,7 +72,7 @@ struct GemmArgs {
     const Scalars* scal;
     const DevOpt* opt;  // optimiser parameters, step count t, stopping tolerance
     int use_stop;       // apply the sos_opt_set_stop rule
-    // kModeBwdUpdate inside sos_descend (vq_next != nullptr): the aux warps also
+    // kModeBwdUpdate(Vtq) inside sos_descend (vq_next != nullptr): the update also
     // write the int8 slices of the updated V (scale kHeadroom * vrow_cur) and the
     // exact row / column maxima of the updated V for the next step
     uint8_t* vq_next;
@@ -81,7 +81,7 @@ struct GemmArgs {
     unsigned* vrow_next;
     unsigned* vcol_next;
     // kModeFwd with Vsrc != nullptr: the aux warps pack V^T slices meanwhile;
-    // kModeBwdUpdate with vtq != nullptr: the update writes the next step's
+    // kModeBwdUpdateVtq: the update also writes the next step's
     // V^T slices (column scale kHeadroom * vcol)
     const float* Vsrc;
     uint8_t* vtq;
@@ -103,7 +103,9 @@ struct OptConsts {
 
 constexpr int kModeFwd = 0;        // Gram tile -> coefficient scatter
 constexpr int kModeBwdStore = 1;   // 4RV tile -> grad (sos_backward, sos_loss_grad)
-constexpr int kModeBwdUpdate = 2;  // 4RV tile -> ring -> aux warps update V (and Adam moments)
+constexpr int kModeBwdUpdate = 2;  // 4RV tile -> staged -> epilogue warps update V (and Adam moments)
+constexpr int kModeBwdUpdateVtq = 3;  // same, also writing the next step's V^T slices (separate
+                                      // instantiation: the extra code costs registers otherwise)
 constexpr int kRingTile = 128 * kTileN;  // floats per ring slot
 
 constexpr int kStages = 5;
@@ -132,6 +134,7 @@ constexpr int kQRows = 16;  // rows per staged batch of the update
 // re-slices the rare rows that leave that window, see sos_pointwise.cu).
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kStageLd = kTileN + 4;  // staged row pitch (floats): column reads hit distinct banks
+template <bool kVtq>
 __device__ __forceinline__ void update_tile_epi(const GemmArgs& a, const OptConsts& o, const float* __restrict__ gt,
                                                 int64_t row0, int64_t col0, int w, int lane, float* stage) {
     constexpr int kE = kTileN / 32;  // columns per lane
@@ -143,23 +146,25 @@ __device__ __forceinline__ void update_tile_epi(const GemmArgs& a, const OptCons
     for (int rb = 0; rb < 128; rb += kQRows) {
         if (row0 + rb >= a.N) break;
         float gv[2][kE], x[2][kE], mm[2][kE], vv[2][kE];
-        int64_t off[2][kE];
+        int64_t ro[2];  // element offset of (row, col0 + lane); column e adds 32 e
         bool ok[2][kE];
 #pragma unroll
-        for (int k = 0; k < 2; ++k)
+        for (int k = 0; k < 2; ++k) {
+            const int rr = rb + 2 * w + k;
+            const int64_t i = row0 + rr;
+            ro[k] = i * a.r + col0 + lane;
 #pragma unroll
             for (int e = 0; e < kE; ++e) {
-                const int c = lane + 32 * e, rr = rb + 2 * w + k;
-                const int64_t i = row0 + rr;
+                const int c = lane + 32 * e;
                 ok[k][e] = col0 + c < a.r && i < a.N;
-                off[k][e] = i * a.r + col0 + c;
                 gv[k][e] = ok[k][e] ? __ldcg(gt + rr * kTileN + c) : 0.f;
-                x[k][e] = ok[k][e] ? __ldcs(a.V + off[k][e]) : 0.f;
+                x[k][e] = ok[k][e] ? __ldcs(a.V + ro[k] + 32 * e) : 0.f;
                 if (a.adam) {
-                    mm[k][e] = ok[k][e] ? __ldcs(a.m + off[k][e]) : 0.f;
-                    vv[k][e] = ok[k][e] ? __ldcs(a.v + off[k][e]) : 0.f;
+                    mm[k][e] = ok[k][e] ? __ldcs(a.m + ro[k] + 32 * e) : 0.f;
+                    vv[k][e] = ok[k][e] ? __ldcs(a.v + ro[k] + 32 * e) : 0.f;
                 }
             }
+        }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             float m = 0.f;
@@ -171,12 +176,12 @@ __device__ __forceinline__ void update_tile_epi(const GemmArgs& a, const OptCons
                         mm[k][e] = o.b1 * mm[k][e] + (1.f - o.b1) * gv[k][e];
                         vv[k][e] = o.b2 * vv[k][e] + (1.f - o.b2) * gv[k][e] * gv[k][e];
                         xn = x[k][e] - o.lr_c1 * mm[k][e] / (sqrtf(vv[k][e]) * o.inv_sqrt_c2 + o.eps);
-                        __stcs(a.m + off[k][e], mm[k][e]);
-                        __stcs(a.v + off[k][e], vv[k][e]);
+                        __stcs(a.m + ro[k] + 32 * e, mm[k][e]);
+                        __stcs(a.v + ro[k] + 32 * e, vv[k][e]);
                     } else {
                         xn = x[k][e] - o.lr * gv[k][e];
                     }
-                    __stcs(a.V + off[k][e], xn);
+                    __stcs(a.V + ro[k] + 32 * e, xn);
                 }
                 if (q) {
                     stage[(2 * w + k) * kStageLd + lane + 32 * e] = xn;
@@ -213,7 +218,7 @@ __device__ __forceinline__ void update_tile_epi(const GemmArgs& a, const OptCons
             }
         }
         const int tv = kEpiThreads - 1 - t;  // VTQ task of this thread (threads 96.. ; 160 tasks)
-        if (a.vtq && tv < kTileN && col0 + tv < a.r) {
+        if (kVtq && tv < kTileN && col0 + tv < a.r) {
             // VTQ row k = col0 + tv: the batch's 16 rows are one 16-value K-chunk of it
             const int64_t k = col0 + tv, i0 = row0 + rb;
             float xs[16];
@@ -253,9 +258,10 @@ template <int kMode>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_gemmq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
     constexpr bool kFwd = kMode == kModeFwd;
+    constexpr bool kUpd = kMode == kModeBwdUpdate || kMode == kModeBwdUpdateVtq;
     // converged (sos_opt_set_stop): the whole grid leaves before any barrier,
     // TMEM or cluster work, so V and the optimiser state stay as they are
-    if (kMode == kModeBwdUpdate && descent_stopped(args.scal, args.opt, args.use_stop)) {
+    if (kUpd && descent_stopped(args.scal, args.opt, args.use_stop)) {
         if (args.rowsig && blockIdx.x == 0)  // nothing changes: release every chunk at once
             for (int c = threadIdx.x; c < args.sig_chunks; c += blockDim.x) atomicExch(args.rowsig + c, kSigReleased);
         return;
@@ -423,7 +429,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
         OptConsts oc{};
-        if (kMode == kModeBwdUpdate) oc = opt_consts(args.opt);
+        if (kUpd) oc = opt_consts(args.opt);
         uint32_t acc_phase = 0;
         for (int tile = cid; tile < args.ntiles; tile += ncl) {
             const TileCoord tc = args.tiles[tile];
@@ -485,7 +491,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                         }
                     }
                 }
-            } else if (kMode == kModeBwdUpdate) {
+            } else if (kUpd) {
                 // stage the finished tile (thread = row) in the ring, then update it
                 // coalesced (thread = column) with all 8 epilogue warps
                 float4* gr = reinterpret_cast<float4*>(args.ring + (int64_t)blockIdx.x * kRingTile +
@@ -499,7 +505,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 }
                 __threadfence_block();
                 asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));  // whole tile in the ring
-                update_tile_epi(args, oc, args.ring + (int64_t)blockIdx.x * kRingTile,
+                update_tile_epi<kMode == kModeBwdUpdateVtq>(args, oc, args.ring + (int64_t)blockIdx.x * kRingTile,
                                 (int64_t)tc.a * kPairM + rank * 128, (int64_t)tc.c0, warp - 2, lane,
                                 reinterpret_cast<float*>(auxbuf));
                 asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));  // ring consumed
@@ -741,7 +747,10 @@ void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBuf
         a.sig_chunks = (int)P.sig_expect.size();
     }
     LaunchScope ls(P, KK_GEMM_BWD, st);
-    launchq<kModeBwdUpdate>(P, tm(P.tmap_rq_a), tm(db ? db->tmap_vtq_cur : P.tmap_vtq_b), a, st);
+    if (a.vtq)
+        launchq<kModeBwdUpdateVtq>(P, tm(P.tmap_rq_a), tm(db->tmap_vtq_cur), a, st);
+    else
+        launchq<kModeBwdUpdate>(P, tm(P.tmap_rq_a), tm(db ? db->tmap_vtq_cur : P.tmap_vtq_b), a, st);
 }
 
 }  // namespace sos

@@ -62,7 +62,8 @@ struct GemmArgs {
     int skew_sleep;            // ns between polls of the progress counter
     unsigned long long* dbg;   // SOS_GEMM_STATS: per-role wait cycles (instrumentation only)
     int kserp;                 // walk K backwards on odd local tiles (L2 reuse across waves)
-    int probe;                 // SOS_GEMM_PROBE (experiment, wrong results): 1 = K-blocks mod 8, 2 = also tile 0, 4 = 2 with B loaded only on the first ring pass
+    int probe;                 // SOS_GEMM_PROBE (experiment, wrong results): 1 = K-blocks mod 8,
+                               // 2 = also tile 0, 4 = 2 with B loaded only on the first ring pass
     // kModeBwdUpdate(Vtq): the optimiser step of PAPER.md:221, applied by the epilogue warps
     float* ring;  // per-CTA staging of the finished gradient tile (128 x 160 fp32, L2-resident)
     float* V;
@@ -73,7 +74,7 @@ struct GemmArgs {
     const DevOpt* opt;  // optimiser parameters, step count t, stopping tolerance
     int use_stop;       // apply the sos_opt_set_stop rule
     // kModeBwdUpdate(Vtq) inside sos_descend (vq_next != nullptr): the update also
-    // write the int8 slices of the updated V (scale kHeadroom * vrow_cur) and the
+    // writes the int8 slices of the updated V (scale kHeadroom * vrow_cur) and the
     // exact row / column maxima of the updated V for the next step
     uint8_t* vq_next;
     int64_t rowsV, nkbV;
@@ -88,7 +89,7 @@ struct GemmArgs {
     int64_t rowsVT;
     int64_t nkbN;
     const unsigned* vcol;
-    // kModeBwdUpdate, last step of sos_solve_host: after the update of a tile is
+    // kModeBwdUpdate(Vtq), last step of sos_solve_host: after the update of a tile is
     // stored, both CTAs of the pair add 1 to rowsig[tile.a / sig_blocks] (system
     // scope) so a copy stream can ship finished row chunks of V while the rest runs
     unsigned* rowsig;

@@ -519,12 +519,13 @@ static int ensure_vtq2(Plan& P) {
 }
 
 static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const float* p, double* losses,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool first = false) {
     CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
     CK(cudaMemsetAsync(P.d_coef, 0, (size_t)P.idx->M * 4, st));
     const bool vu = P.vtq_from_update;
-    // VTQ[b] came from the previous update (or the prologue); else the forward packs it
-    launch_gemm_fwd(P, P.d_coef, vu ? nullptr : V, st, d.urow[b], d.vcol[b]);
+    // VTQ[b] came from the previous update; else (and in the first step of a call,
+    // into VTQ[0] = P.d_vtq with the exact column maxima) the forward packs it
+    launch_gemm_fwd(P, P.d_coef, vu && !first ? nullptr : V, st, d.urow[b], d.vcol[b]);
     launch_residual(P, P.d_coef, p, P.d_res, st);
     launch_step_begin(P, losses, st);  // t += 1, losses[k] = L(V_t)
     launch_pack_r(P, P.d_res, st, 1);
@@ -556,7 +557,7 @@ static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps
             CK(cudaEventRecord(P.sig_ev, st));
         }
         P.sig_on = sig;
-        const int r = descend_step(P, d, (int)(t & 1), V_dev, p_dev, losses_dev, st);
+        const int r = descend_step(P, d, (int)(t & 1), V_dev, p_dev, losses_dev, st, t == 0);
         P.sig_on = false;
         return r;
     };
@@ -566,10 +567,8 @@ static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps
     // step 0 starts from the exact maxima and slices of the caller's V
     launch_pack_v(P, V_dev, st, d.vrowx[0], d.vcol[0]);
     CK(cudaMemcpyAsync(d.urow[0], d.vrowx[0], P.rowsV * 4, cudaMemcpyDeviceToDevice, st));
-    if (P.vtq_from_update) {
-        launch_pack_vtq(P, V_dev, st, d.vcol[0]);
+    if (P.vtq_from_update)  // step 0's forward packs VTQ[0] with the exact column maxima
         CK(cudaMemcpyAsync(d.ucol[0], d.vcol[0], P.rowsVT * 4, cudaMemcpyDeviceToDevice, st));
-    }
     if ((rc = plain_step(0))) return rc;
     int64_t left = steps - 1;
     const bool timing = P.timing && P.timing->on;  // per-kernel events need plain launches

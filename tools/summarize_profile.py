@@ -15,8 +15,10 @@ for r in rows[1:]:
 ids = sorted(d)
 # one full step: from the 2nd-to-last forward GEMM up to the next forward GEMM
 fw = [i for i in ids if "k_gemmq<0>" in d[i]["k"]]
-pairs = [(x, y) for x, y in zip(fw, fw[1:]) if not any("k_vmax" in d[i]["k"] for i in ids if x <= i < y)]
-a, b = pairs[-1]  # a steady-state step (no per-call prologue inside)
+# a steady-state step: the forward follows the previous step's fixup (not a call's prologue)
+pairs = [(x, y) for x, y in zip(fw, fw[1:])
+         if x - 1 in d and "fixup" in d[x - 1]["k"] and not any("k_vmax" in d[i]["k"] for i in ids if x <= i < y)]
+a, b = pairs[-1]
 tot = sum(d[i]["gpu__time_duration.sum"] for i in ids if a <= i < b)
 print(f"one step in the ncu list (IDs {a}..{b - 1}): {tot / 1e6:.3f} ms")
 agg = OrderedDict()

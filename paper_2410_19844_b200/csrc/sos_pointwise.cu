@@ -271,93 +271,6 @@ __global__ void __launch_bounds__(256, 6) k_pack_rq_sym(const uint32_t* __restri
     }
 }
 
-// ----------------------------------------------------- fused row packers ----
-// One pass per row: a block stages a whole row in shared memory (contiguous
-// loads for V, gathers through PT for R), reduces the row maximum, then slices
-// the row from shared memory -- no separate maxima pass, and each residual is
-// gathered once per step.
-__device__ __forceinline__ float block_max(float m, float* red, int nthreads) {
-    m = warp_max(m);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    float x = red[0];
-    for (int w = 1; w < nthreads / 32; ++w) x = fmaxf(x, red[w]);
-    return x;
-}
-
-// slice the staged row (nkb * 64 floats in buf) into a Q-layout; chunk cc = 16 values
-__device__ __forceinline__ void slice_row(const float* buf, int64_t nkb, int64_t row, int64_t rows_total, float c,
-                                          uint8_t* __restrict__ Q, int nthreads) {
-    const int64_t chunks = nkb * 4;
-    for (int64_t cc = threadIdx.x; cc < chunks; cc += nthreads) {
-        const float4* s4 = reinterpret_cast<const float4*>(buf + cc * 16);
-        float x[16];
-        const int rot = threadIdx.x & 3;  // rotate the 4 float4 reads: fewer bank conflicts
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int qq = (q + rot) & 3;
-            const float4 f = s4[qq];
-            x[4 * qq] = f.x; x[4 * qq + 1] = f.y; x[4 * qq + 2] = f.z; x[4 * qq + 3] = f.w;
-        }
-        uint4 q[3];
-        slice16(x, c, q);
-        store_q16(Q, cc >> 2, row, (int)(cc & 3), nkb, rows_total, q);
-    }
-}
-
-// RQ rows with their maxima (rrow): row i of R gathered through PT once.  Lane
-// l of a warp owns column j = base + l: for a fixed row, consecutive j give
-// nearby ranks rank(alpha_i + alpha_j) in colex order, so a warp's 32 gathers
-// fall into few 32-byte sectors of res.
-constexpr int kRThreads = 512;
-__global__ void __launch_bounds__(kRThreads, 2) k_pack_r_rows(const uint32_t* __restrict__ pt,
-                                                              const float* __restrict__ res, int64_t Np, int64_t nkb,
-                                                              unsigned* __restrict__ rrow, uint8_t* __restrict__ RQ,
-                                                              const Scalars* sc, const DevOpt* opt, int use_stop) {
-    if (descent_stopped(sc, opt, use_stop)) return;
-    extern __shared__ float buf[];  // nkb * 64 floats = the row (K = j padded to 64)
-    __shared__ float red[kRThreads / 32];
-    const int64_t K = nkb * kPtW;
-    for (int64_t i = blockIdx.x; i < Np; i += gridDim.x) {
-        float m = 0.f;
-        const uint32_t* prow = pt + i * kPtW;
-        // batches of kRB columns per thread; the ranks of batch b+1 are loaded
-        // while the residuals of batch b are gathered (PT latency hidden)
-        constexpr int kRB = 8;
-        const int64_t step = (int64_t)kRThreads * kRB;
-        uint32_t kn[kRB];
-#pragma unroll
-        for (int u = 0; u < kRB; ++u) {
-            const int64_t j = threadIdx.x + (int64_t)u * kRThreads;
-            kn[u] = j < K ? __ldg(prow + (j / kPtW) * Np * kPtW + (j % kPtW)) : kInvalidRank;
-        }
-        for (int64_t j0 = 0; j0 < K; j0 += step) {
-            uint32_t kc[kRB];
-#pragma unroll
-            for (int u = 0; u < kRB; ++u) kc[u] = kn[u];
-            if (j0 + step < K) {
-#pragma unroll
-                for (int u = 0; u < kRB; ++u) {
-                    const int64_t j = j0 + step + threadIdx.x + (int64_t)u * kRThreads;
-                    kn[u] = j < K ? __ldg(prow + (j / kPtW) * Np * kPtW + (j % kPtW)) : kInvalidRank;
-                }
-            }
-            float x[kRB];
-#pragma unroll
-            for (int u = 0; u < kRB; ++u) x[u] = kc[u] != kInvalidRank ? __ldg(res + kc[u]) : 0.f;
-#pragma unroll
-            for (int u = 0; u < kRB; ++u) {
-                const int64_t j = j0 + threadIdx.x + (int64_t)u * kRThreads;
-                if (j < K) buf[j] = x[u];
-                m = fmaxf(m, fabsf(x[u]));
-            }
-        }
-        m = block_max(m, red, kRThreads);
-        if (threadIdx.x == 0) rrow[i] = __float_as_uint(m);
-        slice_row(buf, nkb, i, Np, slice_scale(__float_as_uint(m)), RQ, kRThreads);
-        __syncthreads();
-    }
-}
 
 // -------------------------------------------------------------- launches ---
 static int grid_for(const Plan& P, int64_t work, int threads, int per_sm = 8) {
@@ -409,9 +322,6 @@ void launch_step_begin(Plan& P, double* losses, cudaStream_t st) {
     k_step_begin<<<1, 1, 0, st>>>(P.d_opt, P.d_scal, losses);
 }
 
-// rows whose staging buffer fits shared memory take the fused one-pass packers
-constexpr int64_t kRowSmemMax = 200 * 1024;
-
 // maxima (one read of V) + VQ (one elementwise pass)
 void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, unsigned* vcol) {
     if (!vrow) vrow = P.d_vrow;
@@ -422,9 +332,8 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, uns
 }
 
 // row maxima + RQ: the row maxima come from the lattice DP (sos_index.cu, a
-// few tens of millions of lookups instead of N^2 gathers), then one streaming
-// pass gathers and slices R.  SOS_RPACK_FUSED=1 selects the one-pass fused
-// packer (row staged in shared memory), SOS_RPACK_TWOPASS=1 the gathered maxima.
+// few tens of millions of lookups instead of N^2 gathers) or the direct pass,
+// then one streaming pass gathers and slices R.
 // R row maxima: the lattice DP costs ~d launches plus sum_D C(n+D-1, D) * n
 // lookups; the direct gather over PT (k_rmax) one launch plus N^2 lookups.
 // Small problems and many variables favour the direct pass (config 2: 60 -> 15
@@ -439,31 +348,15 @@ static bool rmax_direct_is_cheaper(const Index& ix) {
 }
 
 void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop) {
-    const int64_t Np = P.idx->Np;
-    const int64_t row_bytes = Np * 4;
-    static const bool fused = getenv("SOS_RPACK_FUSED") && atoi(getenv("SOS_RPACK_FUSED"));
     static const char* tp_env = getenv("SOS_RPACK_TWOPASS");
-    if (!fused || row_bytes > kRowSmemMax) {
-        if (tp_env ? atoi(tp_env) != 0 : rmax_direct_is_cheaper(*P.idx)) {
-            launch_rmax(P, res, st, use_stop);
-        } else {
-            LaunchScope ls(P, KK_ABSMAX_R, st);
-            launch_rmax_dp(*P.idx, res, P.d_rlev, P.d_rrow, st, P.d_scal, P.d_opt, use_stop);
-            P.launches += P.idx->d - 1;  // one kernel per lattice level (the scope counts one)
-        }
-        launch_pack_rq(P, res, st, use_stop);
-        return;
+    if (tp_env ? atoi(tp_env) != 0 : rmax_direct_is_cheaper(*P.idx)) {
+        launch_rmax(P, res, st, use_stop);
+    } else {
+        LaunchScope ls(P, KK_ABSMAX_R, st);
+        launch_rmax_dp(*P.idx, res, P.d_rlev, P.d_rrow, st, P.d_scal, P.d_opt, use_stop);
+        P.launches += P.idx->d - 1;  // one kernel per lattice level (the scope counts one)
     }
-    LaunchScope ls(P, KK_PACK_R, st);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_pack_r_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmemMax);
-        attr = true;
-    }
-    const int bps = row_bytes <= 100 * 1024 ? 2 : 1;
-    const unsigned blocks = (unsigned)std::min<int64_t>(Np, (int64_t)P.num_sms * bps);
-    k_pack_r_rows<<<blocks, kRThreads, (size_t)(P.nkbN * kPtW * 4), st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow,
-                                                                         P.d_rq, P.d_scal, P.d_opt, use_stop);
+    launch_pack_rq(P, res, st, use_stop);
 }
 
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop) {

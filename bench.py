@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-loss-grad", action="store_true")
     return ap.parse_args()
 
 
@@ -295,6 +296,20 @@ def run_ours(args):
                "d2h_bytes_per_step": int((N * r * 4 + args.steps * 8) / args.steps),
                "api": "sos_solve_host (host V and p, K steps per call, copies inside the timed region)"}
 
+    # ---- sos_loss_grad alone: north_star's fused loss + gradient call (no update) ----
+    lg_ms = None
+    if not args.no_loss_grad:
+        for _ in range(2):
+            plan.loss_grad(V, p)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            plan.loss_grad(V, p)
+        e1.record()
+        torch.cuda.synchronize()
+        lg_ms = max_over_ranks(e0.elapsed_time(e1) / 3, dist, dev)
+
     if rank != 0:
         if ws > 1:
             dist.destroy_process_group()
@@ -352,6 +367,10 @@ def run_ours(args):
         "clocks": clk,
         "loss_rel": {"first": float(loss_hist[0] / pnorm2), "last": float(loss_hist[-1] / pnorm2)},
         "e2e": e2e,
+        "loss_grad": None if lg_ms is None else {
+            "api": "sos_loss_grad (forward + residual/loss + R slices + backward 4RV into a gradient buffer)",
+            "ms_per_call": lg_ms, "tflops": flops["step"] / (lg_ms / 1e3) / 1e12,
+            "frac": flops["step"] / (lg_ms / 1e3) / 1e12 / peak_tensor},
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)

@@ -174,7 +174,10 @@ int sos_step(sos_plan *plan, float *V_dev, const float *p_dev, double *loss_dev,
  * the per-step maxima and slicing passes over V disappear.  Results agree with
  * sos_step to the slice precision (~1e-7 relative), not bit for bit.  V_dev must
  * not be modified by anyone else during the call (it is asynchronous on
- * `stream`).  Honours sos_opt_set_lr / sos_opt_set_stop settings. */
+ * `stream`).  Honours sos_opt_set_lr / sos_opt_set_stop settings.  For long K
+ * (N >= 8192 monomials) the update also writes the next step's V^T slices,
+ * into a second V^T slice buffer (3 * r' * N' bytes, r' = r rounded up to 160,
+ * N' = N rounded up to 64) the plan allocates on the first call. */
 int sos_descend(sos_plan *plan, float *V_dev, const float *p_dev, int64_t steps, double *losses_dev,
                 void *stream);
 

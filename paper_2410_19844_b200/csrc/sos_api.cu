@@ -527,7 +527,7 @@ static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const fl
     // into VTQ[0] = P.d_vtq with the exact column maxima) the forward packs it
     launch_gemm_fwd(P, P.d_coef, vu && !first ? nullptr : V, st, d.urow[b], d.vcol[b]);
     launch_residual(P, P.d_coef, p, P.d_res, st);
-    launch_step_begin(P, losses, st);  // t += 1, losses[k] = L(V_t)
+    launch_step_begin(P, nullptr, st, true);  // t += 1, losses[k] = L(V_t) (the call's array, DevOpt)
     launch_pack_r(P, P.d_res, st, 1);
     CK(cudaMemsetAsync(d.vrowx[b ^ 1], 0, P.rowsV * 4, st));
     CK(cudaMemsetAsync(d.vcol[b ^ 1], 0, P.rowsVT * 4, st));
@@ -564,6 +564,8 @@ static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps
     int rc = upload_opt(P, st);
     if (rc) return rc;
     CK(cudaMemsetAsync(&P.d_opt->loss_idx, 0, sizeof(long long), st));
+    P.h_losses = losses_dev;  // pageable source: staged synchronously by the copy below
+    CK(cudaMemcpyAsync(&P.d_opt->losses, &P.h_losses, sizeof(double*), cudaMemcpyHostToDevice, st));
     // step 0 starts from the exact maxima and slices of the caller's V
     launch_pack_v(P, V_dev, st, d.vrowx[0], d.vcol[0]);
     CK(cudaMemcpyAsync(d.urow[0], d.vrowx[0], P.rowsV * 4, cudaMemcpyDeviceToDevice, st));
@@ -575,7 +577,7 @@ static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps
     const int64_t keep_plain = sig_last ? 1 : 0;      // the signalling step is never replayed
     if (left >= 2 + keep_plain && !timing) {
         // steps 1, 2 (parities 1, 0) captured once as a graph, replayed for every pair
-        const void* key[3] = {V_dev, p_dev, losses_dev};
+        const void* key[3] = {V_dev, p_dev, nullptr};  // the loss array is read from DevOpt
         if (!P.gexec || memcmp(key, P.gkey, sizeof(key)) != 0) {
             if (P.gexec) {
                 cudaGraphExecDestroy(P.gexec);

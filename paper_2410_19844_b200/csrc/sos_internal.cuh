@@ -87,6 +87,8 @@ struct DevOpt {
     double stop_tol;        // sos_opt_set_stop (0 = off), uploaded by the host
     long long t;            // Adam step count (device-managed)
     long long loss_idx;     // sos_descend: next entry of the caller's loss array (device-managed)
+    double* losses;         // sos_descend: the call's loss array (set per call, so the captured
+                            // step graph does not depend on it)
 };
 
 // the device-side stopping rule of sos_step (sos_opt_set_stop), read after
@@ -155,7 +157,8 @@ struct Plan {
     DevOpt* d_opt;    // device copy of the optimiser parameters + step counter
     // sos_descend: a captured pair of steps, replayed with cudaGraphLaunch
     cudaGraphExec_t gexec;
-    const void* gkey[3];   // (V, p, losses) the graph was captured for
+    const void* gkey[3];   // (V, p, -) the graph was captured for
+    double* h_losses;      // host copy of the current sos_descend call's loss array pointer
     int64_t glaunches;     // kernels per replay (launch accounting)
     // sos_solve_host: device staging of the caller's host buffers (lazy)
     float* d_hV;
@@ -220,7 +223,8 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow = nu
                    unsigned* vcol = nullptr);  // maxima + VQ
 void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st, const unsigned* vcol = nullptr);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
-void launch_step_begin(Plan& P, double* losses, cudaStream_t st);
+// losses_from_opt: record into the loss array set for the current sos_descend call
+void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt = false);
 void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop);
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop);
 void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop);  // maxima + RQ

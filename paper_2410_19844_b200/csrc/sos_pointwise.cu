@@ -312,14 +312,15 @@ void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop) {
 
 // one thread: t += 1 (Adam bias correction of this step), and in sos_descend
 // the loss of this step into the caller's array
-__global__ void k_step_begin(DevOpt* opt, const Scalars* sc, double* losses) {
+__global__ void k_step_begin(DevOpt* opt, const Scalars* sc, double* losses, int from_opt) {
     opt->t += 1;
+    if (from_opt) losses = opt->losses;
     if (losses) losses[opt->loss_idx++] = sc->loss;
 }
 
-void launch_step_begin(Plan& P, double* losses, cudaStream_t st) {
+void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt) {
     LaunchScope ls(P, KK_UPDATE, st);
-    k_step_begin<<<1, 1, 0, st>>>(P.d_opt, P.d_scal, losses);
+    k_step_begin<<<1, 1, 0, st>>>(P.d_opt, P.d_scal, losses_from_opt ? nullptr : losses, losses_from_opt ? 1 : 0);
 }
 
 // maxima (one read of V) + VQ (one elementwise pass)

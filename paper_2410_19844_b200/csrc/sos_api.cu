@@ -238,6 +238,12 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         // would lengthen the update-bound backward (profiles/r1_vtq_next_ab.log)
         const char* e = getenv("SOS_VTQ_UPDATE");
         P.vtq_from_update = e ? atoi(e) != 0 : P.nkbN >= 128;
+        // short K: a tile's MMAs (~nkbN x 0.5 us) cannot hide the fused update
+        // (~25 us per tile), so store the gradient and update with all SMs
+        // (profiles/r1_update_split_ab.log)
+        const char* u = getenv("SOS_UPDATE_SPLIT");
+        P.update_split = u ? atoi(u) != 0 : P.nkbN < kUpdateSplitKb;
+        if (P.update_split) P.vtq_from_update = false;
     }
     // row chunks of the last step's V release = the raster's row groups
     P.sig_blocks = (int)tile_group();
@@ -257,7 +263,8 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         (rc = dalloc(&P.d_progress, 2 * sizeof(unsigned long long))) ||
         (rc = dalloc(&P.d_tiles_fwd, std::max<size_t>(1, tf.size()) * sizeof(TileCoord))) ||
         (rc = dalloc(&P.d_tiles_bwd, std::max<size_t>(1, tb.size()) * sizeof(TileCoord))) ||
-        (rc = dalloc(&P.d_rowsig, std::max<size_t>(1, P.sig_expect.size()) * sizeof(unsigned)))) {
+        (rc = dalloc(&P.d_rowsig, std::max<size_t>(1, P.sig_expect.size()) * sizeof(unsigned))) ||
+        (P.update_split && (rc = dalloc(&P.d_grad, (size_t)N * r * sizeof(float))))) {
         sos_plan_destroy(pl);
         return rc;
     }
@@ -318,6 +325,7 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_tiles_fwd);
     cudaFree(P.d_tiles_bwd);
     cudaFree(P.d_rowsig);
+    cudaFree(P.d_grad);
     if (P.copy_st) cudaStreamDestroy(P.copy_st);
     if (P.sig_ev) cudaEventDestroy(P.sig_ev);
     if (P.timing) {
@@ -659,7 +667,8 @@ int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t ste
         return fail(SOS_ERR_CUDA, "H2D copy");
     // ship V back in row chunks while the last step's backward still runs (needs
     // stream memory operations; otherwise one copy after the last step)
-    const PFN_wait_value32 wait = steps > 0 ? wait_value_fn() : nullptr;
+    // (the split update of short-K plans does not release chunks: one copy at the end)
+    const PFN_wait_value32 wait = steps > 0 && !P.update_split ? wait_value_fn() : nullptr;
     bool overlap = wait != nullptr;
     if (overlap && !P.copy_st)
         overlap = cudaStreamCreateWithFlags(&P.copy_st, cudaStreamNonBlocking) == cudaSuccess &&

@@ -719,6 +719,18 @@ void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st) {
 // optimiser step (GD or Adam): the gradient never makes an HBM round trip.  The
 // GEMM reads the packed copy VTQ, never V, so updating V in place is safe.
 void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBufs* db) {
+    if (P.update_split) {
+        // short K: the tiles' MMAs are too short to hide the update, so the
+        // gradient goes through HBM and the update runs on all SMs
+        GemmArgs a = bwd_args(P, db ? db->ucol_cur : nullptr);
+        a.grad = P.d_grad;
+        {
+            LaunchScope ls(P, KK_GEMM_BWD, st);
+            launchq<kModeBwdStore>(P, tm(P.tmap_rq_a), tm(db ? db->tmap_vtq_cur : P.tmap_vtq_b), a, st);
+        }
+        launch_update_split(P, V, st, db);
+        return;
+    }
     GemmArgs a = bwd_args(P, db ? db->ucol_cur : nullptr);
     if (db) {
         a.vq_next = P.d_vq;

@@ -131,6 +131,9 @@ struct Plan {
     uint8_t* d_vtq;   // VTQ
     uint8_t* d_vtq2;  // sos_descend: second VTQ buffer (the update writes step t+1's while step t's is read)
     bool vtq_from_update;  // sos_descend: the backward's update writes the next VTQ (long K only)
+    bool update_split;     // short K: gradient stored, then the all-SM k_update (the fused update
+                           // in 8 warps per SM would bound the backward)
+    float* d_grad;         // N x r gradient buffer of the split update (update_split only)
     uint8_t* d_rq;    // RQ
     unsigned* d_vrow; // max_k |V_ik| (float bits), rowsV
     unsigned* d_vcol; // max_j |V_jk| (float bits), rowsVT
@@ -238,6 +241,11 @@ struct DescendBufs {
     const uint8_t* tmap_vtq_cur;  // tensor map of the current VTQ buffer
     uint8_t* vtq_next;         // VTQ buffer the update writes for the next step
 };
+// plans with fewer K-blocks (N / 64) than this use the split update (Plan::update_split)
+constexpr int kUpdateSplitKb = 48;
+// the optimiser step as its own all-SM kernel (update_split), same arithmetic and
+// outputs as the backward's fused update (db: sos_descend's next-step VQ + maxima)
+void launch_update_split(Plan& P, float* V, cudaStream_t st, const DescendBufs* db);
 // slices written by the update use kHeadroom x the current row maximum
 constexpr float kHeadroom = 2.f;
 

@@ -318,6 +318,132 @@ __global__ void k_step_begin(DevOpt* opt, const Scalars* sc, double* losses, int
     if (losses) losses[opt->loss_idx++] = sc->loss;
 }
 
+// The optimiser step over the whole N x r gradient (short-K problems, see
+// Plan::update_split).  Block tile = 16 rows x 256 columns: warp w owns rows
+// 2w, 2w+1, lane l the columns l + 32e (e < 8), so every access is a coalesced
+// row segment and all 64 loads of a thread are in flight together; the new
+// values are staged in shared memory for the next step's VQ chunks (task =
+// row x 16-column chunk, scale kHeadroom * old row max); row maxima by warp
+// shuffles, column maxima per thread over its rows, then across the 8 warps.
+constexpr int kUpdCols = 256, kUpdLd = kUpdCols + 4;
+__global__ void __launch_bounds__(256) k_update(const float* __restrict__ grad, float* __restrict__ V,
+                                                float* __restrict__ m, float* __restrict__ v, int64_t N, int64_t r,
+                                                int adam, const DevOpt* opt, const Scalars* sc,
+                                                uint8_t* __restrict__ vq_next, int64_t rowsV, int64_t nkbV,
+                                                const unsigned* __restrict__ vrow_cur, unsigned* __restrict__ vrow_next,
+                                                unsigned* __restrict__ vcol_next) {
+    if (descent_stopped(sc, opt, 1)) return;
+    constexpr int kE = kUpdCols / 32;
+    __shared__ float cst[6];
+    __shared__ __align__(16) float stage[16 * kUpdLd];
+    __shared__ float cm_s[8][kUpdCols];
+    if (threadIdx.x == 0) {
+        const DevOpt o = *opt;
+        cst[0] = o.lr;
+        cst[1] = o.b1;
+        cst[2] = o.b2;
+        cst[3] = o.eps;
+        cst[4] = (float)((double)o.lr / (1.0 - pow((double)o.b1, (double)o.t)));
+        cst[5] = (float)(1.0 / sqrt(1.0 - pow((double)o.b2, (double)o.t)));
+    }
+    __syncthreads();
+    const float lr = cst[0], b1 = cst[1], b2 = cst[2], eps = cst[3], lr_c1 = cst[4], isc2 = cst[5];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, t = threadIdx.x;
+    const bool q = vq_next != nullptr;
+    const int64_t col_tiles = (r + kUpdCols - 1) / kUpdCols, row_tiles = (N + 15) / 16;
+    for (int64_t blk = blockIdx.x; blk < row_tiles * col_tiles; blk += gridDim.x) {
+        const int64_t row0 = (blk / col_tiles) * 16, col0 = (blk % col_tiles) * kUpdCols;
+        float gv[2][kE], x[2][kE], mm[2][kE], vv[2][kE];
+        bool ok[2][kE];
+        int64_t ro[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int64_t i = row0 + 2 * w + k;
+            ro[k] = i * r + col0 + lane;
+#pragma unroll
+            for (int e = 0; e < kE; ++e) {
+                ok[k][e] = i < N && col0 + lane + 32 * e < r;
+                gv[k][e] = ok[k][e] ? grad[ro[k] + 32 * e] : 0.f;
+                x[k][e] = ok[k][e] ? V[ro[k] + 32 * e] : 0.f;
+                if (adam) {
+                    mm[k][e] = ok[k][e] ? m[ro[k] + 32 * e] : 0.f;
+                    vv[k][e] = ok[k][e] ? v[ro[k] + 32 * e] : 0.f;
+                }
+            }
+        }
+        float cm[kE];
+#pragma unroll
+        for (int e = 0; e < kE; ++e) cm[e] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            float mx = 0.f;
+#pragma unroll
+            for (int e = 0; e < kE; ++e) {
+                float xn = 0.f;
+                if (ok[k][e]) {
+                    if (adam) {
+                        mm[k][e] = b1 * mm[k][e] + (1.f - b1) * gv[k][e];
+                        vv[k][e] = b2 * vv[k][e] + (1.f - b2) * gv[k][e] * gv[k][e];
+                        xn = x[k][e] - lr_c1 * mm[k][e] / (sqrtf(vv[k][e]) * isc2 + eps);
+                        m[ro[k] + 32 * e] = mm[k][e];
+                        v[ro[k] + 32 * e] = vv[k][e];
+                    } else {
+                        xn = x[k][e] - lr * gv[k][e];
+                    }
+                    V[ro[k] + 32 * e] = xn;
+                }
+                if (q) {
+                    stage[(2 * w + k) * kUpdLd + lane + 32 * e] = xn;
+                    mx = fmaxf(mx, fabsf(xn));
+                    cm[e] = fmaxf(cm[e], fabsf(xn));
+                }
+            }
+            if (q) {
+                mx = warp_max(mx);
+                const int64_t i = row0 + 2 * w + k;
+                if (lane == 0 && i < N && mx > 0.f) atomicMax(vrow_next + i, __float_as_uint(mx));
+            }
+        }
+        if (q) {
+#pragma unroll
+            for (int e = 0; e < kE; ++e) cm_s[w][lane + 32 * e] = cm[e];
+            __syncthreads();
+            {   // task t = (row t / 16, 16-column chunk t % 16)
+                const int rr = t >> 4, cq = t & 15;
+                const int64_t i = row0 + rr, k0 = col0 + 16 * cq;
+                if (i < N && k0 < r) {
+                    float xs[16];
+                    const float4* s4 = reinterpret_cast<const float4*>(stage + rr * kUpdLd + 16 * cq);
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const float4 f = s4[q4];
+                        xs[4 * q4] = f.x; xs[4 * q4 + 1] = f.y; xs[4 * q4 + 2] = f.z; xs[4 * q4 + 3] = f.w;
+                    }
+                    const float um = kHeadroom * __uint_as_float(__ldg(vrow_cur + i));
+                    uint4 qq[3];
+                    slice16(xs, slice_scale(__float_as_uint(um)), qq);
+                    store_q16(vq_next, k0 >> 6, i, (int)((k0 >> 4) & 3), nkbV, rowsV, qq);
+                }
+            }
+            {   // column t: maximum over the 16 rows (8 warps x 2)
+                float c = 0.f;
+#pragma unroll
+                for (int ww = 0; ww < 8; ++ww) c = fmaxf(c, cm_s[ww][t]);
+                if (col0 + t < r && c > 0.f) atomicMax(vcol_next + col0 + t, __float_as_uint(c));
+            }
+            __syncthreads();
+        }
+    }
+}
+
+void launch_update_split(Plan& P, float* V, cudaStream_t st, const DescendBufs* db) {
+    LaunchScope ls(P, KK_UPDATE, st);
+    const int64_t N = P.idx->N, blocks = ((N + 15) / 16) * ((P.r + kUpdCols - 1) / kUpdCols);
+    k_update<<<grid_for(P, blocks * 256, 256), 256, 0, st>>>(
+        P.d_grad, V, P.d_m, P.d_v, N, P.r, P.opt_kind == 1, P.d_opt, P.d_scal, db ? P.d_vq : nullptr, P.rowsV,
+        P.nkbV, db ? db->vrow_cur : nullptr, db ? db->vrow_next : nullptr, db ? db->vcol_next : nullptr);
+}
+
 void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt) {
     LaunchScope ls(P, KK_UPDATE, st);
     k_step_begin<<<1, 1, 0, st>>>(P.d_opt, P.d_scal, losses_from_opt ? nullptr : losses, losses_from_opt ? 1 : 0);

@@ -534,9 +534,11 @@ def test_descend_matches_steps(sos, kind, lr, r, vtq_update, monkeypatch):
     Row 5 and column 9 of V0 are zero, so their first update leaves the
     headroom window and is re-sliced by the fixup kernels (VQ row, VTQ row).
     r = 336 (a multiple of 4) and r = 330 (rows not 16-byte aligned).
-    vtq_update = 1 forces the path where the update also writes the next
-    step's V^T slices (the default only for long K)."""
+    vtq_update = 1 forces the fused update that also writes the next step's
+    V^T slices (the default only for long K); vtq_update = 0 runs the split
+    update (gradient stored, all-SM k_update: the default for short K)."""
     monkeypatch.setenv("SOS_VTQ_UPDATE", vtq_update)  # read at plan creation
+    monkeypatch.setenv("SOS_UPDATE_SPLIT", "0" if vtq_update == "1" else "1")  # both update paths
     c = si.CONFIGS["c1_n8_2d8"]
     o = oracle(c.n, c.d)
     ix = sos.SosIndex(c.n, c.d)

@@ -5,7 +5,8 @@ switches, read once per process, hence subprocesses) must agree:
   same R slices and a bit-identical backward;
 * V^T slices from the forward's aux warps vs the all-SM pack kernel: same bytes,
   bit-identical backward inside the descent;
-* next-step V^T slices from the backward's update vs packed by the forward:
+* next-step V^T slices from the backward's update vs packed by the forward,
+  and the fused update vs the split one (gradient stored, all-SM k_update):
   the descent agrees to the slice precision;
 * narrow tiles vs full 160-wide grid tiles: the same integer products, so a
   bit-identical plain backward; the descent (forward atomics in another order)
@@ -60,9 +61,19 @@ def test_narrow_vs_full_tiles(tmp_path):
 
 @pytest.mark.gpu
 def test_vtq_from_update_vs_forward_pack(tmp_path):
-    a = _run(tmp_path, "upd", {"SOS_VTQ_UPDATE": "1"})
-    b = _run(tmp_path, "fwd", {"SOS_VTQ_UPDATE": "0"})
+    a = _run(tmp_path, "upd", {"SOS_VTQ_UPDATE": "1", "SOS_UPDATE_SPLIT": "0"})
+    b = _run(tmp_path, "fwd", {"SOS_VTQ_UPDATE": "0", "SOS_UPDATE_SPLIT": "0"})
     assert np.array_equal(a["grad"], b["grad"])  # sos_backward does not use it
+    rel = np.linalg.norm(a["V3"] - b["V3"]) / np.linalg.norm(a["V3"])
+    assert rel <= 1e-6
+    assert np.allclose(a["losses"], b["losses"], rtol=1e-5)
+
+
+@pytest.mark.gpu
+def test_update_fused_vs_split(tmp_path):
+    a = _run(tmp_path, "fused", {"SOS_UPDATE_SPLIT": "0"})
+    b = _run(tmp_path, "split", {"SOS_UPDATE_SPLIT": "1"})
+    assert np.array_equal(a["grad"], b["grad"])
     rel = np.linalg.norm(a["V3"] - b["V3"]) / np.linalg.norm(a["V3"])
     assert rel <= 1e-6
     assert np.allclose(a["losses"], b["losses"], rtol=1e-5)

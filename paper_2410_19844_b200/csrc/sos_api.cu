@@ -278,6 +278,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         cudaMemset(P.d_vcol, 0, (size_t)P.rowsVT * 4) != cudaSuccess ||
         cudaMemset(P.d_rrow, 0, (size_t)Np * 4) != cudaSuccess ||
         cudaMemset(P.d_rq, 0, (size_t)kSlices * P.nkbN * Np * 64) != cudaSuccess ||  // padding rows stay 0
+        cudaMemset(P.d_progress, 0, 2 * sizeof(unsigned long long)) != cudaSuccess ||  // GEMMs reset it themselves
         cudaMemset(P.d_dbuf, 0, (size_t)(4 * P.rowsV + 4 * P.rowsVT) * 4) != cudaSuccess ||
         cudaMemset(P.d_opt, 0, sizeof(DevOpt)) != cudaSuccess) {
         sos_plan_destroy(pl);
@@ -528,17 +529,19 @@ static int ensure_vtq2(Plan& P) {
 
 static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const float* p, double* losses,
                         cudaStream_t st, bool first = false) {
-    CK(cudaMemsetAsync(P.d_scal, 0, sizeof(Scalars), st));
-    CK(cudaMemsetAsync(P.d_coef, 0, (size_t)P.idx->M * 4, st));
+    // no memset nodes inside the replayed steps: the forward clears the loss
+    // accumulators, step_begin clears coef for the next forward and the next
+    // step's maxima (the first step of a call starts from a clean coef)
+    if (first) CK(cudaMemsetAsync(P.d_coef, 0, (size_t)P.idx->M * 4, st));
     const bool vu = P.vtq_from_update;
     // VTQ[b] came from the previous update; else (and in the first step of a call,
     // into VTQ[0] = P.d_vtq with the exact column maxima) the forward packs it
-    launch_gemm_fwd(P, P.d_coef, vu && !first ? nullptr : V, st, d.urow[b], d.vcol[b]);
+    launch_gemm_fwd(P, P.d_coef, vu && !first ? nullptr : V, st, d.urow[b], d.vcol[b], true);
     launch_residual(P, P.d_coef, p, P.d_res, st);
-    launch_step_begin(P, nullptr, st, true);  // t += 1, losses[k] = L(V_t) (the call's array, DevOpt)
+    // t += 1, losses[k] = L(V_t) (the call's array, from DevOpt); clear the next
+    // maxima and the coefficient accumulator (read by the residual, done)
+    launch_step_begin(P, nullptr, st, true, d.vrowx[b ^ 1], P.rowsV, d.vcol[b ^ 1], P.rowsVT, P.d_coef);
     launch_pack_r(P, P.d_res, st, 1);
-    CK(cudaMemsetAsync(d.vrowx[b ^ 1], 0, P.rowsV * 4, st));
-    CK(cudaMemsetAsync(d.vcol[b ^ 1], 0, P.rowsVT * 4, st));
     const DescendBufs db = vu ? DescendBufs{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1], d.ucol[b],
                                             d.tmap_vtq[b], d.vtq[b ^ 1]}
                               : DescendBufs{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1], d.vcol[b],

@@ -55,6 +55,7 @@ struct GemmArgs {
     int64_t Np;
     const uint32_t* pt;
     float* coef;
+    Scalars* zero_scal;  // forward inside sos_descend: clear the loss accumulators first
     float* grad;
     int64_t r;
     unsigned long long* progress;
@@ -283,6 +284,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const bool leader = rank == 0;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
+    if (kFwd && args.zero_scal && blockIdx.x == 0 && threadIdx.x == 0) {
+        args.zero_scal->loss = 0.0;  // the residual that follows accumulates the new loss
+        args.zero_scal->pnorm2 = 0.0;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
@@ -358,7 +363,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
-            if (lane == 0) atomicAdd(args.progress, 1ull << 32);
+            if (lane == 0) {
+                // done marker (releases any CTA still pacing itself); the last CTA to
+                // finish resets the counter for the next launch (no memset per launch)
+                const unsigned long long old = atomicAdd(args.progress, 1ull << 32);
+                if ((old >> 32) + 1 == (unsigned long long)gridDim.x) atomicExch(args.progress, 0ull);
+            }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer --
@@ -620,7 +630,6 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
     int grid = 2 * a.ntiles < sms ? 2 * a.ntiles : sms;
     grid &= ~1;
     if (grid <= 0) return cudaSuccess;
-    cudaMemsetAsync(a.progress, 0, sizeof(unsigned long long), st);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kGemmThreads);
@@ -661,7 +670,7 @@ static bool vtq_in_aux(const Plan& P) {
 }
 
 void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st, const unsigned* urow,
-                     const unsigned* vcol) {
+                     const unsigned* vcol, bool zero_scal) {
     if (V_for_vtq && !vtq_in_aux(P)) {
         launch_pack_vtq(P, V_for_vtq, st, vcol);
         V_for_vtq = nullptr;
@@ -685,6 +694,7 @@ void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t 
     a.Np = P.idx->Np;
     a.pt = P.idx->d_pt;
     a.coef = coef;
+    a.zero_scal = zero_scal ? P.d_scal : nullptr;
     a.progress = P.d_progress;
     LaunchScope ls(P, KK_GEMM_FWD, st);
     launchq<kModeFwd>(P, tm(P.tmap_vq_a), tm(P.tmap_vq_b), a, st);

@@ -226,8 +226,11 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow = nu
                    unsigned* vcol = nullptr);  // maxima + VQ
 void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st, const unsigned* vcol = nullptr);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
-// losses_from_opt: record into the loss array set for the current sos_descend call
-void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt = false);
+// losses_from_opt: record into the loss array set for the current sos_descend call;
+// zero0 / zero1 (n0 / n1 words), zero_coef (M floats): accumulators to clear for the next stage
+void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt = false,
+                       unsigned* zero0 = nullptr, int64_t n0 = 0, unsigned* zero1 = nullptr, int64_t n1 = 0,
+                       float* zero_coef = nullptr);
 void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop);
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop);
 void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop);  // maxima + RQ
@@ -250,7 +253,7 @@ void launch_update_split(Plan& P, float* V, cudaStream_t st, const DescendBufs* 
 constexpr float kHeadroom = 2.f;
 
 void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st, const unsigned* urow = nullptr,
-                     const unsigned* vcol = nullptr);
+                     const unsigned* vcol = nullptr, bool zero_scal = false);
 void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st);
 void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBufs* db = nullptr);
 void launch_descend_fixup_cols(Plan& P, const float* V, const unsigned* vcol_cur, const unsigned* vcol_next,

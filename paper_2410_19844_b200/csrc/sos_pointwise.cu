@@ -312,10 +312,24 @@ void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop) {
 
 // one thread: t += 1 (Adam bias correction of this step), and in sos_descend
 // the loss of this step into the caller's array
-__global__ void k_step_begin(DevOpt* opt, const Scalars* sc, double* losses, int from_opt) {
-    opt->t += 1;
-    if (from_opt) losses = opt->losses;
-    if (losses) losses[opt->loss_idx++] = sc->loss;
+// step bookkeeping (Adam t, loss record) and, inside sos_descend, zeroing of
+// the next step's maxima accumulators (zero0 / zero1: n0 / n1 words) and of
+// the coefficient accumulator of the next forward (zc: nc floats, 16-B aligned)
+__global__ void k_step_begin(DevOpt* opt, const Scalars* sc, double* losses, int from_opt, unsigned* zero0,
+                             int64_t n0, unsigned* zero1, int64_t n1, float* zc, int64_t nc) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        opt->t += 1;
+        if (from_opt) losses = opt->losses;
+        if (losses) losses[opt->loss_idx++] = sc->loss;
+    }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (int64_t e = tid; e < n0 + n1; e += stride) {
+        if (e < n0) zero0[e] = 0u;
+        else zero1[e - n0] = 0u;
+    }
+    for (int64_t e = tid; e < nc / 4; e += stride) reinterpret_cast<float4*>(zc)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t e = (nc / 4) * 4 + tid; e < nc; e += stride) zc[e] = 0.f;
 }
 
 // The optimiser step over the whole N x r gradient (short-K problems, see
@@ -444,9 +458,13 @@ void launch_update_split(Plan& P, float* V, cudaStream_t st, const DescendBufs* 
         P.nkbV, db ? db->vrow_cur : nullptr, db ? db->vrow_next : nullptr, db ? db->vcol_next : nullptr);
 }
 
-void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt) {
+void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt, unsigned* zero0, int64_t n0,
+                       unsigned* zero1, int64_t n1, float* zero_coef) {
     LaunchScope ls(P, KK_UPDATE, st);
-    k_step_begin<<<1, 1, 0, st>>>(P.d_opt, P.d_scal, losses_from_opt ? nullptr : losses, losses_from_opt ? 1 : 0);
+    const int64_t nc = zero_coef ? P.idx->M : 0;
+    const int blocks = zero0 || zero1 || zero_coef ? grid_for(P, std::max<int64_t>(n0 + n1, nc / 4), 256, 4) : 1;
+    k_step_begin<<<blocks, 256, 0, st>>>(P.d_opt, P.d_scal, losses_from_opt ? nullptr : losses, losses_from_opt ? 1 : 0,
+                                         zero0, zero0 ? n0 : 0, zero1, zero1 ? n1 : 0, zero_coef, nc);
 }
 
 // maxima (one read of V) + VQ (one elementwise pass)

@@ -82,7 +82,10 @@ int sos_index_pair_ranks(const sos_index *idx, const int64_t *i_dev, const int64
 
 /* ------------------------------------------------------------------------
  * Plan: workspaces for one (index, r).  Device memory ~ 3*Np*(2*r + Np) bytes
- * (int8 slices of V, V^T and R) plus 8*N*r once Adam is enabled.
+ * (int8 slices of V, V^T and R) plus 8*N*r once Adam is enabled, plus 4*N*r
+ * (a gradient buffer) when N < 3072 (short K: the optimiser step then runs as
+ * its own kernel after the backward instead of inside it), plus a second V^T
+ * slice buffer on the first sos_descend call when N >= 8192.
  * ------------------------------------------------------------------------ */
 int sos_plan_create(const sos_index *idx, int64_t r, sos_plan **out);
 int sos_plan_destroy(sos_plan *plan);

@@ -83,9 +83,9 @@ int sos_index_pair_ranks(const sos_index *idx, const int64_t *i_dev, const int64
 /* ------------------------------------------------------------------------
  * Plan: workspaces for one (index, r).  Device memory ~ 3*Np*(2*r + Np) bytes
  * (int8 slices of V, V^T and R) plus 8*N*r once Adam is enabled, plus 4*N*r
- * (a gradient buffer) when N < 3072 (short K: the optimiser step then runs as
+ * (a gradient buffer) when N <= 3008 (short K: the optimiser step then runs as
  * its own kernel after the backward instead of inside it), plus a second V^T
- * slice buffer on the first sos_descend call when N >= 8192.
+ * slice buffer on the first sos_descend call when N > 8128.
  * ------------------------------------------------------------------------ */
 int sos_plan_create(const sos_index *idx, int64_t r, sos_plan **out);
 int sos_plan_destroy(sos_plan *plan);
@@ -178,7 +178,7 @@ int sos_step(sos_plan *plan, float *V_dev, const float *p_dev, double *loss_dev,
  * sos_step to the slice precision (~1e-7 relative), not bit for bit.  V_dev must
  * not be modified by anyone else during the call (it is asynchronous on
  * `stream`).  Honours sos_opt_set_lr / sos_opt_set_stop settings.  For long K
- * (N >= 8192 monomials) the update also writes the next step's V^T slices,
+ * (N > 8128 monomials) the update also writes the next step's V^T slices,
  * into a second V^T slice buffer (3 * r' * N' bytes, r' = r rounded up to 160,
  * N' = N rounded up to 64) the plan allocates on the first call. */
 int sos_descend(sos_plan *plan, float *V_dev, const float *p_dev, int64_t steps, double *losses_dev,

@@ -302,6 +302,32 @@ def test_full_size_backward_sampled(sos, big, nonneg):
     assert err <= REL_TOL
 
 
+def test_full_size_descend_step_sampled(sos, big):
+    """One sos_descend step (the launch configuration bench.py times: forward,
+    residual, R slices, backward with the fused Adam update) at full size, on
+    sampled rows against the oracle.  p = coef(V0) - res0 makes the residual a
+    known probe, so the oracle needs only gradient rows; Adam's first step is
+    V1 = V0 - lr g / (|g| + eps)."""
+    c, ix, plan, V = big
+    o = oracle(c.n, c.d)
+    Vd = torch.from_numpy(V).cuda()
+    coef = plan.forward(Vd).cpu().numpy().astype(np.float64)
+    res0 = si.residual_probe(o.M, seed=21)
+    p = (coef - res0).astype(np.float32)
+    res_eff = coef - p.astype(np.float64)  # what the GPU's residual sees, up to forward rounding
+    lr = 1e-3
+    plan.opt_init("adam", lr)
+    V1 = Vd.clone()
+    plan.descend(V1, torch.from_numpy(p).cuda(), 1)
+    rows = np.array([0, 7, o.N // 2, o.N - 1], dtype=np.int64)
+    g = o.grad_rows(V, res_eff, rows)
+    want = -lr * g / (np.abs(g) + 1e-8)
+    got = V1[torch.from_numpy(rows).cuda()].cpu().numpy().astype(np.float64) - V[rows]
+    err = rel_l2(got, want)
+    print(f"{c.name} descend step sampled rel err {err:.2e}")
+    assert err <= 1e-4
+
+
 def test_config3_target_with_eps_term(sos):
     """Config 3's target p = coef(W W^T) + eps (sum x_i^2)^6: the eps term is
     added on the exponent table the index exports; check it on sampled

@@ -60,7 +60,8 @@ int sos_version(void);
  * rank(alpha_i + alpha_j) in the degree-2d basis for every ordered pair (i,j),
  * computed by the combinatorial number system.  Synchronous.
  * Limits: 1 <= n, 1 <= d <= 32, n + 2d <= 255, M < 2^32 - 1, N <= 65536.
- * Device memory: about 4*Np^2 bytes (Np = N rounded up to 256). */
+ * Device memory: about 2*Np^2 bytes (Np = N rounded up to 256): the pair-rank
+ * table is stored for one triangle of 64 x 64 blocks (it is symmetric). */
 int sos_build_index(int n, int d, sos_index **out);
 int sos_index_destroy(sos_index *idx);
 

@@ -117,7 +117,7 @@ int sos_build_index(int n, int d, sos_index** out) {
         }
     if ((rc = dalloc(&ix.d_binom, hb.size() * 4)) || (rc = dalloc(&ix.d_ms, (size_t)ix.N * d)) ||
         (rc = dalloc(&ix.d_alpha, (size_t)ix.N * n)) ||
-        (rc = dalloc(&ix.d_pt, (size_t)ix.Np * ix.Np * 4))) {
+        (rc = dalloc(&ix.d_pt, (size_t)pt_entries(ix.Np) * 4))) {
         sos_index_destroy(h);
         return rc;
     }

@@ -481,8 +481,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     for (int ch = 0; ch < kEpiCols / 16; ++ch) {
                         const int64_t c0 = cbase + ch * 16;
                         if (ch * 16 >= ncol || c0 >= args.N) break;
-                        const uint4* prow = reinterpret_cast<const uint4*>(
-                            args.pt + ((c0 / kPtW) * args.Np + i) * kPtW + (c0 % kPtW));
+                        // PT holds blocks i/64 <= j/64 only; a later row block means j < i
+                        // for all 16 columns (weight 0), and the diagonal tile's columns grow
+                        if ((i >> 6) > (c0 >> 6)) continue;
+                        const uint4* prow = reinterpret_cast<const uint4*>(args.pt + pt_entry(i, c0));
                         const uint4* pu = reinterpret_cast<const uint4*>(args.umaxB + c0);
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {

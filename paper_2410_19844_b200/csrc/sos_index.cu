@@ -71,20 +71,23 @@ __device__ __forceinline__ uint32_t pair_rank(const uint8_t* mi, const uint8_t* 
     return rank;
 }
 
-// PT in [jb][i][64] order (jb = j / 64); one thread per entry
+// PT, one block triangle (pt_entry in sos_internal.cuh); one thread per entry
 __global__ void k_pair_table(int64_t N, int64_t Np, int d, const uint32_t* __restrict__ g_binom, int nb,
                              const uint8_t* __restrict__ ms, uint32_t* __restrict__ pt) {
     extern __shared__ uint32_t s_binom[];
     const int bstride = 2 * d + 1;
     for (int t = threadIdx.x; t < nb * bstride; t += blockDim.x) s_binom[t] = g_binom[t];
     __syncthreads();
-    const int64_t total = Np * Np;
+    const int64_t total = pt_entries(Np);
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t jb = t / (Np * kPtW);
-        int64_t rem = t - jb * Np * kPtW;
-        int64_t i = rem / kPtW;
-        int64_t j = jb * kPtW + rem % kPtW;
+        // row r of the layout = 64 J (J+1) / 2 + i: block column J, then row i < 64 (J+1)
+        const int64_t r = t >> 6, q = r >> 6;  // q: row in units of 64-row groups
+        int64_t jb = (int64_t)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
+        while (jb * (jb + 1) / 2 > q) --jb;
+        while ((jb + 1) * (jb + 2) / 2 <= q) ++jb;
+        const int64_t i = r - jb * (jb + 1) / 2 * 64;
+        const int64_t j = jb * kPtW + (t & 63);
         uint32_t out = kInvalidRank;
         if (i < N && j < N) {
             uint8_t mi[kMaxDeg2 / 2], mj[kMaxDeg2 / 2];
@@ -104,7 +107,7 @@ __global__ void k_pair_lookup(const uint32_t* __restrict__ pt, int64_t N, int64_
     if (t >= cnt) return;
     int64_t i = I[t], j = J[t];
     uint32_t v = kInvalidRank;
-    if (i >= 0 && j >= 0 && i < N && j < N) v = pt[((j / kPtW) * Np + i) * kPtW + (j % kPtW)];
+    if (i >= 0 && j >= 0 && i < N && j < N) v = pt[pt_entry_sym(i, j)];
     out[t] = v;
 }
 

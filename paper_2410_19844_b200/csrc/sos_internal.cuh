@@ -100,6 +100,22 @@ __device__ __forceinline__ bool descent_stopped(const Scalars* sc, const DevOpt*
     return use_stop && descent_stopped(sc, opt->stop_tol);
 }
 
+// Pair-rank table layout: PT(i, j) = rank(alpha_i + alpha_j) = PT(j, i), stored
+// only for 64-blocks I = i / 64 <= J = j / 64.  Block column J holds rows
+// i < 64 (J + 1), 64 ranks (j % 64) per row: entry ((64 J (J+1) / 2 + i) 64 + j % 64).
+// A 64 x 64 block (I <= J) is contiguous; a row i of block column J is 256 bytes.
+__host__ __device__ inline int64_t pt_entry(int64_t i, int64_t j) {  // needs i / 64 <= j / 64
+    const int64_t J = j >> 6;
+    return ((J * (J + 1) / 2) * 64 + i) * 64 + (j & 63);
+}
+__host__ __device__ inline int64_t pt_entry_sym(int64_t i, int64_t j) {
+    return (i >> 6) <= (j >> 6) ? pt_entry(i, j) : pt_entry(j, i);
+}
+__host__ __device__ inline int64_t pt_entries(int64_t Np) {
+    const int64_t nb = Np / 64;
+    return nb * (nb + 1) / 2 * 64 * 64;
+}
+
 struct Index {
     int n, d;
     int64_t N, M, Np;
@@ -107,7 +123,7 @@ struct Index {
     uint32_t* d_binom;         // [nb][2d+1] C(x,k), x < nb, k <= 2d   (device)
     uint8_t* d_ms;             // [N][d] sorted variable indices of alpha_i
     uint8_t* d_alpha;          // [N][n] exponents of alpha_i
-    uint32_t* d_pt;            // pair-rank table PT (Np*Np)
+    uint32_t* d_pt;            // pair-rank table PT, one block triangle (pt_entries(Np))
 };
 
 // One CTA-pair output tile: rows [256a, 256a + 256) x columns [c0, c0 + nb).

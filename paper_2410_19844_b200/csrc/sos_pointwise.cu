@@ -165,64 +165,57 @@ __global__ void k_residual(const float* __restrict__ coef, const float* __restri
 }
 
 // ---------------------------------------------------------------- R maxima --
-// rrow[i] = max_j |res[rank(alpha_i + alpha_j)]|: one warp per row; per step
-// the two half-warps read the 256-byte PT rows (jb, i) and (jb+1, i).
+// rrow[i] = max_j |res[rank(alpha_i + alpha_j)]| by one pass over the stored
+// block triangle of PT: a CTA gathers one 64 x 64 block {I <= J} of |R| into
+// shared memory and folds it into the maxima of the rows of I (across the
+// block's columns) and of the rows of J (across its rows: R is symmetric) with
+// atomicMax on float bits (rrow zeroed before).  Used when N^2 lookups are
+// cheaper than the lattice DP (small problems, many variables).
 __global__ void __launch_bounds__(256) k_rmax(const uint32_t* __restrict__ pt, const float* __restrict__ res,
-                                              int64_t Np, unsigned* __restrict__ rrow, const Scalars* sc,
+                                              int64_t nkb, unsigned* __restrict__ rrow, const Scalars* sc,
                                               const DevOpt* opt, int use_stop) {
     if (descent_stopped(sc, opt, use_stop)) return;
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const int64_t njb = Np / kPtW;
-    for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < Np; i += warps) {
-        float m = 0.f;
-        for (int64_t jb = lane >> 4; jb < njb; jb += 2) {
-            const uint4 k = __ldg(reinterpret_cast<const uint4*>(pt + (jb * Np + i) * kPtW) + (lane & 15));
-            const uint32_t kk[4] = {k.x, k.y, k.z, k.w};
+    __shared__ float tile[kPtW][kPtW + 1];
+    const int t = threadIdx.x;
+    const int64_t npairs = nkb * (nkb + 1) / 2;
+    for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+        int64_t J = (int64_t)((sqrt(8.0 * (double)pr + 1.0) - 1.0) * 0.5);
+        while (J * (J + 1) / 2 > pr) --J;
+        while ((J + 1) * (J + 2) / 2 <= pr) ++J;
+        const int64_t I = pr - J * (J + 1) / 2;
+        const uint32_t* p0 = pt + pt_entry(I * kPtW, J * kPtW);
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (kk[e] != kInvalidRank) m = fmaxf(m, fabsf(__ldg(res + kk[e])));
+        for (int u = 0; u < 4; ++u) {
+            const int e = (u * 256 + t) * 4;
+            const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + e));
+            float* d = &tile[e >> 6][e & 63];
+            d[0] = k.x != kInvalidRank ? fabsf(__ldg(res + k.x)) : 0.f;
+            d[1] = k.y != kInvalidRank ? fabsf(__ldg(res + k.y)) : 0.f;
+            d[2] = k.z != kInvalidRank ? fabsf(__ldg(res + k.z)) : 0.f;
+            d[3] = k.w != kInvalidRank ? fabsf(__ldg(res + k.w)) : 0.f;
         }
-        m = warp_max(m);
-        if (lane == 0) rrow[i] = __float_as_uint(m);
+        __syncthreads();
+        // thread t: row (t & 63) of the block if t < 64 ... four threads per line
+        const int line = t >> 2, part = t & 3;
+        float mr = 0.f, mc = 0.f;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            mr = fmaxf(mr, tile[line][part * 16 + e]);   // row `line` of I
+            mc = fmaxf(mc, tile[part * 16 + e][line]);   // column `line` = row of J
+        }
+        mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 1));
+        mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 2));
+        mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, 1));
+        mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, 2));
+        if (part == 0) {
+            if (mr > 0.f) atomicMax(rrow + I * kPtW + line, __float_as_uint(mr));
+            if (I != J && mc > 0.f) atomicMax(rrow + J * kPtW + line, __float_as_uint(mc));
+        }
+        __syncthreads();
     }
 }
 
 // --------------------------------------------------------------- pack RQ ----
-// Row maxima known (rrow): a warp packs 8 rows x one 64-wide K-block.  Lanes
-// gather consecutive j (for a fixed row, consecutive j give nearby ranks in
-// colex order, so a warp's 32 gathers touch few 32-byte sectors of res) into a
-// per-warp shared-memory tile; then lane (row r, chunk c) slices 16 values and
-// the 32 lanes write 8 consecutive 64-byte Q-rows per slice.
-__global__ void __launch_bounds__(256) k_pack_rq(const uint32_t* __restrict__ pt, const float* __restrict__ res,
-                                                 int64_t Np, int64_t nkb, const unsigned* __restrict__ rrow,
-                                                 uint8_t* __restrict__ RQ, const Scalars* sc, const DevOpt* opt,
-                                                 int use_stop) {
-    if (descent_stopped(sc, opt, use_stop)) return;
-    __shared__ float tile[8][8][kPtW + 4];  // [warp][row][j], padded
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t groups = Np / 8;
-    const int64_t tasks = nkb * groups;  // (jb, 8-row group)
-    for (int64_t task = blockIdx.x * 8 + w; task < tasks; task += (int64_t)gridDim.x * 8) {
-        const int64_t jb = task / groups, i0 = (task - jb * groups) * 8;
-        const uint32_t* p0 = pt + (jb * Np + i0) * kPtW;  // 8 rows x 64 ranks, contiguous
-        uint32_t k[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) k[u] = __ldg(p0 + u * 32 + lane);  // row u/2, column (u%2)*32 + lane
-#pragma unroll
-        for (int u = 0; u < 16; ++u) tile[w][u >> 1][(u & 1) * 32 + lane] = k[u] != kInvalidRank ? __ldg(res + k[u]) : 0.f;
-        __syncwarp();
-        const int r = lane >> 2, c = lane & 3;
-        float x[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) x[e] = tile[w][r][c * 16 + e];
-        uint4 q[3];
-        slice16(x, slice_scale(__ldg(rrow + i0 + r)), q);
-        store_q16(RQ, jb, i0 + r, c, nkb, Np, q);
-        __syncwarp();
-    }
-}
-
 // R is symmetric (R_ij = res[rank(alpha_i + alpha_j)] = R_ji): one 64 x 64 block of
 // PT is read per unordered block pair {I <= J} and both RQ blocks -- rows of I at
 // K-block J and rows of J at K-block I (the transposed tile) -- are written from
@@ -242,7 +235,7 @@ __global__ void __launch_bounds__(256, 6) k_pack_rq_sym(const uint32_t* __restri
         while (J * (J + 1) / 2 > pr) --J;
         while ((J + 1) * (J + 2) / 2 <= pr) ++J;
         const int64_t I = pr - J * (J + 1) / 2;
-        const uint32_t* p0 = pt + (J * Np + I * kPtW) * kPtW;  // 64 rows x 64 ranks, contiguous
+        const uint32_t* p0 = pt + pt_entry(I * kPtW, J * kPtW);  // 64 rows x 64 ranks, contiguous
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int e = (u * 256 + t) * 4;
@@ -306,8 +299,10 @@ void launch_residual(Plan& P, const float* coef, const float* p, float* res, cud
 
 void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     LaunchScope ls(P, KK_ABSMAX_R, st);
-    k_rmax<<<grid_for(P, P.idx->Np * 32, 256), 256, 0, st>>>(P.idx->d_pt, res, P.idx->Np, P.d_rrow, P.d_scal,
-                                                             P.d_opt, use_stop);
+    cudaMemsetAsync(P.d_rrow, 0, (size_t)P.idx->Np * sizeof(unsigned), st);
+    const int64_t nkb = P.idx->Np / kPtW, npairs = nkb * (nkb + 1) / 2;
+    const unsigned blocks = (unsigned)std::min<int64_t>(npairs, (int64_t)P.num_sms * 8);
+    k_rmax<<<blocks, 256, 0, st>>>(P.idx->d_pt, res, nkb, P.d_rrow, P.d_scal, P.d_opt, use_stop);
 }
 
 // one thread: t += 1 (Adam bias correction of this step), and in sos_descend
@@ -507,16 +502,10 @@ void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop) {
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     const int64_t Np = P.idx->Np;
     LaunchScope ls(P, KK_PACK_R, st);
-    static const bool sym = !getenv("SOS_RPACK_SYM") || atoi(getenv("SOS_RPACK_SYM"));
-    if (sym) {
-        const int64_t npairs = P.nkbN * (P.nkbN + 1) / 2;
-        const unsigned blocks = (unsigned)std::min<int64_t>(npairs, (int64_t)P.num_sms * 8);
-        k_pack_rq_sym<<<blocks, 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow, P.d_rq, P.d_scal, P.d_opt,
-                                              use_stop);
-        return;
-    }
-    k_pack_rq<<<grid_for(P, P.nkbN * (Np / 8) * 32, 256), 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow, P.d_rq,
-                                                                       P.d_scal, P.d_opt, use_stop);
+    const int64_t npairs = P.nkbN * (P.nkbN + 1) / 2;
+    const unsigned blocks = (unsigned)std::min<int64_t>(npairs, (int64_t)P.num_sms * 8);
+    k_pack_rq_sym<<<blocks, 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow, P.d_rq, P.d_scal, P.d_opt,
+                                          use_stop);
 }
 
 

@@ -209,7 +209,7 @@ def config_block(cfg, args, world):
         "optimizer": args.opt, "lr": args.lr,
         "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
         "l2": "inputs larger than L2 every step (V 1.66 GB fp32, int8 slices of R 1.26 GB and of V / V^T "
-              "1.25 GB each, pair-rank table 1.68 GB; L2 is 126 MB), no flush needed",
+              "1.25 GB each, pair-rank table 0.84 GB; L2 is 126 MB), no flush needed",
     }
 
 

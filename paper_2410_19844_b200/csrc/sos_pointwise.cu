@@ -476,14 +476,14 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, uns
 // then one streaming pass gathers and slices R.
 // R row maxima: the lattice DP costs ~d launches plus sum_D C(n+D-1, D) * n
 // lookups; the direct gather over PT (k_rmax) one launch plus N^2 lookups.
-// Small problems and many variables favour the direct pass (config 2: 60 -> 15
-// us; N = 5050 quartic: 110 -> 44 us); configs 3 and 4 the DP (0.18 / 0.33 ms vs
-// 0.22 / ~0.6 ms).  Rates fitted to those measurements.
+// Small problems and many variables favour the direct pass (config 2: 60 -> 14
+// us; N = 5050 quartic: 100 -> 32 us); config 4 the DP (0.33 vs 0.46 ms); config
+// 3 is even (0.178 / 0.175 ms).  Rates fitted to those measurements.
 static bool rmax_direct_is_cheaper(const Index& ix) {
     double lookups = 0;
     for (int D = ix.d; D <= 2 * ix.d - 1; ++D) lookups += (double)rmax_level_count(ix.n, D) * ix.n;
     const double dp_us = 12.0 * ix.d + lookups / 2e5;
-    const double direct_us = 10.0 + (double)ix.N * ix.N / 7e5;
+    const double direct_us = 6.0 + (double)ix.N * ix.N / 9e5;  // per stored block pair (k_rmax)
     return direct_us < dp_us;
 }
 

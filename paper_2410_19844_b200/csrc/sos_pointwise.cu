@@ -475,7 +475,8 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, uns
 // few tens of millions of lookups instead of N^2 gathers) or the direct pass,
 // then one streaming pass gathers and slices R.
 // R row maxima: the lattice DP costs ~d launches plus sum_D C(n+D-1, D) * n
-// lookups; the direct gather over PT (k_rmax) one launch plus N^2 lookups.
+// lookups; the direct pass over the stored PT triangle (k_rmax) a memset, one
+// launch and N^2 / 2 lookups.
 // Small problems and many variables favour the direct pass (config 2: 60 -> 14
 // us; N = 5050 quartic: 100 -> 32 us); config 4 the DP (0.33 vs 0.46 ms); config
 // 3 is even (0.178 / 0.175 ms).  Rates fitted to those measurements.

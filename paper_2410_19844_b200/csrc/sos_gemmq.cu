@@ -619,7 +619,8 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
     a.kserp = kserp;
     static unsigned long long* dbg = nullptr;
     if (env_int("SOS_GEMM_STATS", 0)) {
-        if (!dbg) cudaMalloc(&dbg, 8 * sizeof(unsigned long long));
+        if (!dbg && cudaMalloc(&dbg, 8 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(dbg, 0, 8 * sizeof(unsigned long long));
         a.dbg = dbg + (kMode == kModeFwd ? 0 : 0);
     }
     static bool configured = false;

@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -58,6 +59,7 @@ def lib():
         L.or_rank2d.argtypes = [_vp, _vp, _i64, _vp]
         L.or_pair_ranks.argtypes = [_vp, _vp, _i64, _vp]
         L.or_forward.argtypes = [_vp, _vp, _i64, _vp]
+        L.or_forward_rows.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp]
         L.or_coef_sample.argtypes = [_vp, _vp, _i64, _vp, _i64, _vp]
         L.or_grad_rows.argtypes = [_vp, _vp, _i64, _vp, _vp, _i64, _vp]
         L.or_loss_grad.restype = ctypes.c_double
@@ -81,6 +83,21 @@ def _f64(a) -> np.ndarray:
 def basis_count(n: int, D: int) -> int:
     """Number of degree-D monomials in n variables, counted by enumeration."""
     return int(lib().or_basis_count(n, D))
+
+
+def host_threads() -> int:
+    """Host cores this process may run on (the threaded helpers' default)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def _row_blocks(N: int, threads: int, block: int = 16):
+    """Static, deterministic split of rows 0..N-1 over `threads` workers:
+    worker t takes row blocks t, t + threads, ... (balances the pair loop)."""
+    starts = list(range(0, N, block))
+    return [[(s, min(N, s + block)) for s in starts[t::threads]] for t in range(threads)]
 
 
 class OracleIndex:
@@ -130,6 +147,79 @@ class OracleIndex:
         out = np.empty(self.M, dtype=np.float64)
         lib().or_forward(self._h, _ptr(V), V.shape[1], _ptr(out))
         return out
+
+    def forward_threaded(self, V, threads: int | None = None) -> np.ndarray:
+        """forward() with the pair loop's rows split over host threads
+        (or_forward_rows per row range; the ctypes calls release the GIL).
+        Equal to forward() up to the order of the fp64 additions."""
+        V = _f64(V)
+        assert V.shape[0] == self.N
+        T = max(1, min(threads or host_threads(), self.N))
+        parts = _row_blocks(self.N, T)
+
+        def work(blocks):
+            acc = np.zeros(self.M, dtype=np.float64)
+            for i0, i1 in blocks:
+                lib().or_forward_rows(self._h, _ptr(V), V.shape[1], i0, i1, _ptr(acc))
+            return acc
+
+        with ThreadPoolExecutor(T) as ex:
+            accs = list(ex.map(work, parts))
+        out = accs[0]
+        for a in accs[1:]:
+            out += a
+        return out
+
+    def grad_rows_threaded(self, V, res, rows, threads: int | None = None) -> np.ndarray:
+        """grad_rows() with the rows split over host threads (same C routine per row)."""
+        V = _f64(V)
+        res = _f64(res)
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        out = np.empty((rows.shape[0], V.shape[1]), dtype=np.float64)
+        T = max(1, min(threads or host_threads(), rows.shape[0]))
+        chunks = [c for c in np.array_split(np.arange(rows.shape[0]), T) if c.size]
+
+        def work(idx):
+            sub = np.ascontiguousarray(rows[idx])
+            g = np.empty((sub.shape[0], V.shape[1]), dtype=np.float64)
+            lib().or_grad_rows(self._h, _ptr(V), V.shape[1], _ptr(res), _ptr(sub), sub.shape[0], _ptr(g))
+            out[idx] = g
+
+        with ThreadPoolExecutor(T) as ex:
+            list(ex.map(work, chunks))
+        return out
+
+    def loss_grad_threaded(self, V, p, want_grad: bool = True, threads: int | None = None):
+        """loss_grad() on host threads: same definitions (Eq. 2 and its gradient 4RV)."""
+        V = _f64(V)
+        p = _f64(p)
+        coef = self.forward_threaded(V, threads)
+        res = coef - p
+        loss = float(np.sum(res * res))
+        grad = self.grad_rows_threaded(V, res, np.arange(self.N), threads) if want_grad else None
+        return loss, grad, coef, res
+
+    def descent_threaded(self, V0, p, kind: str, steps: int, lr: float, b1: float = 0.9, b2: float = 0.999,
+                         eps: float = 1e-8, threads: int | None = None):
+        """The loop of or_descent (losses[t] = L(V_t) before update t, then
+        GD or Adam with step index t+1), each loss/gradient evaluated on host
+        threads and each update by the oracle's own or_gd_update /
+        or_adam_update.  Returns (V_steps, losses): V_steps[t] = V_t."""
+        V = _f64(V0).copy()
+        p = _f64(p)
+        m = np.zeros_like(V)
+        v = np.zeros_like(V)
+        Vs, losses = [V.copy()], []
+        for t in range(steps):
+            loss, g, _, _ = self.loss_grad_threaded(V, p, True, threads)
+            losses.append(loss)
+            if kind == "gd":
+                lib().or_gd_update(_ptr(V), _ptr(g), V.size, lr)
+            else:
+                lib().or_adam_update(_ptr(V), _ptr(g), _ptr(m), _ptr(v), V.size, lr, b1, b2, eps, t + 1)
+            Vs.append(V.copy())
+        losses.append(self.loss_grad_threaded(V, p, False, threads)[0])
+        return Vs, np.array(losses)
 
     def coef_sample(self, V, betas) -> np.ndarray:
         V = _f64(V)

@@ -214,6 +214,24 @@ void or_forward(void *hv, const double *V, int64_t r, double *coef) {
     }
 }
 
+/* The same pair loop restricted to rows i0 <= i < i1 (all j), ADDED into coef
+ * (the caller zeroes it).  Summing the partial vectors of a partition of the
+ * rows gives or_forward up to the order of the additions, so independent row
+ * ranges can run on separate host threads (the loop body is unchanged). */
+void or_forward_rows(void *hv, const double *V, int64_t r, int64_t i0, int64_t i1, double *coef) {
+    or_index_t *h = (or_index_t *)hv;
+    int n = h->n;
+    int64_t N = h->a.count;
+    uint8_t s[256];
+    for (int64_t i = i0; i < i1 && i < N; ++i) {
+        for (int64_t j = 0; j < N; ++j) {
+            for (int v = 0; v < n; ++v) s[v] = (uint8_t)(h->a.ex[i * n + v] + h->a.ex[j * n + v]);
+            int64_t q = basis_rank_ex(&h->b, s);
+            coef[q] += dot_row(V, r, i, j);
+        }
+    }
+}
+
 /* Selected coefficients only: coef_beta = sum over ordered pairs (i,j) with
  * alpha_i + alpha_j = beta of <v_i, v_j>  (same definition, per beta). */
 void or_coef_sample(void *hv, const double *V, int64_t r, const int64_t *betas, int64_t k, double *out) {

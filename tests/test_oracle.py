@@ -233,12 +233,86 @@ def test_adam_first_step_and_zero_grad():
     np.testing.assert_array_equal(V2, V)
 
 
+def test_adam_hand_computed_three_steps():
+    """Adam (Kingma & Ba, Alg. 1) worked by hand for three steps
+    with distinct beta1 = 1/2, beta2 = 3/4, lr = 1, eps = 0 and gradients
+    1, 3, -2 (all moments exact binary fractions):
+        t=1: m = 1/2,    v = 1/4,        m^ = 1,    v^ = 1      -> step 1
+        t=2: m = 7/4,    v = 39/16,      m^ = 7/3,  v^ = 39/7   -> step (7/3)/sqrt(39/7)
+        t=3: m = -1/8,   v = 181/64,     m^ = -1/7, v^ = 181/37 -> step (-1/7)/sqrt(181/37)
+    A beta1 <-> beta2 swap, a missing bias correction or a bias correction
+    with the wrong t changes every step after the first."""
+    x, m, v = np.array([5.0]), np.zeros(1), np.zeros(1)
+    want_m = [0.5, 7 / 4, -1 / 8]
+    want_v = [0.25, 39 / 16, 181 / 64]
+    want_x = [5.0 - 1.0]
+    want_x.append(want_x[-1] - (7 / 3) / math.sqrt(39 / 7))
+    want_x.append(want_x[-1] - (-1 / 7) / math.sqrt(181 / 37))
+    for t, g in enumerate([1.0, 3.0, -2.0], start=1):
+        x, m, v = adam_update(x, np.array([g]), m, v, 1.0, 0.5, 0.75, 0.0, t)
+        assert m[0] == want_m[t - 1] and v[0] == want_v[t - 1]
+        assert abs(x[0] - want_x[t - 1]) <= 1e-15 * abs(want_x[t - 1])
+
+
+def test_adam_matches_torch_optim_adam():
+    """The oracle's Adam over 8 steps against an independent implementation,
+    torch.optim.Adam on fp64 CPU tensors (foreach/fused off): parameters and
+    both moments after every step, non-default betas and eps, gradients that
+    change sign and scale from step to step."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(17)
+    V = rng.standard_normal((7, 5))
+    lr, b1, b2, eps = 3e-2, 0.8, 0.95, 1e-6
+    P = torch.tensor(V.copy(), dtype=torch.float64, requires_grad=True)
+    opt = torch.optim.Adam([P], lr=lr, betas=(b1, b2), eps=eps, foreach=False, fused=False)
+    m, v = np.zeros_like(V), np.zeros_like(V)
+    for t in range(1, 9):
+        g = rng.standard_normal(V.shape) * (10.0 ** rng.uniform(-3, 2)) * (-1) ** t
+        V, m, v = adam_update(V, g, m, v, lr, b1, b2, eps, t)
+        P.grad = torch.tensor(g, dtype=torch.float64)
+        opt.step()
+        st = opt.state[P]
+        np.testing.assert_allclose(m, st["exp_avg"].numpy(), rtol=1e-13, atol=0)
+        np.testing.assert_allclose(v, st["exp_avg_sq"].numpy(), rtol=1e-13, atol=0)
+        np.testing.assert_allclose(V, P.detach().numpy(), rtol=1e-13, atol=1e-15)
+
+
 def test_adam_scalar_quadratic():
     """100 Adam steps on (x-3)^2 from x=0 with lr=0.1 end within 0.5 of 3."""
     x, m, v = np.zeros(1), np.zeros(1), np.zeros(1)
     for t in range(1, 101):
         x, m, v = adam_update(x, 2 * (x - 3), m, v, 0.1, 0.9, 0.999, 1e-8, t)
     assert abs(x[0] - 3) < 0.5
+
+
+# ----------------------------------------------- threaded oracle helpers ----
+
+def test_forward_threaded_matches_forward():
+    """forward_threaded (row ranges of the same pair loop on host threads) is
+    forward() up to fp64 addition order; exact on integer V."""
+    h = OracleIndex(4, 3)
+    V = si.gaussian(h.N, 9, 1.0, seed=4, stream=98).astype(np.float64)
+    np.testing.assert_allclose(h.forward_threaded(V, threads=3), h.forward(V), rtol=1e-13, atol=1e-13)
+    Vi = np.random.default_rng(3).integers(-3, 4, size=(h.N, 4)).astype(np.float64)
+    np.testing.assert_array_equal(h.forward_threaded(Vi, threads=5), h.forward(Vi))
+
+
+def test_grad_and_descent_threaded_match_c():
+    """grad_rows_threaded == grad_rows; descent_threaded (Python loop over the
+    threaded loss/gradient and the oracle's update routines) == or_descent."""
+    h = OracleIndex(3, 3)
+    rng = np.random.default_rng(8)
+    V = rng.standard_normal((h.N, 4)) * 0.3
+    p = h.forward(rng.standard_normal((h.N, 2)) * 0.3)
+    res = rng.standard_normal(h.M)
+    rows = np.arange(h.N)[::-1]
+    np.testing.assert_array_equal(h.grad_rows_threaded(V, res, rows, threads=3), h.grad_rows(V, res, rows))
+    for kind, lr in (("gd", 1e-2), ("adam", 1e-2)):
+        Vc, Lc = h.descent(V, p, kind, 5, lr, b1=0.8, b2=0.9, eps=1e-7)
+        Vs, Lt = h.descent_threaded(V, p, kind, 5, lr, b1=0.8, b2=0.9, eps=1e-7, threads=2)
+        assert len(Vs) == 6
+        np.testing.assert_allclose(Vs[-1], Vc, rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(Lt, Lc, rtol=1e-12)
 
 
 def test_descent_config0_reaches_1e8():

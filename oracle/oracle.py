@@ -200,11 +200,14 @@ class OracleIndex:
         return loss, grad, coef, res
 
     def descent_threaded(self, V0, p, kind: str, steps: int, lr: float, b1: float = 0.9, b2: float = 0.999,
-                         eps: float = 1e-8, threads: int | None = None):
+                         eps: float = 1e-8, threads: int | None = None, final_loss: bool = True,
+                         grads_out: list | None = None):
         """The loop of or_descent (losses[t] = L(V_t) before update t, then
         GD or Adam with step index t+1), each loss/gradient evaluated on host
         threads and each update by the oracle's own or_gd_update /
-        or_adam_update.  Returns (V_steps, losses): V_steps[t] = V_t."""
+        or_adam_update.  Returns (V_steps, losses): V_steps[t] = V_t; the
+        last loss L(V_steps) only with final_loss.  grads_out (a list), if
+        given, receives each step's gradient."""
         V = _f64(V0).copy()
         p = _f64(p)
         m = np.zeros_like(V)
@@ -213,12 +216,15 @@ class OracleIndex:
         for t in range(steps):
             loss, g, _, _ = self.loss_grad_threaded(V, p, True, threads)
             losses.append(loss)
+            if grads_out is not None:
+                grads_out.append(g.copy())
             if kind == "gd":
                 lib().or_gd_update(_ptr(V), _ptr(g), V.size, lr)
             else:
                 lib().or_adam_update(_ptr(V), _ptr(g), _ptr(m), _ptr(v), V.size, lr, b1, b2, eps, t + 1)
             Vs.append(V.copy())
-        losses.append(self.loss_grad_threaded(V, p, False, threads)[0])
+        if final_loss:
+            losses.append(self.loss_grad_threaded(V, p, False, threads)[0])
         return Vs, np.array(losses)
 
     def coef_sample(self, V, betas) -> np.ndarray:

@@ -1,0 +1,140 @@
+"""GPU parity of the multi-step descent on sos_descend's default long-K path
+and of the backward's segmented s32 accumulation, against the fp64 oracle
+(its loss / gradient evaluated on host threads, oracle.OracleIndex.*_threaded).
+
+* N = 8855 (n=20, 2d=8; 139 K-blocks of 64): the backward applies the update
+  in its epilogue warps and also writes the next step's V and V^T slices
+  ("sos_descend: the update writes the next step's operands");
+  4 steps = plain step 0, graph-replayed steps 1-2, plain step 3.
+* N = 53130 (n=21, 2d=10): K = N > 43648 = the exact-s32 bound, so every
+  backward tile drains TMEM per K segment (sos_internal.cuh kSegKBMax).
+"""
+import numpy as np
+import pytest
+
+import seeded_inputs as si
+from oracle import OracleIndex
+from strata import stratified_rows
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(got, want):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    den = np.linalg.norm(want)
+    return np.linalg.norm(got - want) / (den if den > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def sos():
+    import paper_2410_19844_b200 as m
+    m.load()
+    return m
+
+
+@pytest.fixture(scope="module")
+def long_k(sos):
+    n, d, r = 20, 4, 200   # r = 160 + 40: a full and a narrow column tile
+    o = OracleIndex(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r)
+    W = si.planted_w(o.N, 32, seed=6)
+    p = o.forward_threaded(W).astype(np.float32)      # planted target, by the oracle
+    V0 = si.v0(o.N, r, seed=7)
+    # Adam first: its recorded first gradient also sets the GD step below
+    g_adam = []
+    Vs_adam, L_adam = o.descent_threaded(V0, p, "adam", 4, 1e-3, final_loss=False, grads_out=g_adam)
+    yield dict(o=o, ix=ix, plan=plan, p=p, V0=V0, adam=(Vs_adam, L_adam, g_adam))
+    plan.close()
+    ix.close()
+
+
+def _gpu_descend(sos, plan, V0, p, kind, lr, steps):
+    plan.opt_init(kind, lr)
+    Vd = torch.from_numpy(V0.copy()).cuda()
+    losses = plan.descend(Vd, torch.from_numpy(p).cuda(), steps).cpu().numpy()
+    return Vd.cpu().numpy().astype(np.float64), losses
+
+
+def test_descend_long_k_adam_4_steps(sos, long_k):
+    """4 Adam steps (lr 1e-3, bench.py's eps 1e-8) through sos_descend vs the
+    oracle's Adam: V_4 - V_0 element-wise (rel. L2 <= 1e-4) and the losses
+    L(V_0..V_3) (rel. <= 1e-5).  Adam's first step is ~lr sign(g_1); the few
+    entries whose oracle g_1 is within 1e-5 rms of 0 may take either sign on
+    the GPU (forward rounding), so they are compared for validity only."""
+    o, plan, p, V0 = long_k["o"], long_k["plan"], long_k["p"], long_k["V0"]
+    Vs, L, g = long_k["adam"]
+    V4, losses = _gpu_descend(sos, plan, V0, p, "adam", 1e-3, 4)
+    dv_o = Vs[4] - V0
+    dv_g = V4 - V0
+    amb = np.abs(g[0]) < 1e-5 * np.sqrt(np.mean(g[0] ** 2))
+    err = rel_l2(dv_g[~amb], dv_o[~amb])
+    lerr = np.abs(losses - L[:4]) / L[:4]
+    print(f"long-K Adam: dV rel err {err:.2e} ({amb.sum()} ambiguous of {amb.size}); loss rel err {lerr.max():.2e}")
+    assert err <= 1e-4
+    assert amb.sum() <= 1e-5 * amb.size
+    assert np.all(np.abs(dv_g[amb] - dv_o[amb]) <= 2 * 4 * 1e-3)
+    assert np.all(lerr <= 1e-5)
+
+
+def test_descend_long_k_gd_4_steps(sos, long_k):
+    """The same with plain GD (every gradient magnitude enters the update): lr
+    sets the first step to 2 % of ||V_0||; V_4 - V_0 and the losses vs the oracle."""
+    o, plan, p, V0 = long_k["o"], long_k["plan"], long_k["p"], long_k["V0"]
+    g1 = long_k["adam"][2][0]  # the gradient at V_0 (same V_0 and p)
+    lr = 0.02 * np.linalg.norm(V0) / np.linalg.norm(g1)
+    Vs, L = o.descent_threaded(V0, p, "gd", 4, lr, final_loss=False)
+    V4, losses = _gpu_descend(sos, plan, V0, p, "gd", lr, 4)
+    err = rel_l2(V4 - V0, Vs[4] - V0)
+    lerr = np.abs(losses - L[:4]) / L[:4]
+    print(f"long-K GD lr={lr:.3g}: dV rel err {err:.2e}; losses {L[:4]} rel err {lerr.max():.2e}")
+    assert L[3] < L[0]
+    assert err <= 1e-4
+    assert np.all(lerr <= 1e-5)
+
+
+def test_backward_segmented_k(sos):
+    """N = 53130 > 43648: the backward's exact s32 accumulators are drained per
+    K segment.  >= 64 stratified gradient rows vs the oracle (random residual,
+    and an all-nonnegative case whose partial sums only grow), sampled
+    coefficients of the forward, and one GD step of sos_descend on sampled rows."""
+    n, d, r = 21, 5, 200
+    o = OracleIndex(n, d)
+    ix = sos.SosIndex(n, d)
+    assert ix.N == o.N == 53130 and ix.N > 43648
+    plan = sos.SosPlan(ix, r)
+    V = si.v0(o.N, r, seed=12)
+    Vd = torch.from_numpy(V).cuda()
+    rows = stratified_rows(o.N)
+    for nonneg in (False, True):
+        res = si.residual_probe(o.M, seed=13)
+        Vx = V
+        if nonneg:
+            res, Vx = np.abs(res), np.abs(V)
+        g = plan.backward(torch.from_numpy(Vx).cuda(), torch.from_numpy(res).cuda())
+        got = g[torch.from_numpy(rows).cuda()].cpu().numpy()
+        want = o.grad_rows_threaded(Vx.astype(np.float64), res, rows)
+        err = rel_l2(got, want)
+        print(f"segmented-K backward (nonneg={nonneg}): {rows.size} rows rel err {err:.2e}")
+        assert err <= 1e-5
+    coef = plan.forward(Vd).cpu().numpy().astype(np.float64)
+    betas = np.concatenate([[0, 1, o.M - 1], np.random.default_rng(14).integers(0, o.M, 40)])
+    assert rel_l2(coef[betas], o.coef_sample(V, betas)) <= 1e-5
+    # one descend step (fused update + next-step slices, segmented backward): GD
+    res0 = si.residual_probe(o.M, seed=15)
+    p = (coef - res0).astype(np.float32)
+    res_eff = res0.astype(np.float64)  # the GPU's residual up to the fp32 rounding of p
+    gw = o.grad_rows_threaded(V.astype(np.float64), res_eff, rows)
+    lr = 0.05 * np.sqrt(np.mean(V[rows].astype(np.float64) ** 2)) / np.sqrt(np.mean(gw ** 2))
+    plan.opt_init("gd", lr)
+    V1 = Vd.clone()
+    plan.descend(V1, torch.from_numpy(p).cuda(), 1)
+    got = V1[torch.from_numpy(rows).cuda()].cpu().numpy().astype(np.float64) - V[rows]
+    err = rel_l2(got, -lr * gw)
+    print(f"segmented-K descend GD step: rel err {err:.2e}")
+    assert err <= 1e-5
+    plan.close()
+    ix.close()

@@ -48,7 +48,7 @@ typedef struct sos_plan sos_plan;   /* per-(index, r) workspaces and optimiser s
 /* Thread-local description of the last error ("" if none). */
 const char *sos_last_error(void);
 
-/* ABI version (increments on incompatible change). */
+/* ABI version (increments on incompatible change; 2: sos_plan_create_ex). */
 int sos_version(void);
 
 /* ------------------------------------------------------------------------
@@ -84,11 +84,38 @@ int sos_index_pair_ranks(const sos_index *idx, const int64_t *i_dev, const int64
 /* ------------------------------------------------------------------------
  * Plan: workspaces for one (index, r).  Device memory ~ 3*Np*(2*r + Np) bytes
  * (int8 slices of V, V^T and R) plus 8*N*r once Adam is enabled, plus 4*N*r
- * (a gradient buffer) when N <= 3008 (short K: the optimiser step then runs as
- * its own kernel after the backward instead of inside it), plus a second V^T
- * slice buffer on the first sos_descend call when N > 8128.
+ * (a gradient buffer) for the split pipeline (default when N <= 3008: short K),
+ * plus a second V^T slice buffer on the first sos_descend call when the update
+ * writes the next step's V^T slices (default when N > 8128).
  * ------------------------------------------------------------------------ */
 int sos_plan_create(const sos_index *idx, int64_t r, sos_plan **out);
+
+/* Implementation choices of a plan.  Every field is -1 (the
+ * library picks by problem size, the default of sos_plan_create) or 0 / 1.
+ * All variants compute the same step; they differ in how it is scheduled and
+ * agree to fp32 rounding (tests/test_gpu_variants.py).  Nothing else -- no
+ * environment variable -- changes what a plan computes.
+ *   split:        1 = "split" step: forward, one cooperative kernel (residual,
+ *                 loss, R maxima, V^T and R slices), backward storing the
+ *                 gradient, one row-block update kernel (4 launches; default
+ *                 for short K, N <= 3008); 0 = the update runs in the
+ *                 backward's epilogue warps.
+ *   vtq_from_update (split = 0, sos_descend): the update also writes the next
+ *                 step's V^T slices (default for N > 8128).
+ *   vtq_in_aux:   the forward's two aux warps write the V^T slices (default
+ *                 when they hide under its MMAs) instead of a separate kernel.
+ *   rmax_direct:  R row maxima by one gather pass over the pair-rank table
+ *                 instead of the monomial-lattice DP (default by a cost model).
+ *   narrow_tiles: tiles narrower than 160 columns where a column block is
+ *                 partly outside the matrix (default 1). */
+typedef struct {
+    int split;
+    int vtq_from_update;
+    int vtq_in_aux;
+    int rmax_direct;
+    int narrow_tiles;
+} sos_plan_opts;
+int sos_plan_create_ex(const sos_index *idx, int64_t r, const sos_plan_opts *opts, sos_plan **out);
 int sos_plan_destroy(sos_plan *plan);
 
 /* Number of kernels this library launched through `plan` so far. */
@@ -104,11 +131,13 @@ int64_t sos_plan_launch_count(const sos_plan *plan);
 #define SOS_KERNEL_PACK_V 1   /* int8 slices of V (and of V^T in sos_backward) */
 #define SOS_KERNEL_GEMM_FWD 2 /* Gram tiles + coefficient scatter (tensor cores) */
 #define SOS_KERNEL_RESIDUAL 3 /* res = coef - p, loss */
-#define SOS_KERNEL_RMAX 4     /* row maxima of R (only when a row exceeds the fused packer) */
-#define SOS_KERNEL_PACK_R 5   /* R gathered through the pair-rank table: row maxima + int8 slices */
+#define SOS_KERNEL_RMAX 4     /* row maxima of R (lattice DP or direct pass) */
+#define SOS_KERNEL_PACK_R 5   /* R gathered through the pair-rank table into int8 slices */
 #define SOS_KERNEL_GEMM_BWD 6 /* 4 R V (tensor cores), in sos_step with the optimiser update */
-#define SOS_KERNEL_UPDATE 7   /* step bookkeeping (Adam t, loss record); the update itself runs inside GEMM_BWD */
-#define SOS_KERNEL_COUNT 8
+#define SOS_KERNEL_UPDATE 7   /* step bookkeeping (Adam t, loss record); the split step's row-block update
+                                 (otherwise the update runs inside GEMM_BWD) */
+#define SOS_KERNEL_MID 8      /* the split step's cooperative kernel: residual, loss, R maxima, V^T and R slices */
+#define SOS_KERNEL_COUNT 9
 int sos_plan_timing(sos_plan *plan, int enable);
 int sos_plan_timing_read(sos_plan *plan, int kernel, double *total_ms, int64_t *launches);
 
@@ -165,8 +194,10 @@ int sos_opt_set_stop(sos_plan *plan, double rel_tol);
  * then V <- V - lr*g (GD) or the bias-corrected Adam update with t += 1:
  *   m <- b1 m + (1-b1) g,  v <- b2 v + (1-b2) g^2,
  *   V <- V - lr (m / (1-b1^t)) / (sqrt(v / (1-b2^t)) + eps).
- * The update runs inside the backward GEMM (the gradient never reaches HBM).
- * With a stopping tolerance set (sos_opt_set_stop) and met, V is left unchanged. */
+ * The update runs inside the backward GEMM (the gradient never reaches HBM), or
+ * for split plans in a row-block kernel after it.  V_dev must be 16-byte
+ * aligned (SOS_ERR_ARG otherwise).  With a stopping tolerance set
+ * (sos_opt_set_stop) and met, V is left unchanged. */
 int sos_step(sos_plan *plan, float *V_dev, const float *p_dev, double *loss_dev, void *stream);
 
 /* `steps` descent steps in one call, in place on V_dev: losses_dev[t] = L(V_t)
@@ -175,7 +206,8 @@ int sos_step(sos_plan *plan, float *V_dev, const float *p_dev, double *loss_dev,
  * also writes the int8 slices and the exact row / column maxima of V_{t+1}
  * (slices scaled by 2x the row maximum of V_t; rows whose new maximum leaves
  * [1/2, 2] of the old one are re-sliced exactly before the next forward), so
- * the per-step maxima and slicing passes over V disappear.  Results agree with
+ * the per-step maxima and slicing passes over V disappear (split plans: exact
+ * new row maxima, no re-slicing).  V_dev must be 16-byte aligned.  Results agree with
  * sos_step to the slice precision (~1e-7 relative), not bit for bit.  V_dev must
  * not be modified by anyone else during the call (it is asynchronous on
  * `stream`).  Honours sos_opt_set_lr / sos_opt_set_stop settings.  For long K

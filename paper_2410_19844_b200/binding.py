@@ -32,6 +32,11 @@ class _OptParams(ctypes.Structure):
                 ("beta2", ctypes.c_float), ("eps", ctypes.c_float)]
 
 
+class _PlanOpts(ctypes.Structure):
+    _fields_ = [("split", ctypes.c_int), ("vtq_from_update", ctypes.c_int), ("vtq_in_aux", ctypes.c_int),
+                ("rmax_direct", ctypes.c_int), ("narrow_tiles", ctypes.c_int)]
+
+
 _lib = None
 
 # name -> argtypes (restype int unless listed in _RESTYPES)
@@ -45,6 +50,7 @@ SIGNATURES = {
     "sos_index_beta": [_vp, _vp, _vp],
     "sos_index_pair_ranks": [_vp, _vp, _vp, _i64, _vp, _vp],
     "sos_plan_create": [_vp, _i64, ctypes.POINTER(_vp)],
+    "sos_plan_create_ex": [_vp, _i64, ctypes.POINTER(_PlanOpts), ctypes.POINTER(_vp)],
     "sos_plan_destroy": [_vp],
     "sos_plan_launch_count": [_vp],
     "sos_plan_timing": [_vp, ctypes.c_int],
@@ -86,9 +92,19 @@ def _stream():
     return _vp(torch.cuda.current_stream().cuda_stream)
 
 
-def _dev_f32(t: torch.Tensor, name: str) -> torch.Tensor:
+def _dev_f32(t: torch.Tensor, name: str, numel: Optional[int] = None) -> torch.Tensor:
     if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
         raise SosError(f"{name} must be a contiguous float32 CUDA tensor")
+    if numel is not None and t.numel() != numel:
+        raise SosError(f"{name} must have {numel} elements, got {t.numel()}")
+    return t
+
+
+def _dev_f64_out(t: torch.Tensor, name: str, min_numel: int) -> torch.Tensor:
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise SosError(f"{name} must be a contiguous float64 CUDA tensor")
+    if t.numel() < min_numel:
+        raise SosError(f"{name} needs at least {min_numel} elements, got {t.numel()}")
     return t
 
 
@@ -127,6 +143,8 @@ class SosIndex:
         return out
 
     def pair_ranks(self, i: torch.Tensor, j: torch.Tensor) -> torch.Tensor:
+        if i.numel() != j.numel():
+            raise SosError(f"i and j must have the same length, got {i.numel()} and {j.numel()}")
         i = i.to(device="cuda", dtype=torch.int64).contiguous()
         j = j.to(device="cuda", dtype=torch.int64).contiguous()
         out = torch.empty(i.numel(), dtype=torch.int32, device="cuda")
@@ -136,13 +154,23 @@ class SosIndex:
 
 
 class SosPlan:
-    """Workspaces for one (index, r); the hot-path calls of the C ABI."""
+    """Workspaces for one (index, r); the hot-path calls of the C ABI.
 
-    def __init__(self, index: SosIndex, r: int):
+    Keyword options (sos_plan_opts: None = the library's choice by size, else
+    True / False): split, vtq_from_update, vtq_in_aux, rmax_direct,
+    narrow_tiles -- implementation variants of the same step."""
+
+    OPTS = ("split", "vtq_from_update", "vtq_in_aux", "rmax_direct", "narrow_tiles")
+
+    def __init__(self, index: SosIndex, r: int, **opts):
+        bad = set(opts) - set(self.OPTS)
+        if bad:
+            raise SosError(f"unknown plan options {sorted(bad)}")
         self.index = index
         self.r = r
         h = _vp()
-        _check(load().sos_plan_create(index._h, r, ctypes.byref(h)))
+        o = _PlanOpts(*[-1 if opts.get(k) is None else int(bool(opts[k])) for k in self.OPTS])
+        _check(load().sos_plan_create_ex(index._h, r, ctypes.byref(o), ctypes.byref(h)))
         self._h = h
 
     def close(self):
@@ -160,7 +188,7 @@ class SosPlan:
     def launch_count(self) -> int:
         return int(load().sos_plan_launch_count(self._h))
 
-    KERNELS = ("vmax", "pack_v", "gemm_fwd", "residual", "rmax", "pack_r", "gemm_bwd", "update")
+    KERNELS = ("vmax", "pack_v", "gemm_fwd", "residual", "rmax", "pack_r", "gemm_bwd", "update", "mid")
 
     def timing(self, enable: bool):
         """Start (clears old records) / stop per-kernel CUDA-event timing."""
@@ -184,20 +212,22 @@ class SosPlan:
     def forward(self, V: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         self._V(V)
         coef = out if out is not None else torch.empty(self.index.M, dtype=torch.float32, device="cuda")
+        _dev_f32(coef, "out", self.index.M)
         _check(load().sos_forward(self._h, _vp(V.data_ptr()), _vp(coef.data_ptr()), _stream()))
         return coef
 
     def backward(self, V: torch.Tensor, res: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         self._V(V)
-        _dev_f32(res, "res")
+        _dev_f32(res, "res", self.index.M)
         grad = out if out is not None else torch.empty_like(V)
+        _dev_f32(grad, "out", V.numel())
         _check(load().sos_backward(self._h, _vp(V.data_ptr()), _vp(res.data_ptr()), _vp(grad.data_ptr()), _stream()))
         return grad
 
     def loss_grad(self, V: torch.Tensor, p: torch.Tensor, want_grad: bool = True,
                   want_res: bool = False) -> Tuple[torch.Tensor, Optional[torch.Tensor], Optional[torch.Tensor]]:
         self._V(V)
-        _dev_f32(p, "p")
+        _dev_f32(p, "p", self.index.M)
         loss = torch.empty(1, dtype=torch.float64, device="cuda")
         grad = torch.empty_like(V) if want_grad else None
         res = torch.empty(self.index.M, dtype=torch.float32, device="cuda") if want_res else None
@@ -222,8 +252,9 @@ class SosPlan:
 
     def step(self, V: torch.Tensor, p: torch.Tensor, loss_out: Optional[torch.Tensor] = None) -> torch.Tensor:
         self._V(V)
-        _dev_f32(p, "p")
+        _dev_f32(p, "p", self.index.M)
         loss = loss_out if loss_out is not None else torch.empty(1, dtype=torch.float64, device="cuda")
+        _dev_f64_out(loss, "loss_out", 1)
         _check(load().sos_step(self._h, _vp(V.data_ptr()), _vp(p.data_ptr()), _vp(loss.data_ptr()), _stream()))
         return loss
 
@@ -232,17 +263,20 @@ class SosPlan:
         """`steps` descent steps in one call (V in place); returns the fp64 device
         tensor of the per-step losses L(V_t)."""
         self._V(V)
-        _dev_f32(p, "p")
+        _dev_f32(p, "p", self.index.M)
         losses = losses_out if losses_out is not None else torch.empty(max(steps, 1), dtype=torch.float64,
                                                                           device="cuda")
+        _dev_f64_out(losses, "losses_out", steps)
         _check(load().sos_descend(self._h, _vp(V.data_ptr()), _vp(p.data_ptr()), steps, _vp(losses.data_ptr()),
                                   _stream()))
         return losses[:steps]
 
     def solve_host(self, V: np.ndarray, p: np.ndarray, steps: int) -> np.ndarray:
         """Host-buffer descent (V updated in place); returns per-step losses."""
-        assert V.dtype == np.float32 and V.flags.c_contiguous and V.shape == (self.index.N, self.r)
-        assert p.dtype == np.float32 and p.flags.c_contiguous and p.shape == (self.index.M,)
+        if not (V.dtype == np.float32 and V.flags.c_contiguous and V.shape == (self.index.N, self.r)):
+            raise SosError(f"V must be a C-contiguous float32 array of shape {(self.index.N, self.r)}")
+        if not (p.dtype == np.float32 and p.flags.c_contiguous and p.shape == (self.index.M,)):
+            raise SosError(f"p must be a C-contiguous float32 array of shape {(self.index.M,)}")
         losses = np.empty(max(steps, 1), dtype=np.float64)
         _check(load().sos_solve_host(self._h, V.ctypes.data_as(_vp), p.ctypes.data_as(_vp), steps,
                                      losses.ctypes.data_as(_vp)))

@@ -85,7 +85,7 @@ static int dalloc(T** p, size_t bytes) {
 extern "C" {
 
 const char* sos_last_error(void) { return g_err; }
-int sos_version(void) { return 1; }
+int sos_version(void) { return 2; }
 
 // ------------------------------------------------------------------ index --
 int sos_build_index(int n, int d, sos_index** out) {
@@ -183,18 +183,20 @@ static size_t rlev_floats(const Index& ix) {
 // CTA-pair tiles: a = 256-row block, b = 160-col block, grouped raster (8 row
 // blocks per group) so a wave of CTAs shares A and B panels in L2
 static int64_t tile_group() {
+#ifdef SOS_EXPERIMENTS
     const char* ga = getenv("SOS_TILE_GROUP");
-    return ga && atoi(ga) > 0 ? atoi(ga) : 8;
+    if (ga && atoi(ga) > 0) return atoi(ga);
+#endif
+    return 8;
 }
 static int round_up32(int64_t x) { return (int)std::max<int64_t>(32, (x + 31) / 32 * 32); }
 
 // forward: upper triangle of the Gram matrix (columns j >= rows' block start);
 // backward: all of R V.  Columns tiled on the 160 grid; see TileCoord for the
 // narrow tiles
-static void build_tiles(int64_t row_blocks, int64_t ncols, bool upper, std::vector<TileCoord>& out) {
+static void build_tiles(int64_t row_blocks, int64_t ncols, bool upper, bool narrow, std::vector<TileCoord>& out) {
     const int64_t GA = tile_group();
     const int64_t col_blocks = (ncols + kTileN - 1) / kTileN;
-    static const bool narrow = !getenv("SOS_NARROW_TILES") || atoi(getenv("SOS_NARROW_TILES"));
     for (int64_t g0 = 0; g0 < row_blocks; g0 += GA) {
         const int64_t g1 = std::min(row_blocks, g0 + GA);
         for (int64_t b = 0; b < col_blocks; ++b)
@@ -211,7 +213,17 @@ static void build_tiles(int64_t row_blocks, int64_t ncols, bool upper, std::vect
 }
 
 int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
+    return sos_plan_create_ex(h, r, nullptr, out);
+}
+
+static bool pick(int opt, bool dflt) { return opt < 0 ? dflt : opt != 0; }
+
+int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts, sos_plan** out) {
     if (!h || !out || r < 1) return fail(SOS_ERR_ARG, "bad argument");
+    sos_plan_opts o = {-1, -1, -1, -1, -1};
+    if (opts) o = *opts;
+    for (int v : {o.split, o.vtq_from_update, o.vtq_in_aux, o.rmax_direct, o.narrow_tiles})
+        if (v < -1 || v > 1) return fail(SOS_ERR_ARG, "sos_plan_opts fields must be -1, 0 or 1");
     *out = nullptr;
     int sms = 0;
     int rc = require_device(&sms);
@@ -227,24 +239,23 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
     P.nkbV = (r + kQK - 1) / kQK;
     P.rowsVT = ((r + kTileN - 1) / kTileN) * kTileN;
     P.nkbN = (N + kQK - 1) / kQK;  // K = j runs over the N monomials (rows stay padded to Np)
+    P.narrow = pick(o.narrow_tiles, true);
     std::vector<TileCoord> tf, tb;
-    build_tiles(Np / kPairM, N, true, tf);
-    build_tiles(Np / kPairM, r, false, tb);
+    build_tiles(Np / kPairM, N, true, P.narrow, tf);
+    build_tiles(Np / kPairM, r, false, P.narrow, tb);
     P.ntiles_fwd = (int)tf.size();
     P.ntiles_bwd = (int)tb.size();
-    {
-        // sos_descend: the update can write the next step's V^T slices when its
-        // extra slicing work hides under a tile's MMAs (long K); for short K it
-        // would lengthen the update-bound backward (profiles/r1_vtq_next_ab.log)
-        const char* e = getenv("SOS_VTQ_UPDATE");
-        P.vtq_from_update = e ? atoi(e) != 0 : P.nkbN >= 128;
-        // short K: a tile's MMAs (~nkbN x 0.5 us) cannot hide the fused update
-        // (~25 us per tile), so store the gradient and update with all SMs
-        // (profiles/r1_update_split_ab.log)
-        const char* u = getenv("SOS_UPDATE_SPLIT");
-        P.update_split = u ? atoi(u) != 0 : P.nkbN < kUpdateSplitKb;
-        if (P.update_split) P.vtq_from_update = false;
-    }
+    // short K: a tile's MMAs (~nkbN x 0.5 us) cannot hide the fused update
+    // (~25 us per tile), so the split step stores the gradient and updates
+    // with all SMs (profiles/r1_update_split_ab.log, r2_split_step_ab.log)
+    P.split = pick(o.split, P.nkbN < kSplitKb);
+    // sos_descend: the update can write the next step's V^T slices when its
+    // extra slicing work hides under a tile's MMAs (long K); for short K it
+    // would lengthen the update-bound backward (profiles/r1_vtq_next_ab.log)
+    P.vtq_from_update = !P.split && pick(o.vtq_from_update, P.nkbN >= 128);
+    P.vtq_in_aux = pick(o.vtq_in_aux, vtq_fits_aux(P));
+    P.rmax_direct = pick(o.rmax_direct, rmax_direct_default(h->ix));
+    if (P.split) P.mid_grid = mid_grid_for(P.nkbN, P.rowsVT, M, sms, &P.mid_tiles);
     // row chunks of the last step's V release = the raster's row groups
     P.sig_blocks = (int)tile_group();
     P.sig_expect.assign((size_t)((Np / kPairM + P.sig_blocks - 1) / P.sig_blocks), 0u);
@@ -264,7 +275,7 @@ int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
         (rc = dalloc(&P.d_tiles_fwd, std::max<size_t>(1, tf.size()) * sizeof(TileCoord))) ||
         (rc = dalloc(&P.d_tiles_bwd, std::max<size_t>(1, tb.size()) * sizeof(TileCoord))) ||
         (rc = dalloc(&P.d_rowsig, std::max<size_t>(1, P.sig_expect.size()) * sizeof(unsigned))) ||
-        (P.update_split && (rc = dalloc(&P.d_grad, (size_t)N * r * sizeof(float))))) {
+        (P.split && (rc = dalloc(&P.d_grad, (size_t)N * r * sizeof(float))))) {
         sos_plan_destroy(pl);
         return rc;
     }
@@ -470,13 +481,26 @@ int sos_opt_set_stop(sos_plan* pl, double rel_tol) {
 
 int sos_step(sos_plan* pl, float* V_dev, const float* p_dev, double* loss_dev, void* stream) {
     if (!pl || !V_dev || !p_dev) return fail(SOS_ERR_ARG, "NULL argument");
+    if (reinterpret_cast<uintptr_t>(V_dev) & 15) return fail(SOS_ERR_ARG, "V_dev must be 16-byte aligned");
     Plan& P = pl->P;
     if (!P.opt_ready) return fail(SOS_ERR_ARG, "sos_opt_init not called");
     cudaStream_t st = (cudaStream_t)stream;
-    // loss and residual of the current V, then the backward GEMM whose aux
-    // warps apply the optimiser update to V in place, tile by tile
     int rc = upload_opt(P, st);
     if (rc) return rc;
+    if (P.split) {
+        // split step: exact maxima + VQ of V, forward, k_mid (residual, loss into
+        // loss_dev, R maxima, V^T and R slices), backward storing the gradient,
+        // row-block update of V (no next-step slices: the next call packs V again)
+        CK(cudaMemsetAsync(P.d_coef, 0, (size_t)P.idx->M * 4, st));
+        launch_pack_v(P, V_dev, st, P.d_vrow, P.d_vcol);
+        launch_gemm_fwd(P, P.d_coef, nullptr, st, P.d_vrow, P.d_vcol, true, true);
+        launch_mid(P, p_dev, V_dev, P.d_vcol, false, nullptr, loss_dev, false, st);
+        launch_gemm_bwd(P, P.d_grad, st, P.d_vcol, P.tmap_vtq_b, true);
+        launch_update_rows(P, V_dev, nullptr, nullptr, nullptr, st);
+        return check_launch("step");
+    }
+    // loss and residual of the current V, then the backward GEMM whose epilogue
+    // warps apply the optimiser update to V in place, tile by tile
     rc = do_loss_grad(P, V_dev, p_dev, loss_dev, nullptr, nullptr, st, true);
     if (rc) return rc;
     launch_step_begin(P, nullptr, st);
@@ -530,9 +554,20 @@ static int ensure_vtq2(Plan& P) {
 static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const float* p, double* losses,
                         cudaStream_t st, bool first = false) {
     // no memset nodes inside the replayed steps: the forward clears the loss
-    // accumulators, step_begin clears coef for the next forward and the next
-    // step's maxima (the first step of a call starts from a clean coef)
+    // accumulators, step_begin / k_mid clear coef for the next forward and the
+    // next step's maxima (the first step of a call starts from a clean coef)
     if (first) CK(cudaMemsetAsync(P.d_coef, 0, (size_t)P.idx->M * 4, st));
+    if (P.split) {
+        // split step (4 launches): VQ holds V_t sliced against its exact row
+        // maxima vrowx[b] (the previous update, or the prologue's pack); k_mid
+        // takes the column maxima of V_t into vcol[b] (cleared by the previous
+        // k_mid; exact already after the prologue, where atomicMax keeps them)
+        launch_gemm_fwd(P, P.d_coef, nullptr, st, d.vrowx[b], d.vcol[b], true, true);
+        launch_mid(P, p, V, d.vcol[b], true, d.vcol[b ^ 1], nullptr, true, st);
+        launch_gemm_bwd(P, P.d_grad, st, d.vcol[b], P.tmap_vtq_b, true);
+        launch_update_rows(P, V, P.d_vq, d.vrowx[b], d.vrowx[b ^ 1], st);
+        return check_launch("descend step");
+    }
     const bool vu = P.vtq_from_update;
     // VTQ[b] came from the previous update; else (and in the first step of a call,
     // into VTQ[0] = P.d_vtq with the exact column maxima) the forward packs it
@@ -540,8 +575,9 @@ static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const fl
     launch_residual(P, P.d_coef, p, P.d_res, st);
     // t += 1, losses[k] = L(V_t) (the call's array, from DevOpt); clear the next
     // maxima and the coefficient accumulator (read by the residual, done)
-    launch_step_begin(P, nullptr, st, true, d.vrowx[b ^ 1], P.rowsV, d.vcol[b ^ 1], P.rowsVT, P.d_coef);
-    launch_pack_r(P, P.d_res, st, 1);
+    launch_step_begin(P, nullptr, st, true, d.vrowx[b ^ 1], P.rowsV, d.vcol[b ^ 1], P.rowsVT, P.d_coef,
+                      P.rmax_direct);
+    launch_pack_r(P, P.d_res, st, 1, P.rmax_direct);
     const DescendBufs db = vu ? DescendBufs{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1], d.ucol[b],
                                             d.tmap_vtq[b], d.vtq[b ^ 1]}
                               : DescendBufs{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1], d.vcol[b],
@@ -579,7 +615,7 @@ static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps
     CK(cudaMemcpyAsync(&P.d_opt->losses, &P.h_losses, sizeof(double*), cudaMemcpyHostToDevice, st));
     // step 0 starts from the exact maxima and slices of the caller's V
     launch_pack_v(P, V_dev, st, d.vrowx[0], d.vcol[0]);
-    CK(cudaMemcpyAsync(d.urow[0], d.vrowx[0], P.rowsV * 4, cudaMemcpyDeviceToDevice, st));
+    if (!P.split) CK(cudaMemcpyAsync(d.urow[0], d.vrowx[0], P.rowsV * 4, cudaMemcpyDeviceToDevice, st));
     if (P.vtq_from_update)  // step 0's forward packs VTQ[0] with the exact column maxima
         CK(cudaMemcpyAsync(d.ucol[0], d.vcol[0], P.rowsVT * 4, cudaMemcpyDeviceToDevice, st));
     if ((rc = plain_step(0))) return rc;
@@ -626,6 +662,7 @@ static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps
 
 int sos_descend(sos_plan* pl, float* V_dev, const float* p_dev, int64_t steps, double* losses_dev, void* stream) {
     if (!pl || !V_dev || !p_dev || steps < 0 || (steps > 0 && !losses_dev)) return fail(SOS_ERR_ARG, "bad argument");
+    if (reinterpret_cast<uintptr_t>(V_dev) & 15) return fail(SOS_ERR_ARG, "V_dev must be 16-byte aligned");
     Plan& P = pl->P;
     if (!P.opt_ready) return fail(SOS_ERR_ARG, "sos_opt_init not called");
     if (steps == 0) return SOS_OK;
@@ -671,7 +708,7 @@ int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t ste
     // ship V back in row chunks while the last step's backward still runs (needs
     // stream memory operations; otherwise one copy after the last step)
     // (the split update of short-K plans does not release chunks: one copy at the end)
-    const PFN_wait_value32 wait = steps > 0 && !P.update_split ? wait_value_fn() : nullptr;
+    const PFN_wait_value32 wait = steps > 0 && !P.split ? wait_value_fn() : nullptr;
     bool overlap = wait != nullptr;
     if (overlap && !P.copy_st)
         overlap = cudaStreamCreateWithFlags(&P.copy_st, cudaStreamNonBlocking) == cudaSuccess &&

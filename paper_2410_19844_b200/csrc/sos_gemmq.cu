@@ -32,6 +32,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -41,6 +42,16 @@
 #include "sos_slice.cuh"
 
 namespace sos {
+
+// Experiment build only (-DSOS_EXPERIMENTS): the wait-cycle counters and the
+// traffic probes below compile away in the shipped library.
+#ifdef SOS_EXPERIMENTS
+constexpr bool kExperiments = true;
+#define SOS_CLOCK() clock64()
+#else
+constexpr bool kExperiments = false;
+#define SOS_CLOCK() 0ll
+#endif
 
 struct GemmArgs {
     int64_t a_rows;   // rows_total of the A Q-layout
@@ -61,9 +72,9 @@ struct GemmArgs {
     unsigned long long* progress;
     int skew_epoch, skew_lag;  // bounded K-skew (K-blocks per epoch, epochs of lead)
     int skew_sleep;            // ns between polls of the progress counter
-    unsigned long long* dbg;   // SOS_GEMM_STATS: per-role wait cycles (instrumentation only)
+    unsigned long long* dbg;   // experiments: SOS_GEMM_STATS per-role wait cycles
     int kserp;                 // walk K backwards on odd local tiles (L2 reuse across waves)
-    int probe;                 // SOS_GEMM_PROBE (experiment, wrong results): 1 = K-blocks mod 8,
+    int probe;                 // experiments: SOS_GEMM_PROBE (wrong results): 1 = K-blocks mod 8,
                                // 2 = also tile 0, 4 = 2 with B loaded only on the first ring pass
     // kModeBwdUpdate(Vtq): the optimiser step of PAPER.md:221, applied by the epilogue warps
     float* ring;  // per-CTA staging of the finished gradient tile (128 x 160 fp32, L2-resident)
@@ -249,10 +260,8 @@ __device__ __forceinline__ OptConsts opt_consts(const DevOpt* p) {
     oc.b1 = o.b1;
     oc.b2 = o.b2;
     oc.eps = o.eps;
-    const double c1 = 1.0 - pow((double)o.b1, (double)o.t);
-    const double c2 = 1.0 - pow((double)o.b2, (double)o.t);
-    oc.lr_c1 = (float)((double)o.lr / c1);
-    oc.inv_sqrt_c2 = (float)(1.0 / sqrt(c2));
+    oc.lr_c1 = o.lr_c1;  // advance_step (k_step_begin) formed them for this step
+    oc.inv_sqrt_c2 = o.inv_sqrt_c2;
     return oc;
 }
 
@@ -261,13 +270,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_gemmq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
     constexpr bool kFwd = kMode == kModeFwd;
     constexpr bool kUpd = kMode == kModeBwdUpdate || kMode == kModeBwdUpdateVtq;
-    // converged (sos_opt_set_stop): the whole grid leaves before any barrier,
-    // TMEM or cluster work, so V and the optimiser state stay as they are
-    if (kUpd && descent_stopped(args.scal, args.opt, args.use_stop)) {
-        if (args.rowsig && blockIdx.x == 0)  // nothing changes: release every chunk at once
-            for (int c = threadIdx.x; c < args.sig_chunks; c += blockDim.x) atomicExch(args.rowsig + c, kSigReleased);
-        return;
-    }
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
@@ -284,10 +286,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const bool leader = rank == 0;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
-    if (kFwd && args.zero_scal && blockIdx.x == 0 && threadIdx.x == 0) {
-        args.zero_scal->loss = 0.0;  // the residual that follows accumulates the new loss
-        args.zero_scal->pnorm2 = 0.0;
-    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
@@ -306,8 +304,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     cluster_sync();  // barrier inits + TMEM address visible pair-wide
     tc_fence_after();
     const uint32_t tbase = *tslot;
+    // launched with programmatic stream serialization (split steps), the setup
+    // above overlapped the previous kernel's tail; its results are visible from here
+    griddep_wait();
+    // converged (sos_opt_set_stop): no CTA touches V or the optimiser state
+    const bool stopped = kUpd && descent_stopped(args.scal, args.opt, args.use_stop);
+    if (stopped && args.rowsig && blockIdx.x == 0)  // nothing changes: release every chunk at once
+        for (int c = threadIdx.x; c < args.sig_chunks; c += blockDim.x) atomicExch(args.rowsig + c, kSigReleased);
+    if (kFwd && args.zero_scal && blockIdx.x == 0 && threadIdx.x == 0) {
+        args.zero_scal->loss = 0.0;  // the residual that follows accumulates the new loss
+        args.zero_scal->pnorm2 = 0.0;
+    }
 
-    if (warp == 0) {
+    if (stopped) {
+        // grid-uniform: straight to the teardown
+    } else if (warp == 0) {
         // ------------------------------------------------------- producer --
         // whole warp (warp-uniform loop state), one elected lane issues
         {
@@ -334,27 +345,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                         if (lane == 0) atomicAdd(args.progress, 1ull);
                         if (e >= args.skew_lag) {
                             const unsigned long long need = G * (unsigned long long)(e - args.skew_lag + 1);
-                            const long long c0 = clock64();
+                            const long long c0 = SOS_CLOCK();
                             if (lane == 0)
                                 for (int spin = 0; spin < kSkewMaxSpin && ld_acquire_u64(args.progress) < need; ++spin)
                                     if (args.skew_sleep) __nanosleep(args.skew_sleep);
                             __syncwarp();
-                            if (args.dbg && lane == 0) atomicAdd(args.dbg + 0, (unsigned long long)(clock64() - c0));
+                            if (kExperiments && args.dbg && lane == 0) atomicAdd(args.dbg + 0, (unsigned long long)(SOS_CLOCK() - c0));
                         }
                     }
                     {
-                        const long long c0 = clock64();
+                        const long long c0 = SOS_CLOCK();
                         mbar_wait(&empty[stage], phase ^ 1);
-                        if (args.dbg && lane == 0) atomicAdd(args.dbg + 1, (unsigned long long)(clock64() - c0));
+                        if (kExperiments && args.dbg && lane == 0) atomicAdd(args.dbg + 1, (unsigned long long)(SOS_CLOCK() - c0));
                     }
                     if (elect_one()) {
                         uint8_t* sa = smem + stage * kStageBytes;
-                        const bool skipB = args.probe == 4 && g >= kStages;
+                        const bool skipB = kExperiments && args.probe == 4 && g >= kStages;
                         if (leader) mbar_arrive_expect_tx(&full[stage], skipB ? 2 * kABytes : 2 * kStageBytes);
                         // the tensor maps view 4 consecutive 64-byte Q-rows as one 256-byte row
-                        const int kq = args.probe ? (kb & 7) : rev ? args.num_kb - 1 - kb : kb;
-                        const int32_t ra = args.probe >= 2 ? (int32_t)rank * 128 : rowA;
-                        const int32_t rb = args.probe >= 2 ? (int32_t)rank * kHalfN : rowB;
+                        const int kq = kExperiments && args.probe ? (kb & 7) : rev ? args.num_kb - 1 - kb : kb;
+                        const int32_t ra = kExperiments && args.probe >= 2 ? (int32_t)rank * 128 : rowA;
+                        const int32_t rb = kExperiments && args.probe >= 2 ? (int32_t)rank * kHalfN : rowB;
                         tma_load_3d_2sm(sa, &tmA, &full[stage], 0, (int32_t)((kq * args.a_rows + ra) >> 2), 0);
                         if (!skipB)
                             tma_load_3d_2sm(sa + kABytes, &tmB, &full[stage], 0, (int32_t)((kq * args.b_rows + rb) >> 2), 0);
@@ -376,7 +387,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         // values in uniform registers); one elected lane issues the MMAs and
         // commits.  A single-lane loop spent ~15 % of the tensor pipe on issue.
         if (leader) {
-            const long long t_start = clock64();
+            const long long t_start = SOS_CLOCK();
             const uint32_t d0 = tbase, d1 = tbase + kTileN, d2 = tbase + 2 * kTileN;
             // descriptor of stage 0, slice 0; other operands differ only in the
             // start-address field (bits 0-13, 16-byte units)
@@ -389,16 +400,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 for (int kb0 = 0; kb0 < args.num_kb; kb0 += args.seg_kb) {
                     const int kb1 = min(args.num_kb, kb0 + args.seg_kb);
                     {
-                        const long long c0 = clock64();
+                        const long long c0 = SOS_CLOCK();
                         mbar_wait_cluster(tempty, acc_phase ^ 1);
-                        if (args.dbg && lane == 0) atomicAdd(args.dbg + 2, (unsigned long long)(clock64() - c0));
+                        if (kExperiments && args.dbg && lane == 0) atomicAdd(args.dbg + 2, (unsigned long long)(SOS_CLOCK() - c0));
                     }
                     tc_fence_after();
                     for (int kb = kb0; kb < kb1; ++kb) {
                         {
-                            const long long c0 = clock64();
+                            const long long c0 = SOS_CLOCK();
                             mbar_wait(&full[stage], phase);
-                            if (args.dbg && lane == 0) atomicAdd(args.dbg + 3, (unsigned long long)(clock64() - c0));
+                            if (kExperiments && args.dbg && lane == 0) atomicAdd(args.dbg + 3, (unsigned long long)(SOS_CLOCK() - c0));
                         }
                         tc_fence_after();
                         const uint64_t sd = desc0 + (uint64_t)((stage * kStageBytes) >> 4);
@@ -433,7 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     acc_phase ^= 1;
                 }
             }
-            if (args.dbg && lane == 0) atomicAdd(args.dbg + 4, (unsigned long long)(clock64() - t_start));
+            if (kExperiments && args.dbg && lane == 0) atomicAdd(args.dbg + 4, (unsigned long long)(SOS_CLOCK() - t_start));
         }
     } else if (warp < 2 + kEpiWarps) {
         // -------------------------------------------------------- epilogue --
@@ -553,8 +564,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             const int t = threadIdx.x - 32 * (2 + kEpiWarps);
             const int64_t nkt = (args.rowsVT + 63) / 64;
             for (int64_t b = blockIdx.x; b < args.nkbN * nkt; b += gridDim.x)
-                pack_vtq_tile(args.Vsrc, args.N, args.r, args.rowsVT, args.nkbN, args.vcol, args.vtq, b / nkt,
-                              (b % nkt) * 64, auxbuf, t, 32 * kAuxWarps);
+                pack_vtq_tile<32 * kAuxWarps>(args.Vsrc, args.N, args.r, args.rowsVT, args.nkbN, args.vcol, args.vtq,
+                                              b / nkt, (b % nkt) * 64, auxbuf, t);
         }
     }
 
@@ -600,36 +611,74 @@ bool make_q_tmap(void* map_out, const uint8_t* base, int64_t rows_total, int64_t
     return r == CUDA_SUCCESS;
 }
 
+#ifdef SOS_EXPERIMENTS
+// Experiment build only (-DSOS_EXPERIMENTS, never the shipped library): tuning
+// and diagnostic switches read from the environment, see DESIGN.md 5.4.
 static int env_int(const char* name, int dflt) {
     const char* s = getenv(name);
     return s && *s ? atoi(s) : dflt;
 }
+#endif
+
+// CTAs of k_gemmq<kMode> that can be resident at once (2 per co-resident
+// cluster): the bounded K-skew waits for all CTAs of the grid, so the grid
+// must never exceed it (else every epoch would run into the spin bound)
+template <int kMode>
+static int resident_ctas(int num_sms) {
+    static int cached = -1;
+    if (cached < 0) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(num_sms & ~1);
+        cfg.blockDim = dim3(kGemmThreads);
+        cfg.dynamicSmemBytes = kSmemBytes;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, k_gemmq<kMode>, &cfg) != cudaSuccess || nc <= 0) {
+            cudaGetLastError();
+            nc = num_sms / 2;
+        }
+        cached = std::min(num_sms, 2 * nc);
+    }
+    return cached;
+}
 
 template <int kMode>
 static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorMap& mb, GemmArgs a,
-                           cudaStream_t st) {
-    static const int epoch = env_int("SOS_SKEW_EPOCH", kSkewEpoch), lag = env_int("SOS_SKEW_LAG", kSkewLag);
-    a.skew_epoch = epoch > 0 ? epoch : 1 << 30;
-    a.skew_lag = lag;
-    static const int sleep_ns = env_int("SOS_SKEW_SLEEP", 256);
-    a.skew_sleep = sleep_ns;
-    static const int probe = env_int("SOS_GEMM_PROBE", 0);
-    a.probe = probe;
-    static const int kserp = env_int("SOS_KSERP", 1);
-    a.kserp = kserp;
-    static unsigned long long* dbg = nullptr;
-    if (env_int("SOS_GEMM_STATS", 0)) {
-        if (!dbg && cudaMalloc(&dbg, 8 * sizeof(unsigned long long)) == cudaSuccess)
-            cudaMemset(dbg, 0, 8 * sizeof(unsigned long long));
-        a.dbg = dbg + (kMode == kModeFwd ? 0 : 0);
-    }
+                           cudaStream_t st, bool pdl = false) {
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(k_gemmq<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         configured = true;
     }
-    static const int max_ctas = env_int("SOS_GEMM_CTAS", 0);  // experiment: cap the persistent grid
-    const int sms = max_ctas > 0 && max_ctas < P.num_sms ? max_ctas : P.num_sms;
+    int sms = resident_ctas<kMode>(P.num_sms);
+    a.skew_epoch = kSkewEpoch;
+    a.skew_lag = kSkewLag;
+    a.skew_sleep = 256;
+    a.kserp = 1;
+#ifdef SOS_EXPERIMENTS
+    {
+        static const int epoch = env_int("SOS_SKEW_EPOCH", kSkewEpoch), lag = env_int("SOS_SKEW_LAG", kSkewLag);
+        a.skew_epoch = epoch > 0 ? epoch : 1 << 30;
+        a.skew_lag = lag;
+        a.skew_sleep = env_int("SOS_SKEW_SLEEP", 256);
+        a.probe = env_int("SOS_GEMM_PROBE", 0);
+        a.kserp = env_int("SOS_KSERP", 1);
+        static unsigned long long* dbg = nullptr;
+        if (env_int("SOS_GEMM_STATS", 0)) {
+            if (!dbg && cudaMalloc(&dbg, 8 * sizeof(unsigned long long)) == cudaSuccess)
+                cudaMemset(dbg, 0, 8 * sizeof(unsigned long long));
+            a.dbg = dbg;
+        }
+        const int max_ctas = env_int("SOS_GEMM_CTAS", 0);  // cap the persistent grid
+        if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
+    }
+#endif
     int grid = 2 * a.ntiles < sms ? 2 * a.ntiles : sms;
     grid &= ~1;
     if (grid <= 0) return cudaSuccess;
@@ -638,9 +687,13 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = kSmemBytes;
     cfg.stream = st;
-    cfg.attrs = nullptr;
-    cfg.numAttrs = 0;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemmq<kMode>, ma, mb, a);
+#ifdef SOS_EXPERIMENTS
     if (a.dbg) {  // SOS_GEMM_STATS: wait cycles summed over CTAs, per launch (instrumentation only)
         unsigned long long h[8];
         cudaStreamSynchronize(st);
@@ -654,6 +707,7 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
                 (double)h[2] / (grid / 2) / 1e6, 100.0 * h[2] / mma_total, (double)h[0] / grid / 1e6,
                 (double)h[1] / grid / 1e6);
     }
+#endif
     return e;
 }
 
@@ -661,20 +715,21 @@ static const CUtensorMap& tm(const uint8_t* raw) { return *reinterpret_cast<cons
 
 // The V^T slices for the backward come from the forward's two aux warps when
 // the forward is long enough to hide them (elements per aux thread vs K-blocks
-// per CTA pair: ~2.5 elements fit under one K-block's MMAs), else from the
-// all-SM k_pack_vtq before the GEMM (small / mid-size problems).
-static bool vtq_in_aux(const Plan& P) {
-    static const int force = env_int("SOS_VTQ_AUX", -1);
-    if (force >= 0) return force != 0;
-    const double pairs = P.num_sms / 2, grid_threads = P.num_sms * 64.0;
-    const double elems_per_thread = (double)P.idx->N * P.r / grid_threads;
+// per CTA pair, over the grid the forward actually launches: ~2.5 elements fit
+// under one K-block's MMAs), else from the all-SM k_pack_vtq before the GEMM
+// (small / mid-size problems).
+bool vtq_fits_aux(const Plan& P) {
+    const int grid = std::min<int64_t>(2 * (int64_t)P.ntiles_fwd, P.num_sms) & ~1;
+    if (grid <= 0) return false;
+    const double pairs = grid / 2, aux_threads = grid * 64.0;
+    const double elems_per_thread = (double)P.idx->N * P.r / aux_threads;
     const double kblocks_per_pair = std::ceil(P.ntiles_fwd / pairs) * P.nkbV;
     return elems_per_thread <= 2.5 * kblocks_per_pair;
 }
 
 void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st, const unsigned* urow,
-                     const unsigned* vcol, bool zero_scal) {
-    if (V_for_vtq && !vtq_in_aux(P)) {
+                     const unsigned* vcol, bool zero_scal, bool pdl) {
+    if (V_for_vtq && !P.vtq_in_aux) {
         launch_pack_vtq(P, V_for_vtq, st, vcol);
         V_for_vtq = nullptr;
     }
@@ -700,7 +755,7 @@ void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t 
     a.zero_scal = zero_scal ? P.d_scal : nullptr;
     a.progress = P.d_progress;
     LaunchScope ls(P, KK_GEMM_FWD, st);
-    launchq<kModeFwd>(P, tm(P.tmap_vq_a), tm(P.tmap_vq_b), a, st);
+    launchq<kModeFwd>(P, tm(P.tmap_vq_a), tm(P.tmap_vq_b), a, st, pdl && !ls.a);
 }
 
 static GemmArgs bwd_args(Plan& P, const unsigned* vcol) {
@@ -721,29 +776,17 @@ static GemmArgs bwd_args(Plan& P, const unsigned* vcol) {
     return a;
 }
 
-void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st) {
-    GemmArgs a = bwd_args(P, nullptr);
+void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st, const unsigned* vcol, const uint8_t* tmap_vtq, bool pdl) {
+    GemmArgs a = bwd_args(P, vcol);
     a.grad = grad;
     LaunchScope ls(P, KK_GEMM_BWD, st);
-    launchq<kModeBwdStore>(P, tm(P.tmap_rq_a), tm(P.tmap_vtq_b), a, st);
+    launchq<kModeBwdStore>(P, tm(P.tmap_rq_a), tm(tmap_vtq ? tmap_vtq : P.tmap_vtq_b), a, st, pdl && !ls.a);
 }
 
 // backward whose finished gradient tiles are consumed in the same kernel by the
 // optimiser step (GD or Adam): the gradient never makes an HBM round trip.  The
 // GEMM reads the packed copy VTQ, never V, so updating V in place is safe.
 void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBufs* db) {
-    if (P.update_split) {
-        // short K: the tiles' MMAs are too short to hide the update, so the
-        // gradient goes through HBM and the update runs on all SMs
-        GemmArgs a = bwd_args(P, db ? db->ucol_cur : nullptr);
-        a.grad = P.d_grad;
-        {
-            LaunchScope ls(P, KK_GEMM_BWD, st);
-            launchq<kModeBwdStore>(P, tm(P.tmap_rq_a), tm(db ? db->tmap_vtq_cur : P.tmap_vtq_b), a, st);
-        }
-        launch_update_split(P, V, st, db);
-        return;
-    }
     GemmArgs a = bwd_args(P, db ? db->ucol_cur : nullptr);
     if (db) {
         a.vq_next = P.d_vq;

@@ -21,9 +21,9 @@
 //       RQ  = R   (rows = monomial i, K = monomial j)    bwd A operand
 //   * per-row scales u = max / 127, kept as the float bits of the row maximum:
 //     vrow[i] = max_k |V_ik|, vcol[k] = max_j |V_jk|, rrow[i] = max_j |R_ij|.
-//   * pair-rank table PT[jb][i][64] (uint32, jb = j / 64):
-//         PT[((j / 64) * Np + i) * 64 + j % 64] = rank(alpha_i + alpha_j),
-//     0xFFFFFFFF for padding (i >= N or j >= N).
+//   * pair-rank table PT (uint32, rank(alpha_i + alpha_j), 0xFFFFFFFF for
+//     padding i >= N or j >= N): only the 64 x 64 blocks I <= J of the
+//     symmetric table are stored, see pt_entry / pt_entries below.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -33,7 +33,7 @@ namespace sos {
 
 // kernel kinds for per-launch event timing (sos_plan_timing_read)
 enum KernelKind { KK_ABSMAX_V = 0, KK_PACK_V, KK_GEMM_FWD, KK_RESIDUAL, KK_ABSMAX_R, KK_PACK_R, KK_GEMM_BWD,
-                  KK_UPDATE, KK_COUNT };
+                  KK_UPDATE, KK_MID, KK_COUNT };
 
 struct TimingRec { int kind; cudaEvent_t a, b; };
 struct Timing {
@@ -61,7 +61,7 @@ constexpr int kEpiWarps = 8;      // 4 TMEM lane quarters x 2 column halves
 constexpr int kEpiCols = kTileN / 2;  // 80 output columns per epilogue thread
 constexpr int kAuxWarps = 2;      // optimiser-update / V^T-pack warps of the GEMMs
 constexpr int kGemmThreads = 64 + 32 * (kEpiWarps + kAuxWarps);  // producer, MMA, epilogue, aux
-constexpr int kPtW = 64;          // pair-rank table chunk width (columns j per [jb][i] row)
+constexpr int kPtW = 64;          // pair-rank table block width (64 x 64 blocks, see pt_entry)
 // bounded K-skew between the CTAs of a GEMM (see the producer in sos_gemmq.cu)
 constexpr int kSkewEpoch = 8;     // K-blocks (of 64) per progress epoch (tools/gpu_skew2.sh)
 constexpr int kSkewLag = 1;       // epochs a CTA may run ahead of the slowest
@@ -89,7 +89,18 @@ struct DevOpt {
     long long loss_idx;     // sos_descend: next entry of the caller's loss array (device-managed)
     double* losses;         // sos_descend: the call's loss array (set per call, so the captured
                             // step graph does not depend on it)
+    float lr_c1;            // Adam constants of step t (device-managed, advance_step):
+    float inv_sqrt_c2;      //   lr / (1 - b1^t) and 1 / sqrt(1 - b2^t)
 };
+
+// t += 1 and the bias-correction constants of the new step (one thread, once per
+// step, before any update of that step reads them)
+__device__ __forceinline__ void advance_step(DevOpt* opt) {
+    const long long t = opt->t + 1;
+    opt->t = t;
+    opt->lr_c1 = (float)((double)opt->lr / (1.0 - pow((double)opt->b1, (double)t)));
+    opt->inv_sqrt_c2 = (float)(1.0 / sqrt(1.0 - pow((double)opt->b2, (double)t)));
+}
 
 // the device-side stopping rule of sos_step (sos_opt_set_stop), read after
 // the residual kernel completed the loss and |p|^2 reductions
@@ -142,14 +153,21 @@ struct Plan {
     int64_t rowsV;    // VQ rows_total: covers the 256-row A blocks and 160-row B blocks of N
     int64_t nkbV;     // VQ K-blocks: ceil(r / 64)
     int64_t rowsVT;   // VTQ rows_total: r rounded up to 160
-    int64_t nkbN;     // VTQ / RQ K-blocks: Np / 64
+    int64_t nkbN;     // VTQ / RQ K-blocks: ceil(N / 64) (RQ rows stay padded to Np)
     uint8_t* d_vq;    // VQ
     uint8_t* d_vtq;   // VTQ
     uint8_t* d_vtq2;  // sos_descend: second VTQ buffer (the update writes step t+1's while step t's is read)
-    bool vtq_from_update;  // sos_descend: the backward's update writes the next VTQ (long K only)
-    bool update_split;     // short K: gradient stored, then the all-SM k_update (the fused update
-                           // in 8 warps per SM would bound the backward)
-    float* d_grad;         // N x r gradient buffer of the split update (update_split only)
+    // implementation choices (sos_plan_opts, fixed at plan creation)
+    bool split;            // split step: fwd, k_mid (cooperative), bwd storing the gradient,
+                           // k_update_rows -- short K, where a tile's MMAs cannot hide the
+                           // fused update (~25 us per tile in 8 warps per SM)
+    bool vtq_from_update;  // sos_descend (fused step): the update writes the next VTQ (long K)
+    bool vtq_in_aux;       // the forward's aux warps write VTQ (else k_pack_vtq before it)
+    bool rmax_direct;      // R row maxima by one gather pass over PT (else the lattice DP)
+    bool narrow;           // narrow tiles at ragged column blocks
+    int mid_grid;          // cooperative grid of k_mid (co-resident blocks)
+    int mid_tiles;         // R blocks each k_mid block holds in shared memory
+    float* d_grad;         // N x r gradient buffer of the split step
     uint8_t* d_rq;    // RQ
     unsigned* d_vrow; // max_k |V_ik| (float bits), rowsV
     unsigned* d_vcol; // max_j |V_jk| (float bits), rowsVT
@@ -243,13 +261,17 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow = nu
 void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st, const unsigned* vcol = nullptr);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
 // losses_from_opt: record into the loss array set for the current sos_descend call;
-// zero0 / zero1 (n0 / n1 words), zero_coef (M floats): accumulators to clear for the next stage
+// zero0 / zero1 (n0 / n1 words), zero_coef (M floats), zero_rrow (the R row
+// maxima): accumulators to clear for the next stage
 void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt = false,
                        unsigned* zero0 = nullptr, int64_t n0 = 0, unsigned* zero1 = nullptr, int64_t n1 = 0,
-                       float* zero_coef = nullptr);
-void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop);
+                       float* zero_coef = nullptr, bool zero_rrow = false);
+void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop, bool rrow_zeroed = false);
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop);
-void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop);  // maxima + RQ
+// maxima + RQ; rrow_zeroed: rrow already cleared on the stream (direct maxima)
+void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop, bool rrow_zeroed = false);
+// the cost model choosing the direct R maxima pass over the lattice DP
+bool rmax_direct_default(const Index& ix);
 // sos_descend: maxima buffers of the current and the next step
 struct DescendBufs {
     const unsigned* vrow_cur;  // exact row maxima of the current V
@@ -260,17 +282,37 @@ struct DescendBufs {
     const uint8_t* tmap_vtq_cur;  // tensor map of the current VTQ buffer
     uint8_t* vtq_next;         // VTQ buffer the update writes for the next step
 };
-// plans with fewer K-blocks (N / 64) than this use the split update (Plan::update_split)
-constexpr int kUpdateSplitKb = 48;
-// the optimiser step as its own all-SM kernel (update_split), same arithmetic and
-// outputs as the backward's fused update (db: sos_descend's next-step VQ + maxima)
-void launch_update_split(Plan& P, float* V, cudaStream_t st, const DescendBufs* db);
+// plans with fewer K-blocks (N / 64) than this use the split step (Plan::split)
+constexpr int kSplitKb = 48;
+// split step, between forward and backward: residual + loss, step bookkeeping
+// (t += 1, loss record: losses[0], or the sos_descend array from DevOpt with
+// losses_from_opt), with colmax the exact column maxima of V (atomicMax into
+// vcol, cleared by the previous k_mid -- or already exact), V^T slices, R row
+// maxima (direct), coef cleared, R slices; zero_cols (rowsVT words) cleared
+// for the next step's k_mid
+void launch_mid(Plan& P, const float* p, const float* V, unsigned* vcol, bool colmax, unsigned* zero_cols,
+                double* losses, bool losses_from_opt, cudaStream_t st);
+// split step, after the backward: GD / Adam on blocks of whole rows of V (the
+// gradient in P.d_grad); with vq_next also the next step's VQ against the EXACT
+// new row maxima (vrow_next); a stopped descent copies the current maxima
+void launch_update_rows(Plan& P, float* V, uint8_t* vq_next, const unsigned* vrow_cur, unsigned* vrow_next,
+                        cudaStream_t st);
+// cooperative grid of k_mid (blocks) and the R blocks each holds (tiles_per_block)
+int mid_grid_for(int64_t nkbN, int64_t rowsVT, int64_t M, int num_sms, int* tiles_per_block);
 // slices written by the update use kHeadroom x the current row maximum
 constexpr float kHeadroom = 2.f;
 
+// pdl: launch with programmatic stream serialization (the kernel's setup overlaps
+// the previous kernel's tail; used where that kernel holds no TMEM)
 void launch_gemm_fwd(Plan& P, float* coef, const float* V_for_vtq, cudaStream_t st, const unsigned* urow = nullptr,
-                     const unsigned* vcol = nullptr, bool zero_scal = false);
-void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st);
+                     const unsigned* vcol = nullptr, bool zero_scal = false, bool pdl = false);
+// backward storing 4RV into grad; vcol / tmap_vtq: column scales and tensor map of
+// the V^T slices to read (default: the plan's VTQ and vcol)
+void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st, const unsigned* vcol = nullptr,
+                     const uint8_t* tmap_vtq = nullptr, bool pdl = false);
+// whether the forward's aux warps can hide the V^T pack (elements per aux thread
+// vs K-blocks per CTA pair over the forward's actual grid)
+bool vtq_fits_aux(const Plan& P);
 void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBufs* db = nullptr);
 void launch_descend_fixup_cols(Plan& P, const float* V, const unsigned* vcol_cur, const unsigned* vcol_next,
                                unsigned* ucol_next, uint8_t* vtq_next, cudaStream_t st);

@@ -4,9 +4,13 @@
 // loss reduction.  The optimiser update of PAPER.md:221 runs inside the backward
 // GEMM (sos_gemmq.cu).  All kernels are coalesced and sized as a multiple of
 // the SM count (grid-stride).
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
+#include "sm100_ptx.cuh"
 #include "sos_internal.cuh"
 #include "sos_slice.cuh"
 
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(256) k_pack_vtq(const float* __restrict__ V, i
     __shared__ float tile[64][65];
     const int64_t nkt = (rowsVT + 63) / 64;
     for (int64_t b = blockIdx.x; b < nkbN * nkt; b += gridDim.x)
-        pack_vtq_tile(V, N, r, rowsVT, nkbN, vcol, VTQ, b / nkt, (b % nkt) * 64, tile, threadIdx.x, 256);
+        pack_vtq_tile<256>(V, N, r, rowsVT, nkbN, vcol, VTQ, b / nkt, (b % nkt) * 64, tile, threadIdx.x);
 }
 
 // ------------------------------------------------------------- residual ----
@@ -297,169 +301,469 @@ void launch_residual(Plan& P, const float* coef, const float* p, float* res, cud
     k_residual<<<grid_for(P, P.idx->M, 256, 4), 256, 0, st>>>(coef, p, res, P.idx->M, P.d_scal);
 }
 
-void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop) {
+// rrow_zeroed: the caller cleared rrow in the same stream (k_step_begin inside
+// sos_descend, so the replayed steps hold no memset node)
+void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop, bool rrow_zeroed) {
     LaunchScope ls(P, KK_ABSMAX_R, st);
-    cudaMemsetAsync(P.d_rrow, 0, (size_t)P.idx->Np * sizeof(unsigned), st);
+    if (!rrow_zeroed) cudaMemsetAsync(P.d_rrow, 0, (size_t)P.idx->Np * sizeof(unsigned), st);
     const int64_t nkb = P.idx->Np / kPtW, npairs = nkb * (nkb + 1) / 2;
     const unsigned blocks = (unsigned)std::min<int64_t>(npairs, (int64_t)P.num_sms * 8);
     k_rmax<<<blocks, 256, 0, st>>>(P.idx->d_pt, res, nkb, P.d_rrow, P.d_scal, P.d_opt, use_stop);
 }
 
-// one thread: t += 1 (Adam bias correction of this step), and in sos_descend
-// the loss of this step into the caller's array
-// step bookkeeping (Adam t, loss record) and, inside sos_descend, zeroing of
-// the next step's maxima accumulators (zero0 / zero1: n0 / n1 words) and of
-// the coefficient accumulator of the next forward (zc: nc floats, 16-B aligned)
+// step bookkeeping (one thread: Adam t += 1; inside sos_descend the loss of
+// this step into the call's array) and zeroing of accumulators: the next
+// step's maxima (zero0 / zero1: n0 / n1 words), the R row maxima of the direct
+// pass (zero2: n2 words) and the coefficient accumulator of the next forward
+// (zc: nc floats, 16-B aligned)
 __global__ void k_step_begin(DevOpt* opt, const Scalars* sc, double* losses, int from_opt, unsigned* zero0,
-                             int64_t n0, unsigned* zero1, int64_t n1, float* zc, int64_t nc) {
+                             int64_t n0, unsigned* zero1, int64_t n1, unsigned* zero2, int64_t n2, float* zc,
+                             int64_t nc) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        opt->t += 1;
+        advance_step(opt);
         if (from_opt) losses = opt->losses;
         if (losses) losses[opt->loss_idx++] = sc->loss;
     }
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    for (int64_t e = tid; e < n0 + n1; e += stride) {
+    for (int64_t e = tid; e < n0 + n1 + n2; e += stride) {
         if (e < n0) zero0[e] = 0u;
-        else zero1[e - n0] = 0u;
+        else if (e < n0 + n1) zero1[e - n0] = 0u;
+        else zero2[e - n0 - n1] = 0u;
     }
     for (int64_t e = tid; e < nc / 4; e += stride) reinterpret_cast<float4*>(zc)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t e = (nc / 4) * 4 + tid; e < nc; e += stride) zc[e] = 0.f;
 }
 
-// The optimiser step over the whole N x r gradient (short-K problems, see
-// Plan::update_split).  Block tile = 16 rows x 256 columns: warp w owns rows
-// 2w, 2w+1, lane l the columns l + 32e (e < 8), so every access is a coalesced
-// row segment and all 64 loads of a thread are in flight together; the new
-// values are staged in shared memory for the next step's VQ chunks (task =
-// row x 16-column chunk, scale kHeadroom * old row max); row maxima by warp
-// shuffles, column maxima per thread over its rows, then across the 8 warps.
-constexpr int kUpdCols = 256, kUpdLd = kUpdCols + 4;
-__global__ void __launch_bounds__(256) k_update(const float* __restrict__ grad, float* __restrict__ V,
-                                                float* __restrict__ m, float* __restrict__ v, int64_t N, int64_t r,
-                                                int adam, const DevOpt* opt, const Scalars* sc,
-                                                uint8_t* __restrict__ vq_next, int64_t rowsV, int64_t nkbV,
-                                                const unsigned* __restrict__ vrow_cur, unsigned* __restrict__ vrow_next,
-                                                unsigned* __restrict__ vcol_next) {
-    if (descent_stopped(sc, opt, 1)) return;
-    constexpr int kE = kUpdCols / 32;
-    __shared__ float cst[6];
-    __shared__ __align__(16) float stage[16 * kUpdLd];
-    __shared__ float cm_s[8][kUpdCols];
-    if (threadIdx.x == 0) {
-        const DevOpt o = *opt;
-        cst[0] = o.lr;
-        cst[1] = o.b1;
-        cst[2] = o.b2;
-        cst[3] = o.eps;
-        cst[4] = (float)((double)o.lr / (1.0 - pow((double)o.b1, (double)o.t)));
-        cst[5] = (float)(1.0 / sqrt(1.0 - pow((double)o.b2, (double)o.t)));
+// ------------------------------------------------- split step: update ----
+// GD / Adam on a block of kUpdRows whole rows of V, in two
+// passes.  Pass 1 is purely elementwise: the block's rows are one contiguous
+// span of V, m, v and the gradient (16-byte aligned: the block starts at a row
+// multiple of 4), streamed as float4 with kUpdU of them in flight per array and
+// thread; the new values also go to a shared-memory copy of the span (or, for
+// rows longer than kUpdSmemR, are re-read from L2).  Pass 2 takes the EXACT
+// maximum of each new row (one warp per row) and slices the rows into the next
+// step's VQ against it (thread = 4 K-values, one word per slice): no headroom
+// scale, no fixup kernel.  (The column maxima of V_{t+1}, for its V^T slices,
+// are taken by the next k_mid.)  A stopped descent (sos_opt_set_stop) leaves V,
+// m, v and VQ unchanged and carries the row maxima over.
+constexpr int kUpdRows = 4, kUpdThreads = 256, kUpdU = 2;
+constexpr int64_t kUpdSmemR = 4096;  // rows up to this length are staged in shared memory (64 KB)
+__device__ __forceinline__ float adam_or_gd(bool adam, float x, float g, float& m, float& v, const DevOpt& o) {
+    if (!adam) return x - o.lr * g;
+    m = o.b1 * m + (1.f - o.b1) * g;
+    v = o.b2 * v + (1.f - o.b2) * g * g;
+    return x - o.lr_c1 * m / (sqrtf(v) * o.inv_sqrt_c2 + o.eps);
+}
+__global__ void __launch_bounds__(kUpdThreads) k_update_rows(
+    const float* __restrict__ grad, float* V, float* __restrict__ m, float* __restrict__ v, int64_t N, int64_t r,
+    int adam, const DevOpt* opt, const Scalars* sc, uint8_t* __restrict__ vq_next, int64_t rowsV, int64_t nkbV,
+    const unsigned* __restrict__ vrow_cur, unsigned* __restrict__ vrow_next) {
+    extern __shared__ float4 stage4[];  // the block's span (flat), when r <= kUpdSmemR
+    __shared__ float rmax_s[kUpdRows];
+    griddep_wait();  // launched with programmatic stream serialization after the backward
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * kUpdRows;
+    const int nr = (int)(N - i0 < kUpdRows ? N - i0 : kUpdRows);
+    if (descent_stopped(sc, opt, 1)) {
+        if (vrow_next && t < nr) vrow_next[i0 + t] = vrow_cur[i0 + t];
+        return;
     }
-    __syncthreads();
-    const float lr = cst[0], b1 = cst[1], b2 = cst[2], eps = cst[3], lr_c1 = cst[4], isc2 = cst[5];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, t = threadIdx.x;
-    const bool q = vq_next != nullptr;
-    const int64_t col_tiles = (r + kUpdCols - 1) / kUpdCols, row_tiles = (N + 15) / 16;
-    for (int64_t blk = blockIdx.x; blk < row_tiles * col_tiles; blk += gridDim.x) {
-        const int64_t row0 = (blk / col_tiles) * 16, col0 = (blk % col_tiles) * kUpdCols;
-        float gv[2][kE], x[2][kE], mm[2][kE], vv[2][kE];
-        bool ok[2][kE];
-        int64_t ro[2];
+    const DevOpt o = *opt;
+    const bool in_smem = r <= kUpdSmemR;
+    const int64_t base = i0 * r, len = nr * r, n4 = len >> 2;
+    const float4* g4 = reinterpret_cast<const float4*>(grad + base);
+    float4* V4 = reinterpret_cast<float4*>(V + base);
+    float4* m4 = reinterpret_cast<float4*>(m + base);
+    float4* v4 = reinterpret_cast<float4*>(v + base);
+    for (int64_t q0 = t; q0 < n4; q0 += kUpdThreads * kUpdU) {
+        float4 gv[kUpdU], x[kUpdU], mm[kUpdU], vv[kUpdU];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int64_t i = row0 + 2 * w + k;
-            ro[k] = i * r + col0 + lane;
-#pragma unroll
-            for (int e = 0; e < kE; ++e) {
-                ok[k][e] = i < N && col0 + lane + 32 * e < r;
-                gv[k][e] = ok[k][e] ? grad[ro[k] + 32 * e] : 0.f;
-                x[k][e] = ok[k][e] ? V[ro[k] + 32 * e] : 0.f;
+        for (int u = 0; u < kUpdU; ++u) {
+            const int64_t q = q0 + kUpdThreads * u;
+            if (q < n4) {
+                gv[u] = __ldcs(g4 + q);
+                x[u] = __ldcs(V4 + q);
                 if (adam) {
-                    mm[k][e] = ok[k][e] ? m[ro[k] + 32 * e] : 0.f;
-                    vv[k][e] = ok[k][e] ? v[ro[k] + 32 * e] : 0.f;
+                    mm[u] = __ldcs(m4 + q);
+                    vv[u] = __ldcs(v4 + q);
                 }
             }
         }
-        float cm[kE];
 #pragma unroll
-        for (int e = 0; e < kE; ++e) cm[e] = 0.f;
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            float mx = 0.f;
-#pragma unroll
-            for (int e = 0; e < kE; ++e) {
-                float xn = 0.f;
-                if (ok[k][e]) {
-                    if (adam) {
-                        mm[k][e] = b1 * mm[k][e] + (1.f - b1) * gv[k][e];
-                        vv[k][e] = b2 * vv[k][e] + (1.f - b2) * gv[k][e] * gv[k][e];
-                        xn = x[k][e] - lr_c1 * mm[k][e] / (sqrtf(vv[k][e]) * isc2 + eps);
-                        m[ro[k] + 32 * e] = mm[k][e];
-                        v[ro[k] + 32 * e] = vv[k][e];
-                    } else {
-                        xn = x[k][e] - lr * gv[k][e];
-                    }
-                    V[ro[k] + 32 * e] = xn;
-                }
-                if (q) {
-                    stage[(2 * w + k) * kUpdLd + lane + 32 * e] = xn;
-                    mx = fmaxf(mx, fabsf(xn));
-                    cm[e] = fmaxf(cm[e], fabsf(xn));
-                }
+        for (int u = 0; u < kUpdU; ++u) {
+            const int64_t q = q0 + kUpdThreads * u;
+            if (q >= n4) break;
+            float4 xn;
+            if (adam) {
+                xn.x = adam_or_gd(true, x[u].x, gv[u].x, mm[u].x, vv[u].x, o);
+                xn.y = adam_or_gd(true, x[u].y, gv[u].y, mm[u].y, vv[u].y, o);
+                xn.z = adam_or_gd(true, x[u].z, gv[u].z, mm[u].z, vv[u].z, o);
+                xn.w = adam_or_gd(true, x[u].w, gv[u].w, mm[u].w, vv[u].w, o);
+                __stcs(m4 + q, mm[u]);
+                __stcs(v4 + q, vv[u]);
+            } else {
+                xn = make_float4(x[u].x - o.lr * gv[u].x, x[u].y - o.lr * gv[u].y, x[u].z - o.lr * gv[u].z,
+                                 x[u].w - o.lr * gv[u].w);
             }
-            if (q) {
-                mx = warp_max(mx);
-                const int64_t i = row0 + 2 * w + k;
-                if (lane == 0 && i < N && mx > 0.f) atomicMax(vrow_next + i, __float_as_uint(mx));
-            }
+            V4[q] = xn;  // default policy: L2-resident for the next k_mid
+            if (in_smem) stage4[q] = xn;
         }
-        if (q) {
+    }
+    float* stage = reinterpret_cast<float*>(stage4);
+    for (int64_t e = 4 * n4 + t; e < len; e += kUpdThreads) {  // ragged end of the last block's span
+        float mm1 = adam ? m[base + e] : 0.f, vv1 = adam ? v[base + e] : 0.f;
+        const float xn = adam_or_gd(adam, V[base + e], grad[base + e], mm1, vv1, o);
+        V[base + e] = xn;
+        if (adam) {
+            m[base + e] = mm1;
+            v[base + e] = vv1;
+        }
+        if (in_smem) stage[e] = xn;
+    }
+    __syncthreads();  // the new rows are in shared memory / in V (visible to the block)
+    const float* src = in_smem ? stage : V + base;
+    if (w < nr) {
+        float mx = 0.f;
+        for (int64_t c = lane; c < r; c += 32) mx = fmaxf(mx, fabsf(src[w * r + c]));
+        mx = warp_max(mx);
+        if (lane == 0) {
+            rmax_s[w] = mx;
+            if (vrow_next) vrow_next[i0 + w] = __float_as_uint(mx);
+        }
+    }
+    if (!vq_next) return;
+    __syncthreads();
+    const int64_t nq = nkbV * 16;  // 4-value quads per VQ row (K padded to 64)
+    for (int rr = 0; rr < nr; ++rr) {
+        const float sc4 = slice_scale(__float_as_uint(rmax_s[rr]));
+        const float* row = src + rr * r;
+        for (int64_t qd = t; qd < nq; qd += kUpdThreads) {
+            const int64_t k0 = 4 * qd;
+            float xs[4];
 #pragma unroll
-            for (int e = 0; e < kE; ++e) cm_s[w][lane + 32 * e] = cm[e];
-            __syncthreads();
-            {   // task t = (row t / 16, 16-column chunk t % 16)
-                const int rr = t >> 4, cq = t & 15;
-                const int64_t i = row0 + rr, k0 = col0 + 16 * cq;
-                if (i < N && k0 < r) {
-                    float xs[16];
-                    const float4* s4 = reinterpret_cast<const float4*>(stage + rr * kUpdLd + 16 * cq);
+            for (int e = 0; e < 4; ++e) xs[e] = k0 + e < r ? row[k0 + e] : 0.f;
+            uint32_t qw[3];
+            slice4(xs, sc4, qw);
+            const int64_t cq = qd >> 2;
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        const float4 f = s4[q4];
-                        xs[4 * q4] = f.x; xs[4 * q4 + 1] = f.y; xs[4 * q4 + 2] = f.z; xs[4 * q4 + 3] = f.w;
-                    }
-                    const float um = kHeadroom * __uint_as_float(__ldg(vrow_cur + i));
-                    uint4 qq[3];
-                    slice16(xs, slice_scale(__float_as_uint(um)), qq);
-                    store_q16(vq_next, k0 >> 6, i, (int)((k0 >> 4) & 3), nkbV, rowsV, qq);
-                }
-            }
-            {   // column t: maximum over the 16 rows (8 warps x 2)
-                float c = 0.f;
-#pragma unroll
-                for (int ww = 0; ww < 8; ++ww) c = fmaxf(c, cm_s[ww][t]);
-                if (col0 + t < r && c > 0.f) atomicMax(vcol_next + col0 + t, __float_as_uint(c));
-            }
-            __syncthreads();
+            for (int sl = 0; sl < 3; ++sl)
+                *reinterpret_cast<uint32_t*>(vq_next + q_offset(sl, cq >> 2, i0 + rr, (int)(cq & 3), nkbV, rowsV) +
+                                             4 * (qd & 3)) = qw[sl];
         }
     }
 }
 
-void launch_update_split(Plan& P, float* V, cudaStream_t st, const DescendBufs* db) {
+void launch_update_rows(Plan& P, float* V, uint8_t* vq_next, const unsigned* vrow_cur, unsigned* vrow_next,
+                        cudaStream_t st) {
     LaunchScope ls(P, KK_UPDATE, st);
-    const int64_t N = P.idx->N, blocks = ((N + 15) / 16) * ((P.r + kUpdCols - 1) / kUpdCols);
-    k_update<<<grid_for(P, blocks * 256, 256), 256, 0, st>>>(
-        P.d_grad, V, P.d_m, P.d_v, N, P.r, P.opt_kind == 1, P.d_opt, P.d_scal, db ? P.d_vq : nullptr, P.rowsV,
-        P.nkbV, db ? db->vrow_cur : nullptr, db ? db->vrow_next : nullptr, db ? db->vcol_next : nullptr);
+    const int64_t N = P.idx->N, blocks = (N + kUpdRows - 1) / kUpdRows;
+    const size_t smem = P.r <= kUpdSmemR ? (size_t)kUpdRows * P.r * sizeof(float) : 0;
+    static size_t configured = 48 * 1024;
+    if (smem > configured) {
+        cudaFuncSetAttribute(k_update_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kUpdRows * kUpdSmemR * 4));
+        configured = kUpdRows * kUpdSmemR * 4;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(kUpdThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = ls.a ? 0 : 1;
+    cudaLaunchKernelEx(&cfg, k_update_rows, (const float*)P.d_grad, V, P.d_m, P.d_v, N, P.r, (int)(P.opt_kind == 1),
+                       (const DevOpt*)P.d_opt, (const Scalars*)P.d_scal, vq_next, P.rowsV, P.nkbV, vrow_cur, vrow_next);
+}
+
+// --------------------------------------------------- split step: k_mid ----
+// Everything between the forward and the backward of a split step in ONE
+// cooperative kernel (three phases separated by grid barriers) instead of
+// 5-7 dependent launches, which bound short-K steps:
+//   A: res = coef - p, loss += res^2 and |p|^2 (fp64 block sums, the stopping
+//      rule's inputs); with colmax, the column maxima of V (per 64 x 64 tile,
+//      atomicMax into vcol, which the previous k_mid cleared); clear rrow and
+//      the next step's column maxima (zero_cols)
+//   B: t += 1 and the loss record; the V^T slices of V (exact column maxima);
+//      unless stopped, each block gathers its 64 x 64 blocks {I <= J} of R
+//      through PT into shared memory (they stay there) and folds them into the
+//      row maxima of I and J (atomicMax); coef cleared for the next forward
+//   C: unless stopped, the held R blocks are sliced into RQ (rows of I at
+//      K-block J and, transposed, rows of J at K-block I) -- R is gathered
+//      once, not once for the maxima and again for the slices
+struct MidArgs {
+    float* coef;
+    const float* p;
+    float* res;
+    int64_t M;
+    Scalars* sc;
+    DevOpt* opt;
+    double* losses;
+    int losses_from_opt;
+    const uint32_t* pt;
+    int64_t Np, nkbN;
+    unsigned* rrow;
+    uint8_t* RQ;
+    const float* V;
+    int64_t N, r, rowsVT;
+    unsigned* vcol;
+    int colmax;
+    uint8_t* VTQ;
+    unsigned* zero_cols;
+    int trace;  // experiment build only
+};
+
+__device__ __forceinline__ void block_pair(int64_t pr, int64_t& I, int64_t& J) {
+    // pr enumerates the upper block triangle column by column: J, then I = 0..J
+    J = (int64_t)((sqrt(8.0 * (double)pr + 1.0) - 1.0) * 0.5);
+    while (J * (J + 1) / 2 > pr) --J;
+    while ((J + 1) * (J + 2) / 2 <= pr) ++J;
+    I = pr - J * (J + 1) / 2;
+}
+
+constexpr int kMidThreads = 256;
+constexpr size_t kMidTileBytes = (size_t)kPtW * (kPtW + 1) * sizeof(float);
+
+#ifdef SOS_EXPERIMENTS
+// SOS_MID_TRACE=1 (experiment build): block 0 prints the phase boundaries of k_mid
+#define MID_MARK(k) do { if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) { \
+    unsigned long long now_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_)); tmark[k] = now_; } } while (0)
+#else
+#define MID_MARK(k) do { } while (0)
+#endif
+
+__global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+#ifdef SOS_EXPERIMENTS
+    unsigned long long tmark[6] = {0, 0, 0, 0, 0, 0};
+#endif
+    MID_MARK(0);
+    extern __shared__ float smem_tiles[];  // R blocks held from phase B to C, 64 x 65 floats each
+    __shared__ double red[2][kMidThreads / 32];
+    float(*tile0)[kPtW + 1] = reinterpret_cast<float(*)[kPtW + 1]>(smem_tiles);
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + t, gstride = (int64_t)gridDim.x * blockDim.x;
+    // ---- A
+    {
+        double l = 0.0, pn = 0.0;
+        for (int64_t e = gtid; e < a.M; e += gstride) {
+            const float pv = a.p[e];
+            const float rv = a.coef[e] - pv;
+            a.res[e] = rv;
+            l += (double)rv * rv;
+            pn += (double)pv * pv;
+        }
+        l = warp_sum(l);
+        pn = warp_sum(pn);
+        if (lane == 0) { red[0][w] = l; red[1][w] = pn; }
+        __syncthreads();
+        if (w == 0) {
+            l = lane < kMidThreads / 32 ? red[0][lane] : 0.0;
+            pn = lane < kMidThreads / 32 ? red[1][lane] : 0.0;
+            l = warp_sum(l);
+            pn = warp_sum(pn);
+            if (lane == 0) {
+                atomicAdd(&a.sc->loss, l);
+                atomicAdd(&a.sc->pnorm2, pn);
+            }
+        }
+        for (int64_t e = gtid; e < a.Np; e += gstride) a.rrow[e] = 0u;
+        if (a.zero_cols)
+            for (int64_t e = gtid; e < a.rowsVT; e += gstride) a.zero_cols[e] = 0u;
+        if (a.colmax) {
+            // tile (64 rows of V) x (64 columns): thread = (column t & 63, 16-row group t >> 6)
+            const int64_t nkc = (a.r + 63) / 64;
+            const int c = t & 63, g = t >> 6;
+            for (int64_t b = blockIdx.x; b < a.nkbN * nkc; b += gridDim.x) {
+                const int64_t j0 = (b / nkc) * 64 + g * 16, k = (b % nkc) * 64 + c;
+                float mx = 0.f;
+                if (k < a.r) {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        if (j0 + e < a.N) mx = fmaxf(mx, fabsf(a.V[(j0 + e) * a.r + k]));
+                }
+                tile0[g][c] = mx;
+                __syncthreads();
+                if (t < 64) {
+                    const float mc = fmaxf(fmaxf(tile0[0][t], tile0[1][t]), fmaxf(tile0[2][t], tile0[3][t]));
+                    const int64_t kk = (b % nkc) * 64 + t;
+                    if (kk < a.r && mc > 0.f) atomicMax(a.vcol + kk, __float_as_uint(mc));
+                }
+                __syncthreads();
+            }
+        }
+    }
+    MID_MARK(1);
+    grid.sync();
+    MID_MARK(2);
+    // ---- B
+    if (blockIdx.x == 0 && t == 0) {
+        advance_step(a.opt);
+        double* L = a.losses_from_opt ? a.opt->losses : a.losses;
+        if (L) L[a.losses_from_opt ? a.opt->loss_idx++ : 0] = a.sc->loss;
+    }
+    const bool stopped = descent_stopped(a.sc, a.opt, 1);
+    const int64_t npairs = a.nkbN * (a.nkbN + 1) / 2;
+    {
+        const int64_t nkt = (a.rowsVT + 63) / 64;
+        for (int64_t b = blockIdx.x; b < a.nkbN * nkt; b += gridDim.x)
+            pack_vtq_tile<256>(a.V, a.N, a.r, a.rowsVT, a.nkbN, a.vcol, a.VTQ, b / nkt, (b % nkt) * 64, tile0, t);
+    }
+    if (!stopped) {
+        int slot = 0;
+        for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++slot) {
+            int64_t I, J;
+            block_pair(pr, I, J);
+            float(*tile)[kPtW + 1] = reinterpret_cast<float(*)[kPtW + 1]>(smem_tiles + slot * kPtW * (kPtW + 1));
+            const uint32_t* p0 = a.pt + pt_entry(I * kPtW, J * kPtW);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = (u * 256 + t) * 4;
+                const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + e));
+                float* d = &tile[e >> 6][e & 63];
+                d[0] = k.x != kInvalidRank ? a.res[k.x] : 0.f;
+                d[1] = k.y != kInvalidRank ? a.res[k.y] : 0.f;
+                d[2] = k.z != kInvalidRank ? a.res[k.z] : 0.f;
+                d[3] = k.w != kInvalidRank ? a.res[k.w] : 0.f;
+            }
+            __syncthreads();
+            const int line = t >> 2, part = t & 3;
+            float mr = 0.f, mc = 0.f;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                mr = fmaxf(mr, fabsf(tile[line][part * 16 + e]));
+                mc = fmaxf(mc, fabsf(tile[part * 16 + e][line]));
+            }
+            mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 1));
+            mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 2));
+            mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, 1));
+            mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, 2));
+            if (part == 0) {
+                if (mr > 0.f) atomicMax(a.rrow + I * kPtW + line, __float_as_uint(mr));
+                if (I != J && mc > 0.f) atomicMax(a.rrow + J * kPtW + line, __float_as_uint(mc));
+            }
+        }
+    }
+    for (int64_t e = gtid; e < a.M / 4; e += gstride) reinterpret_cast<float4*>(a.coef)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t e = (a.M / 4) * 4 + gtid; e < a.M; e += gstride) a.coef[e] = 0.f;
+    if (stopped) return;  // grid-uniform: every block leaves before the barrier
+    MID_MARK(3);
+    grid.sync();
+    MID_MARK(4);
+    // ---- C: slice the held blocks
+    int slot = 0;
+    for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++slot) {
+        int64_t I, J;
+        block_pair(pr, I, J);
+        const float(*tile)[kPtW + 1] = reinterpret_cast<const float(*)[kPtW + 1]>(smem_tiles + slot * kPtW * (kPtW + 1));
+        const int rr = t >> 2, c = t & 3;
+        float x[16];
+        uint4 q[3];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[e] = tile[rr][c * 16 + e];
+        slice16(x, slice_scale(a.rrow[I * kPtW + rr]), q);
+        store_q16(a.RQ, J, I * kPtW + rr, c, a.nkbN, a.Np, q);
+        if (I != J) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = tile[c * 16 + e][rr];
+            slice16(x, slice_scale(a.rrow[J * kPtW + rr]), q);
+            store_q16(a.RQ, I, J * kPtW + rr, c, a.nkbN, a.Np, q);
+        }
+    }
+    MID_MARK(5);
+#ifdef SOS_EXPERIMENTS
+    if (a.trace && blockIdx.x == 0 && t == 0)
+        printf("k_mid block0 (us): A %.2f | sync %.2f | B %.2f | sync %.2f | C %.2f\n", (tmark[1] - tmark[0]) * 1e-3,
+               (tmark[2] - tmark[1]) * 1e-3, (tmark[3] - tmark[2]) * 1e-3, (tmark[4] - tmark[3]) * 1e-3,
+               (tmark[5] - tmark[4]) * 1e-3);
+#endif
+}
+
+// cooperative grid of k_mid: no more blocks than work items of its largest phase
+// (a grid barrier costs more with more blocks), at most 4 per SM, and every
+// block must hold ceil(npairs / grid) R blocks in shared memory; returns the grid
+// (blocks) and sets the tiles per block
+int mid_grid_for(int64_t nkbN, int64_t rowsVT, int64_t M, int num_sms, int* tiles_per_block) {
+    const int64_t npairs = nkbN * (nkbN + 1) / 2;
+    const int64_t work = std::max<int64_t>({npairs, nkbN * ((rowsVT + 63) / 64), (M + 1023) / 1024, 1});
+    int tpb = 1, grid = num_sms;
+    for (int it = 0; it < 8; ++it) {
+        const size_t smem = (size_t)tpb * kMidTileBytes;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_mid, kMidThreads, smem) != cudaSuccess || nb < 1) {
+            cudaGetLastError();
+            nb = 1;
+        }
+        grid = (int)std::min<int64_t>(work, (int64_t)num_sms * std::min(nb, 4));
+        const int need = (int)((npairs + grid - 1) / grid);
+        if (need <= tpb) break;
+        tpb = need;
+    }
+    *tiles_per_block = tpb;
+    return grid;
+}
+
+void launch_mid(Plan& P, const float* p, const float* V, unsigned* vcol, bool colmax, unsigned* zero_cols,
+                double* losses, bool losses_from_opt, cudaStream_t st) {
+    LaunchScope ls(P, KK_MID, st);
+    MidArgs a;
+    a.coef = P.d_coef;
+    a.p = p;
+    a.res = P.d_res;
+    a.M = P.idx->M;
+    a.sc = P.d_scal;
+    a.opt = P.d_opt;
+    a.losses = losses;
+    a.losses_from_opt = losses_from_opt ? 1 : 0;
+    a.pt = P.idx->d_pt;
+    a.Np = P.idx->Np;
+    a.nkbN = P.nkbN;
+    a.rrow = P.d_rrow;
+    a.RQ = P.d_rq;
+    a.V = V;
+    a.N = P.idx->N;
+    a.r = P.r;
+    a.rowsVT = P.rowsVT;
+    a.vcol = vcol;
+    a.colmax = colmax ? 1 : 0;
+    a.VTQ = P.d_vtq;
+    a.zero_cols = zero_cols;
+    a.trace = 0;
+#ifdef SOS_EXPERIMENTS
+    {
+        const char* e = getenv("SOS_MID_TRACE");
+        a.trace = e && atoi(e) ? 1 : 0;
+    }
+#endif
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P.mid_grid);
+    cfg.blockDim = dim3(kMidThreads);
+    cfg.dynamicSmemBytes = (size_t)P.mid_tiles * kMidTileBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_mid, a);
 }
 
 void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt, unsigned* zero0, int64_t n0,
-                       unsigned* zero1, int64_t n1, float* zero_coef) {
+                       unsigned* zero1, int64_t n1, float* zero_coef, bool zero_rrow) {
     LaunchScope ls(P, KK_UPDATE, st);
     const int64_t nc = zero_coef ? P.idx->M : 0;
-    const int blocks = zero0 || zero1 || zero_coef ? grid_for(P, std::max<int64_t>(n0 + n1, nc / 4), 256, 4) : 1;
+    const int64_t n2 = zero_rrow ? P.idx->Np : 0;
+    if (!zero0) n0 = 0;
+    if (!zero1) n1 = 0;
+    const int64_t nz = n0 + n1 + n2;
+    const int blocks = nz || nc ? grid_for(P, std::max<int64_t>(nz, nc / 4), 256, 4) : 1;
     k_step_begin<<<blocks, 256, 0, st>>>(P.d_opt, P.d_scal, losses_from_opt ? nullptr : losses, losses_from_opt ? 1 : 0,
-                                         zero0, zero0 ? n0 : 0, zero1, zero1 ? n1 : 0, zero_coef, nc);
+                                         zero0, n0, zero1, n1, P.d_rrow, n2, zero_coef, nc);
 }
 
 // maxima (one read of V) + VQ (one elementwise pass)
@@ -480,7 +784,7 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, uns
 // Small problems and many variables favour the direct pass (config 2: 60 -> 14
 // us; N = 5050 quartic: 100 -> 32 us); config 4 the DP (0.33 vs 0.46 ms); config
 // 3 is even (0.178 / 0.175 ms).  Rates fitted to those measurements.
-static bool rmax_direct_is_cheaper(const Index& ix) {
+bool rmax_direct_default(const Index& ix) {
     double lookups = 0;
     for (int D = ix.d; D <= 2 * ix.d - 1; ++D) lookups += (double)rmax_level_count(ix.n, D) * ix.n;
     const double dp_us = 12.0 * ix.d + lookups / 2e5;
@@ -488,10 +792,9 @@ static bool rmax_direct_is_cheaper(const Index& ix) {
     return direct_us < dp_us;
 }
 
-void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop) {
-    static const char* tp_env = getenv("SOS_RPACK_TWOPASS");
-    if (tp_env ? atoi(tp_env) != 0 : rmax_direct_is_cheaper(*P.idx)) {
-        launch_rmax(P, res, st, use_stop);
+void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop, bool rrow_zeroed) {
+    if (P.rmax_direct) {
+        launch_rmax(P, res, st, use_stop, rrow_zeroed);
     } else {
         LaunchScope ls(P, KK_ABSMAX_R, st);
         launch_rmax_dp(*P.idx, res, P.d_rlev, P.d_rrow, st, P.d_scal, P.d_opt, use_stop);

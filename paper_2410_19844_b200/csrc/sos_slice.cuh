@@ -43,6 +43,23 @@ __device__ __forceinline__ void slice16(const float* v, float c, uint4 (&q)[3]) 
     for (int s = 0; s < 3; ++s) q[s] = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
 }
 
+// 4 consecutive K-values of one row -> one 4-byte word per slice (the same digits
+// as slice16; word w of a 16-byte chunk holds K-values 4w .. 4w+3)
+__device__ __forceinline__ void slice4(const float* v, float c, uint32_t (&q)[3]) {
+    int d3[4], d2[4], d1[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int x = __float2int_rn(v[e] * c);
+        const int x2 = (x + 128) >> 8;
+        d3[e] = x;
+        d2[e] = x2;
+        d1[e] = (x2 + 128) >> 8;
+    }
+    q[2] = __byte_perm(__byte_perm(d3[0], d3[1], 0x0040), __byte_perm(d3[2], d3[3], 0x0040), 0x5410);
+    q[1] = __byte_perm(__byte_perm(d2[0], d2[1], 0x0040), __byte_perm(d2[2], d2[3], 0x0040), 0x5410);
+    q[0] = __byte_perm(__byte_perm(d1[0], d1[1], 0x0040), __byte_perm(d1[2], d1[3], 0x0040), 0x5410);
+}
+
 // byte offset of chunk c (16 K-values) of row `row`, K-block kb, slice s in a Q-layout
 __device__ __forceinline__ int64_t q_offset(int s, int64_t kb, int64_t row, int c, int64_t nkb, int64_t rows_total) {
     return ((s * nkb + kb) * rows_total + row) * 64 + ((c ^ (int)((row >> 1) & 3)) << 4);
@@ -56,33 +73,48 @@ __device__ __forceinline__ void store_q16(uint8_t* base, int64_t kb, int64_t row
 
 // VTQ row k (a column of V), K = j (a row of V): a 64 (j) x 64 (k) tile of V is
 // transposed through shared memory; thread (k, chunk c) writes 16 j's.  Used by
-// k_pack_vtq and by the aux warps of the forward GEMM (named barrier 1).
+// k_pack_vtq, k_mid (kThreads = 256, __syncthreads) and by the aux warps of the
+// forward GEMM (kThreads = 64, named barrier 1).  The tile's loads are unrolled
+// so that they are all in flight together.
+template <int kThreads>
 __device__ __forceinline__ void pack_vtq_tile(const float* __restrict__ V, int64_t N, int64_t r, int64_t rowsVT,
                                               int64_t nkbN, const unsigned* __restrict__ vcol,
                                               uint8_t* __restrict__ VTQ, int64_t jb, int64_t k0,
-                                              float (*tile)[65], int t, int nthreads) {
+                                              float (*tile)[65], int t) {
     const int64_t j0 = jb * 64;
-    for (int e = t; e < 64 * 64; e += nthreads) {
-        const int jj = e >> 6, kk = e & 63;
-        const int64_t j = j0 + jj, k = k0 + kk;
-        tile[jj][kk] = (j < N && k < r) ? __ldg(V + j * r + k) : 0.f;
+    constexpr int kLoads = 64 * 64 / kThreads;
+    float x[kLoads < 16 ? kLoads : 16];
+#pragma unroll
+    for (int b0 = 0; b0 < kLoads; b0 += 16) {
+#pragma unroll
+        for (int u = 0; u < 16 && b0 + u < kLoads; ++u) {
+            const int e = t + (b0 + u) * kThreads;
+            const int jj = e >> 6, kk = e & 63;
+            const int64_t j = j0 + jj, k = k0 + kk;
+            x[u] = (j < N && k < r) ? V[j * r + k] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 16 && b0 + u < kLoads; ++u) {
+            const int e = t + (b0 + u) * kThreads;
+            tile[e >> 6][e & 63] = x[u];
+        }
     }
-    if (nthreads == 256) __syncthreads();
-    else asm volatile("bar.sync 1, %0;" ::"r"(nthreads));
-    for (int e = t; e < 64 * 4; e += nthreads) {
+    if (kThreads == 256) __syncthreads();
+    else asm volatile("bar.sync 1, %0;" ::"n"(kThreads));
+    for (int e = t; e < 64 * 4; e += kThreads) {
         const int kk = e >> 2, c = e & 3;
         const int64_t k = k0 + kk;
         if (k >= rowsVT) continue;
         const float sc = k < r ? slice_scale(__ldg(vcol + k)) : 0.f;
-        float x[16];
+        float xs[16];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) x[u] = tile[c * 16 + u][kk];
+        for (int u = 0; u < 16; ++u) xs[u] = tile[c * 16 + u][kk];
         uint4 q[3];
-        slice16(x, sc, q);
+        slice16(xs, sc, q);
         store_q16(VTQ, jb, k, c, nkbN, rowsVT, q);
     }
-    if (nthreads == 256) __syncthreads();
-    else asm volatile("bar.sync 1, %0;" ::"r"(nthreads));
+    if (kThreads == 256) __syncthreads();
+    else asm volatile("bar.sync 1, %0;" ::"n"(kThreads));
 }
 
 }  // namespace sos

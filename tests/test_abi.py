@@ -41,7 +41,7 @@ def test_binding_covers_every_declared_symbol():
 
 def test_version_and_error_without_device(lib):
     lib.sos_version.restype = ctypes.c_int
-    assert lib.sos_version() == 1
+    assert lib.sos_version() == 2
     lib.sos_last_error.restype = ctypes.c_char_p
     import torch
     if torch.cuda.is_available():
@@ -73,3 +73,13 @@ def test_product_package_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 for bad in ("import oracle", "from oracle", "sos_oracle", "or_index_create"):
                     assert bad not in txt, (f, bad)
+
+
+def test_release_library_reads_no_tuning_environment(lib):
+    """No environment variable can change what the shipped library computes:
+    the experiment switches (SOS_GEMM_PROBE, SOS_SKEW_*, ...) exist only in a
+    -DSOS_EXPERIMENTS build; implementation variants are sos_plan_opts."""
+    from paper_2410_19844_b200 import build
+    blob = open(build.LIB, "rb").read()
+    assert b"SOS_" not in blob
+    assert hasattr(lib, "sos_plan_create_ex")

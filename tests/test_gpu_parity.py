@@ -589,23 +589,23 @@ def test_zero_rows_and_columns(sos):
 
 # -------------------------------------------------------------- sos_descend --
 
-@pytest.mark.parametrize("vtq_update", ["0", "1"])
+@pytest.mark.parametrize("variant", ["split", "fused_vtq_update"])
 @pytest.mark.parametrize("kind,lr,r", [("adam", 1e-3, 330), ("gd", 5e-3, 330), ("adam", 1e-3, 336)])
-def test_descend_matches_steps(sos, kind, lr, r, vtq_update, monkeypatch):
+def test_descend_matches_steps(sos, kind, lr, r, variant):
     """sos_descend (slices of V_{t+1} written by the update of step t) follows
     the same iteration as repeated sos_step calls, to the slice precision.
     Row 5 and column 9 of V0 are zero, so their first update leaves the
-    headroom window and is re-sliced by the fixup kernels (VQ row, VTQ row).
-    r = 336 (a multiple of 4) and r = 330 (rows not 16-byte aligned).
-    vtq_update = 1 forces the fused update that also writes the next step's
-    V^T slices (the default only for long K); vtq_update = 0 runs the split
-    update (gradient stored, all-SM k_update: the default for short K)."""
-    monkeypatch.setenv("SOS_VTQ_UPDATE", vtq_update)  # read at plan creation
-    monkeypatch.setenv("SOS_UPDATE_SPLIT", "0" if vtq_update == "1" else "1")  # both update paths
+    headroom window of the fused variant and is re-sliced by the fixup kernels
+    (VQ row, VTQ row).  r = 336 (a multiple of 4) and r = 330 (rows not 16-byte
+    aligned).  "fused_vtq_update": the update in the backward's epilogue warps
+    also writes the next step's V^T slices (the default only for long K);
+    "split": forward, k_mid, backward storing the gradient, row-block update
+    with exact next-step scales (the default for short K)."""
+    opts = {"split": True} if variant == "split" else {"split": False, "vtq_from_update": True}
     c = si.CONFIGS["c1_n8_2d8"]
     o = oracle(c.n, c.d)
     ix = sos.SosIndex(c.n, c.d)
-    plan = sos.SosPlan(ix, r)
+    plan = sos.SosPlan(ix, r, **opts)
     p = torch.from_numpy(o.forward(si.planted_w(o.N, c.r_star, 0)).astype(np.float32)).cuda()
     V0 = si.v0(o.N, r, 0)
     V0[5] = 0.0

@@ -1,79 +1,107 @@
-"""Implementation variants chosen by the plan (or forced by environment
-switches, read once per process, hence subprocesses) must agree:
+"""Implementation variants of a plan (sos_plan_opts, include/sos_b200.h) must
+compute the same step:
 
 * R row maxima by the lattice DP vs the direct gather pass: same maxima, so the
   same R slices and a bit-identical backward;
 * V^T slices from the forward's aux warps vs the all-SM pack kernel: same bytes,
   bit-identical backward inside the descent;
-* next-step V^T slices from the backward's update vs packed by the forward,
-  and the fused update vs the split one (gradient stored, all-SM k_update):
-  the descent agrees to the slice precision;
+* next-step V^T slices from the backward's update vs packed by the forward;
+* the split step (forward, cooperative k_mid, backward storing the gradient,
+  row-block update with exact next-step scales) vs the fused one (update in the
+  backward's epilogue warps, headroom scales + fixups): the descent agrees to
+  the slice precision;
 * narrow tiles vs full 160-wide grid tiles: the same integer products, so a
   bit-identical plain backward; the descent (forward atomics in another order)
   agrees to fp32 rounding.
 """
-import os
-import subprocess
-import sys
-
 import numpy as np
 import pytest
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SHAPE = ("9", "4", "700")  # N = 495: several tiles, a narrow last column block (700 = 4*160 + 60)
+import seeded_inputs as si
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+SHAPE = (9, 4, 700)  # N = 495: several tiles, a narrow last column block (700 = 4*160 + 60)
 
 
-def _run(tmp_path, tag, env):
-    out = str(tmp_path / f"{tag}.npz")
-    e = dict(os.environ)
-    e.update(env)
-    subprocess.run([sys.executable, os.path.join(ROOT, "tools", "variant_grad.py"), *SHAPE, out], env=e,
-                   check=True, timeout=300)
-    return np.load(out)
+@pytest.fixture(scope="module")
+def sos():
+    import paper_2410_19844_b200 as m
+    m.load()
+    return m
 
 
-@pytest.mark.gpu
-def test_rmax_dp_vs_direct(tmp_path):
-    a = _run(tmp_path, "dp", {"SOS_RPACK_TWOPASS": "0"})
-    b = _run(tmp_path, "direct", {"SOS_RPACK_TWOPASS": "1"})
-    assert np.array_equal(a["grad"], b["grad"])
+@pytest.fixture(scope="module")
+def ix(sos):
+    n, d, _ = SHAPE
+    return sos.SosIndex(n, d)
 
 
-@pytest.mark.gpu
-def test_vtq_aux_vs_kernel(tmp_path):
-    a = _run(tmp_path, "aux", {"SOS_VTQ_AUX": "1"})
-    b = _run(tmp_path, "kernel", {"SOS_VTQ_AUX": "0"})
-    assert np.array_equal(a["grad"], b["grad"])
-    rel = np.linalg.norm(a["V3"] - b["V3"]) / np.linalg.norm(a["V3"])
-    assert rel <= 1e-6
+def _run(sos, ix, **opts):
+    r = SHAPE[2]
+    plan = sos.SosPlan(ix, r, **opts)
+    V = torch.from_numpy(si.v0(ix.N, r, seed=11)).cuda()
+    res = torch.from_numpy(si.residual_probe(ix.M, seed=12)).cuda()
+    g = plan.backward(V, res).cpu().numpy()
+    W = torch.zeros(ix.N, r, device="cuda")
+    W[:, : r // 2] = torch.from_numpy(si.planted_w(ix.N, r // 2, 13)).cuda()
+    p = plan.forward(W)
+    plan.opt_init("adam", 1e-3)
+    V3 = V.clone()
+    losses = plan.descend(V3, p, 3).cpu().numpy()
+    out = {"grad": g, "V3": V3.cpu().numpy(), "losses": losses, "dV": V3.cpu().numpy() - V.cpu().numpy()}
+    plan.close()
+    return out
+
+
+def _same_descent(a, b, tol=1e-5):
+    """3 Adam steps: V_3 within 1e-6 (relative L2), the update V_3 - V_0
+    within tol, the losses within 1e-5."""
+    assert np.linalg.norm(a["V3"] - b["V3"]) / np.linalg.norm(a["V3"]) <= 1e-6
+    rel = np.linalg.norm(a["dV"] - b["dV"]) / np.linalg.norm(a["dV"])
+    assert rel <= tol, rel
     assert np.allclose(a["losses"], b["losses"], rtol=1e-5)
 
 
-@pytest.mark.gpu
-def test_narrow_vs_full_tiles(tmp_path):
-    a = _run(tmp_path, "narrow", {"SOS_NARROW_TILES": "1"})
-    b = _run(tmp_path, "full", {"SOS_NARROW_TILES": "0"})
+def test_rmax_dp_vs_direct(sos, ix):
+    a = _run(sos, ix, rmax_direct=False, split=False)
+    b = _run(sos, ix, rmax_direct=True, split=False)
     assert np.array_equal(a["grad"], b["grad"])
-    rel = np.linalg.norm(a["V3"] - b["V3"]) / np.linalg.norm(a["V3"])
-    assert rel <= 1e-6
-    assert np.allclose(a["losses"], b["losses"], rtol=1e-5)
+    _same_descent(a, b)
 
 
-@pytest.mark.gpu
-def test_vtq_from_update_vs_forward_pack(tmp_path):
-    a = _run(tmp_path, "upd", {"SOS_VTQ_UPDATE": "1", "SOS_UPDATE_SPLIT": "0"})
-    b = _run(tmp_path, "fwd", {"SOS_VTQ_UPDATE": "0", "SOS_UPDATE_SPLIT": "0"})
+def test_vtq_aux_vs_kernel(sos, ix):
+    a = _run(sos, ix, vtq_in_aux=True, split=False, vtq_from_update=False)
+    b = _run(sos, ix, vtq_in_aux=False, split=False, vtq_from_update=False)
+    assert np.array_equal(a["grad"], b["grad"])
+    _same_descent(a, b)
+
+
+def test_narrow_vs_full_tiles(sos, ix):
+    a = _run(sos, ix, narrow_tiles=True)
+    b = _run(sos, ix, narrow_tiles=False)
+    assert np.array_equal(a["grad"], b["grad"])
+    _same_descent(a, b)
+
+
+def test_vtq_from_update_vs_forward_pack(sos, ix):
+    a = _run(sos, ix, split=False, vtq_from_update=True)
+    b = _run(sos, ix, split=False, vtq_from_update=False)
     assert np.array_equal(a["grad"], b["grad"])  # sos_backward does not use it
-    rel = np.linalg.norm(a["V3"] - b["V3"]) / np.linalg.norm(a["V3"])
-    assert rel <= 1e-6
-    assert np.allclose(a["losses"], b["losses"], rtol=1e-5)
+    _same_descent(a, b)
 
 
-@pytest.mark.gpu
-def test_update_fused_vs_split(tmp_path):
-    a = _run(tmp_path, "fused", {"SOS_UPDATE_SPLIT": "0"})
-    b = _run(tmp_path, "split", {"SOS_UPDATE_SPLIT": "1"})
+def test_split_vs_fused_step(sos, ix):
+    a = _run(sos, ix, split=True)
+    b = _run(sos, ix, split=False)
     assert np.array_equal(a["grad"], b["grad"])
-    rel = np.linalg.norm(a["V3"] - b["V3"]) / np.linalg.norm(a["V3"])
-    assert rel <= 1e-6
-    assert np.allclose(a["losses"], b["losses"], rtol=1e-5)
+    # the split step slices V_{t+1} against its exact row maxima, the fused one
+    # against 2x the old maximum: both ~22-23 bits
+    _same_descent(a, b)
+
+
+def test_plan_options_validated(sos, ix):
+    with pytest.raises(sos.SosError):
+        sos.SosPlan(ix, 8, bogus=True)

@@ -1,16 +1,21 @@
 """Device time per descent step for an arbitrary (n, d, r) (planted target, Adam):
-python tools/time_shape.py n d r [steps]"""
+python tools/time_shape.py n d r [steps] [--kernels] [split=0|1 rmax_direct=0|1 ...]
+(key=value arguments are sos_plan_opts fields, for same-box A/B runs)"""
 import os, sys
 import numpy as np
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import seeded_inputs as si
 import paper_2410_19844_b200 as sos
+if "--exp" in sys.argv:  # the -DSOS_EXPERIMENTS build (environment switches, probes, traces)
+    from paper_2410_19844_b200 import build as _b
+    sos.load(_b.build(experiments=True))
 
 n, d, r = (int(x) for x in sys.argv[1:4])
-steps = int(sys.argv[4]) if len(sys.argv) > 4 else 20
+steps = int(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4].isdigit() else 20
+opts = {k: bool(int(v)) for k, v in (a.split("=") for a in sys.argv[4:] if "=" in a)}
 ix = sos.SosIndex(n, d)
-plan = sos.SosPlan(ix, r)
+plan = sos.SosPlan(ix, r, **opts)
 rs = max(1, ix.N // 2)
 W = torch.zeros(ix.N, r, device="cuda")
 W[:, : min(r, rs)] = torch.from_numpy(si.planted_w(ix.N, min(r, rs), 1)).cuda()
@@ -25,7 +30,7 @@ plan.descend(V, p, steps)
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / steps
-print(f"n={n} d={d} N={ix.N} r={r} ms/step={ms:.3f} steps/s={1e3 / ms:.3f}")
+print(f"n={n} d={d} N={ix.N} r={r} {opts} ms/step={ms:.4f} steps/s={1e3 / ms:.1f}")
 if "--kernels" in sys.argv:  # per-kernel split (plain launches with events, a few extra us each)
     plan.timing(True)
     plan.descend(V, p, 10)

@@ -148,14 +148,17 @@ class OracleIndex:
         lib().or_forward(self._h, _ptr(V), V.shape[1], _ptr(out))
         return out
 
-    def forward_threaded(self, V, threads: int | None = None) -> np.ndarray:
+    def forward_threaded(self, V, threads: int | None = None, rows: tuple | None = None) -> np.ndarray:
         """forward() with the pair loop's rows split over host threads
         (or_forward_rows per row range; the ctypes calls release the GIL).
-        Equal to forward() up to the order of the fp64 additions."""
+        Equal to forward() up to the order of the fp64 additions.  rows=(i0, i1)
+        restricts the loop to those rows (a partial sum; bench.py times it)."""
         V = _f64(V)
         assert V.shape[0] == self.N
-        T = max(1, min(threads or host_threads(), self.N))
-        parts = _row_blocks(self.N, T)
+        i0, i1 = rows if rows is not None else (0, self.N)
+        T = max(1, min(threads or host_threads(), i1 - i0))
+        block = max(1, min(16, (i1 - i0) // (2 * T)))  # >= 2 blocks per thread when the range allows
+        parts = [[(a + i0, b + i0) for a, b in part] for part in _row_blocks(i1 - i0, T, block)]
 
         def work(blocks):
             acc = np.zeros(self.M, dtype=np.float64)

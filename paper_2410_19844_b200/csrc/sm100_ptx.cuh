@@ -26,9 +26,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -49,19 +46,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// 32 lanes x 32 consecutive 32-bit columns; thread t of the warp gets lane (base+t)
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
-          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
-          "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-}
 // 32 lanes x 16 consecutive 32-bit columns
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile(
@@ -73,17 +57,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// UMMA shared-memory descriptor, K-major, 128-byte swizzle: rows of 128 B,
-// 8-row swizzle atoms of 1024 B stacked densely (SBO = 1024 B), version 1.
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;  // SBO
-    d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;            // SWIZZLE_128B
-    return d;
-}
 
 // UMMA shared-memory descriptor, K-major, 64-byte swizzle: rows of 64 B,
 // 8-row swizzle atoms of 512 B stacked densely (SBO = 512 B), version 1.
@@ -98,10 +71,6 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) {
     return d;
 }
 
-// instruction descriptor: kind::f16, A=B=F16, D=F32, both K-major, M x N
-__host__ __device__ constexpr uint32_t umma_idesc_f16_f32(int M, int N) {
-    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
 // instruction descriptor: kind::i8, A=B=signed int8, D=S32, both K-major, M x N
 __host__ __device__ constexpr uint32_t umma_idesc_s8_s32(int M, int N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -154,18 +123,9 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
     }
 }
 
-// 2-D TMA tensor load for a CTA pair: bytes land in this CTA's shared memory,
-// completion is signalled on the LEADER CTA's mbarrier (peer bit cleared).
-__device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const void* tmap, uint64_t* bar, int32_t c0,
-                                                int32_t c1) {
-    const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
-        "l"(tmap), "r"(mbar), "r"(c0), "r"(c1)
-        : "memory");
-}
-// 3-D variant (inner bytes, rows, slice plane)
+// 3-D TMA tensor load for a CTA pair (inner bytes, rows, slice plane): bytes land
+// in this CTA's shared memory, completion is signalled on the LEADER CTA's mbarrier
+// (peer bit cleared)
 __device__ __forceinline__ void tma_load_3d_2sm(void* smem_dst, const void* tmap, uint64_t* bar, int32_t c0,
                                                 int32_t c1, int32_t c2) {
     const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
@@ -186,15 +146,6 @@ __device__ __forceinline__ void tmem_alloc_2sm(uint32_t* slot_smem, uint32_t nco
 }
 __device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr, uint32_t ncols) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
-}
-// D (+)= A * B^T for the CTA pair, M = 256 (128 rows per CTA), issued by the leader
-__device__ __forceinline__ void umma_f16_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                             uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 // D (+)= A * B^T on int8 operands, s32 accumulate (exact), M = 256 over the pair, K = 32.
 // kColl = A-operand collector usage: 0 none, 1 fill (read A and keep it), 2 use

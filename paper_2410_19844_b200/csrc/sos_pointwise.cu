@@ -512,6 +512,7 @@ struct MidArgs {
     int colmax;
     uint8_t* VTQ;
     unsigned* zero_cols;
+    int hold;   // every block holds its R blocks from phase B to C (else C gathers them again)
     int trace;  // experiment build only
 };
 
@@ -525,6 +526,25 @@ __device__ __forceinline__ void block_pair(int64_t pr, int64_t& I, int64_t& J) {
 
 constexpr int kMidThreads = 256;
 constexpr size_t kMidTileBytes = (size_t)kPtW * (kPtW + 1) * sizeof(float);
+constexpr int kMidMaxHeld = 12;  // R blocks a k_mid block can hold in shared memory (~200 KB)
+
+// the 64 x 64 block {I <= J} of R (I's rows x J's columns) gathered through the
+// stored PT block into a padded shared-memory tile (plain loads: res is written
+// in the same kernel)
+__device__ __forceinline__ void gather_r_tile(const uint32_t* __restrict__ pt, const float* res, int64_t I, int64_t J,
+                                              float (*tile)[kPtW + 1], int t) {
+    const uint32_t* p0 = pt + pt_entry(I * kPtW, J * kPtW);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int e = (u * 256 + t) * 4;
+        const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + e));
+        float* d = &tile[e >> 6][e & 63];
+        d[0] = k.x != kInvalidRank ? res[k.x] : 0.f;
+        d[1] = k.y != kInvalidRank ? res[k.y] : 0.f;
+        d[2] = k.z != kInvalidRank ? res[k.z] : 0.f;
+        d[3] = k.w != kInvalidRank ? res[k.w] : 0.f;
+    }
+}
 
 #ifdef SOS_EXPERIMENTS
 // SOS_MID_TRACE=1 (experiment build): block 0 prints the phase boundaries of k_mid
@@ -617,18 +637,9 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
         for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++slot) {
             int64_t I, J;
             block_pair(pr, I, J);
-            float(*tile)[kPtW + 1] = reinterpret_cast<float(*)[kPtW + 1]>(smem_tiles + slot * kPtW * (kPtW + 1));
-            const uint32_t* p0 = a.pt + pt_entry(I * kPtW, J * kPtW);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = (u * 256 + t) * 4;
-                const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + e));
-                float* d = &tile[e >> 6][e & 63];
-                d[0] = k.x != kInvalidRank ? a.res[k.x] : 0.f;
-                d[1] = k.y != kInvalidRank ? a.res[k.y] : 0.f;
-                d[2] = k.z != kInvalidRank ? a.res[k.z] : 0.f;
-                d[3] = k.w != kInvalidRank ? a.res[k.w] : 0.f;
-            }
+            float(*tile)[kPtW + 1] =
+                a.hold ? reinterpret_cast<float(*)[kPtW + 1]>(smem_tiles + slot * kPtW * (kPtW + 1)) : tile0;
+            gather_r_tile(a.pt, a.res, I, J, tile, t);
             __syncthreads();
             const int line = t >> 2, part = t & 3;
             float mr = 0.f, mc = 0.f;
@@ -645,6 +656,7 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
                 if (mr > 0.f) atomicMax(a.rrow + I * kPtW + line, __float_as_uint(mr));
                 if (I != J && mc > 0.f) atomicMax(a.rrow + J * kPtW + line, __float_as_uint(mc));
             }
+            if (!a.hold) __syncthreads();  // tile0 is reused by the next block pair
         }
     }
     for (int64_t e = gtid; e < a.M / 4; e += gstride) reinterpret_cast<float4*>(a.coef)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -653,12 +665,17 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
     MID_MARK(3);
     grid.sync();
     MID_MARK(4);
-    // ---- C: slice the held blocks
+    // ---- C: slice the held blocks (or, when they do not fit, gather them again)
     int slot = 0;
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++slot) {
         int64_t I, J;
         block_pair(pr, I, J);
-        const float(*tile)[kPtW + 1] = reinterpret_cast<const float(*)[kPtW + 1]>(smem_tiles + slot * kPtW * (kPtW + 1));
+        float(*tile)[kPtW + 1] =
+            a.hold ? reinterpret_cast<float(*)[kPtW + 1]>(smem_tiles + slot * kPtW * (kPtW + 1)) : tile0;
+        if (!a.hold) {
+            gather_r_tile(a.pt, a.res, I, J, tile, t);
+            __syncthreads();
+        }
         const int rr = t >> 2, c = t & 3;
         float x[16];
         uint4 q[3];
@@ -672,6 +689,7 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
             slice16(x, slice_scale(a.rrow[J * kPtW + rr]), q);
             store_q16(a.RQ, I, J * kPtW + rr, c, a.nkbN, a.Np, q);
         }
+        if (!a.hold) __syncthreads();
     }
     MID_MARK(5);
 #ifdef SOS_EXPERIMENTS
@@ -684,25 +702,31 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
 
 // cooperative grid of k_mid: no more blocks than work items of its largest phase
 // (a grid barrier costs more with more blocks), at most 4 per SM, and every
-// block must hold ceil(npairs / grid) R blocks in shared memory; returns the grid
-// (blocks) and sets the tiles per block
+// block holds ceil(npairs / grid) R blocks in shared memory -- or, when that
+// exceeds kMidMaxHeld (long K), one block at a time with phase C gathering
+// again (tiles_per_block = 0).  Returns the grid (blocks).
 int mid_grid_for(int64_t nkbN, int64_t rowsVT, int64_t M, int num_sms, int* tiles_per_block) {
     const int64_t npairs = nkbN * (nkbN + 1) / 2;
     const int64_t work = std::max<int64_t>({npairs, nkbN * ((rowsVT + 63) / 64), (M + 1023) / 1024, 1});
-    int tpb = 1, grid = num_sms;
-    for (int it = 0; it < 8; ++it) {
-        const size_t smem = (size_t)tpb * kMidTileBytes;
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto grid_for_smem = [&](size_t smem) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int nb = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_mid, kMidThreads, smem) != cudaSuccess || nb < 1) {
             cudaGetLastError();
             nb = 1;
         }
-        grid = (int)std::min<int64_t>(work, (int64_t)num_sms * std::min(nb, 4));
+        return (int)std::min<int64_t>(work, (int64_t)num_sms * std::min(nb, 4));
+    };
+    int tpb = 1, grid = grid_for_smem(kMidTileBytes);
+    for (int it = 0; it < 8; ++it) {
         const int need = (int)((npairs + grid - 1) / grid);
         if (need <= tpb) break;
+        if (need > kMidMaxHeld) {  // R does not fit: hold nothing
+            *tiles_per_block = 0;
+            return grid_for_smem(kMidTileBytes);
+        }
         tpb = need;
+        grid = grid_for_smem((size_t)tpb * kMidTileBytes);
     }
     *tiles_per_block = tpb;
     return grid;
@@ -743,7 +767,8 @@ void launch_mid(Plan& P, const float* p, const float* V, unsigned* vcol, bool co
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(P.mid_grid);
     cfg.blockDim = dim3(kMidThreads);
-    cfg.dynamicSmemBytes = (size_t)P.mid_tiles * kMidTileBytes;
+    a.hold = P.mid_tiles > 0 ? 1 : 0;
+    cfg.dynamicSmemBytes = (size_t)std::max(P.mid_tiles, 1) * kMidTileBytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;

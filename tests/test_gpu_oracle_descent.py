@@ -40,15 +40,18 @@ def long_k(sos):
     n, d, r = 20, 4, 200   # r = 160 + 40: a full and a narrow column tile
     o = OracleIndex(n, d)
     ix = sos.SosIndex(n, d)
-    plan = sos.SosPlan(ix, r)
+    plan = sos.SosPlan(ix, r)                # default at this size: fused update, V^T slices from it
+    plan_split = sos.SosPlan(ix, r, split=True)  # the split step forced (k_mid re-gathers R)
     W = si.planted_w(o.N, 32, seed=6)
     p = o.forward_threaded(W).astype(np.float32)      # planted target, by the oracle
     V0 = si.v0(o.N, r, seed=7)
     # Adam first: its recorded first gradient also sets the GD step below
     g_adam = []
     Vs_adam, L_adam = o.descent_threaded(V0, p, "adam", 4, 1e-3, final_loss=False, grads_out=g_adam)
-    yield dict(o=o, ix=ix, plan=plan, p=p, V0=V0, adam=(Vs_adam, L_adam, g_adam))
+    yield dict(o=o, ix=ix, plans={"default": plan, "split": plan_split}, p=p, V0=V0,
+               adam=(Vs_adam, L_adam, g_adam))
     plan.close()
+    plan_split.close()
     ix.close()
 
 
@@ -59,13 +62,14 @@ def _gpu_descend(sos, plan, V0, p, kind, lr, steps):
     return Vd.cpu().numpy().astype(np.float64), losses
 
 
-def test_descend_long_k_adam_4_steps(sos, long_k):
+@pytest.mark.parametrize("variant", ["default", "split"])
+def test_descend_long_k_adam_4_steps(sos, long_k, variant):
     """4 Adam steps (lr 1e-3, bench.py's eps 1e-8) through sos_descend vs the
     oracle's Adam: V_4 - V_0 element-wise (rel. L2 <= 1e-4) and the losses
     L(V_0..V_3) (rel. <= 1e-5).  Adam's first step is ~lr sign(g_1); the few
     entries whose oracle g_1 is within 1e-5 rms of 0 may take either sign on
     the GPU (forward rounding), so they are compared for validity only."""
-    o, plan, p, V0 = long_k["o"], long_k["plan"], long_k["p"], long_k["V0"]
+    o, plan, p, V0 = long_k["o"], long_k["plans"][variant], long_k["p"], long_k["V0"]
     Vs, L, g = long_k["adam"]
     V4, losses = _gpu_descend(sos, plan, V0, p, "adam", 1e-3, 4)
     dv_o = Vs[4] - V0
@@ -73,24 +77,27 @@ def test_descend_long_k_adam_4_steps(sos, long_k):
     amb = np.abs(g[0]) < 1e-5 * np.sqrt(np.mean(g[0] ** 2))
     err = rel_l2(dv_g[~amb], dv_o[~amb])
     lerr = np.abs(losses - L[:4]) / L[:4]
-    print(f"long-K Adam: dV rel err {err:.2e} ({amb.sum()} ambiguous of {amb.size}); loss rel err {lerr.max():.2e}")
+    print(f"long-K Adam ({variant}): dV rel err {err:.2e} ({amb.sum()} ambiguous of {amb.size}); loss rel err {lerr.max():.2e}")
     assert err <= 1e-4
     assert amb.sum() <= 1e-5 * amb.size
     assert np.all(np.abs(dv_g[amb] - dv_o[amb]) <= 2 * 4 * 1e-3)
     assert np.all(lerr <= 1e-5)
 
 
-def test_descend_long_k_gd_4_steps(sos, long_k):
+@pytest.mark.parametrize("variant", ["default", "split"])
+def test_descend_long_k_gd_4_steps(sos, long_k, variant):
     """The same with plain GD (every gradient magnitude enters the update): lr
     sets the first step to 2 % of ||V_0||; V_4 - V_0 and the losses vs the oracle."""
-    o, plan, p, V0 = long_k["o"], long_k["plan"], long_k["p"], long_k["V0"]
+    o, plan, p, V0 = long_k["o"], long_k["plans"][variant], long_k["p"], long_k["V0"]
     g1 = long_k["adam"][2][0]  # the gradient at V_0 (same V_0 and p)
     lr = 0.02 * np.linalg.norm(V0) / np.linalg.norm(g1)
-    Vs, L = o.descent_threaded(V0, p, "gd", 4, lr, final_loss=False)
+    if "gd" not in long_k:
+        long_k["gd"] = o.descent_threaded(V0, p, "gd", 4, lr, final_loss=False)
+    Vs, L = long_k["gd"]
     V4, losses = _gpu_descend(sos, plan, V0, p, "gd", lr, 4)
     err = rel_l2(V4 - V0, Vs[4] - V0)
     lerr = np.abs(losses - L[:4]) / L[:4]
-    print(f"long-K GD lr={lr:.3g}: dV rel err {err:.2e}; losses {L[:4]} rel err {lerr.max():.2e}")
+    print(f"long-K GD ({variant}) lr={lr:.3g}: dV rel err {err:.2e}; losses {L[:4]} rel err {lerr.max():.2e}")
     assert L[3] < L[0]
     assert err <= 1e-4
     assert np.all(lerr <= 1e-5)

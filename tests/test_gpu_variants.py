@@ -56,10 +56,10 @@ def _run(sos, ix, **opts):
     return out
 
 
-def _same_descent(a, b, tol=1e-5):
-    """3 Adam steps: V_3 within 1e-6 (relative L2), the update V_3 - V_0
+def _same_descent(a, b, tol=1e-5, vtol=1e-6):
+    """3 Adam steps: V_3 within vtol (relative L2), the update V_3 - V_0
     within tol, the losses within 1e-5."""
-    assert np.linalg.norm(a["V3"] - b["V3"]) / np.linalg.norm(a["V3"]) <= 1e-6
+    assert np.linalg.norm(a["V3"] - b["V3"]) / np.linalg.norm(a["V3"]) <= vtol
     rel = np.linalg.norm(a["dV"] - b["dV"]) / np.linalg.norm(a["dV"])
     assert rel <= tol, rel
     assert np.allclose(a["losses"], b["losses"], rtol=1e-5)
@@ -105,3 +105,28 @@ def test_split_vs_fused_step(sos, ix):
 def test_plan_options_validated(sos, ix):
     with pytest.raises(sos.SosError):
         sos.SosPlan(ix, 8, bogus=True)
+
+
+def test_split_vs_fused_long_k(sos):
+    """The split step forced on a long-K shape (N = 8855: 139 K-blocks, 9730 R
+    block pairs -- more than k_mid's blocks can hold in shared memory, so its
+    phase C gathers R again) against the default fused step there."""
+    ix = sos.SosIndex(20, 4)
+    r = 96
+    out = []
+    for split in (True, False):
+        plan = sos.SosPlan(ix, r, split=split)
+        V = torch.from_numpy(si.v0(ix.N, r, seed=21)).cuda()
+        W = torch.zeros(ix.N, r, device="cuda")
+        W[:, :48] = torch.from_numpy(si.planted_w(ix.N, 48, 22)).cuda()
+        p = plan.forward(W)
+        plan.opt_init("adam", 1e-3)
+        V3 = V.clone()
+        losses = plan.descend(V3, p, 3).cpu().numpy()
+        out.append({"V3": V3.cpu().numpy(), "dV": V3.cpu().numpy() - V.cpu().numpy(), "losses": losses})
+        plan.close()
+    # different slice scales of V_{t+1} (exact vs 2x headroom) perturb the
+    # gradients by ~1e-7 relative, which Adam's g / sqrt(v) normalisation
+    # amplifies on entries with small |g| (DESIGN.md R8); both variants are
+    # checked against the fp64 oracle in tests/test_gpu_oracle_descent.py
+    _same_descent(out[0], out[1], tol=1e-4, vtol=1e-5)

@@ -275,7 +275,8 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
         (rc = dalloc(&P.d_tiles_fwd, std::max<size_t>(1, tf.size()) * sizeof(TileCoord))) ||
         (rc = dalloc(&P.d_tiles_bwd, std::max<size_t>(1, tb.size()) * sizeof(TileCoord))) ||
         (rc = dalloc(&P.d_rowsig, std::max<size_t>(1, P.sig_expect.size()) * sizeof(unsigned))) ||
-        (P.split && (rc = dalloc(&P.d_grad, (size_t)N * r * sizeof(float))))) {
+        (P.split && (rc = dalloc(&P.d_grad, (size_t)N * r * sizeof(float)))) ||
+        (P.split && (rc = dalloc(&P.d_part, (size_t)2 * std::max(P.mid_grid, 1) * sizeof(double))))) {
         sos_plan_destroy(pl);
         return rc;
     }
@@ -338,6 +339,7 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_tiles_bwd);
     cudaFree(P.d_rowsig);
     cudaFree(P.d_grad);
+    cudaFree(P.d_part);
     if (P.copy_st) cudaStreamDestroy(P.copy_st);
     if (P.sig_ev) cudaEventDestroy(P.sig_ev);
     if (P.timing) {

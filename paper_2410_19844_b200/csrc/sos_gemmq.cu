@@ -48,9 +48,13 @@ namespace sos {
 #ifdef SOS_EXPERIMENTS
 constexpr bool kExperiments = true;
 #define SOS_CLOCK() clock64()
+// SOS_GEMM_TRACE=1: CTA 0 records %globaltimer at phase boundaries (slot k) and prints them
+#define GEMM_MARK(k) do { if (args.trace && blockIdx.x == 0) { unsigned long long now_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_)); tmark_s[k] = now_; } } while (0)
 #else
 constexpr bool kExperiments = false;
 #define SOS_CLOCK() 0ll
+#define GEMM_MARK(k) do { } while (0)
 #endif
 
 struct GemmArgs {
@@ -73,6 +77,7 @@ struct GemmArgs {
     int skew_epoch, skew_lag;  // bounded K-skew (K-blocks per epoch, epochs of lead)
     int skew_sleep;            // ns between polls of the progress counter
     unsigned long long* dbg;   // experiments: SOS_GEMM_STATS per-role wait cycles
+    int trace;                 // experiments: SOS_GEMM_TRACE phase times of CTA 0
     int kserp;                 // walk K backwards on odd local tiles (L2 reuse across waves)
     int probe;                 // experiments: SOS_GEMM_PROBE (wrong results): 1 = K-blocks mod 8,
                                // 2 = also tile 0, 4 = 2 with B loaded only on the first ring pass
@@ -129,7 +134,8 @@ constexpr uint32_t kBBytes = kSlices * kBSliceBytes;
 constexpr uint32_t kStageBytes = kABytes + kBBytes;  // 39936
 constexpr uint32_t kBarBytes = 256;
 constexpr uint32_t kAuxSmemBytes = 64 * 65 * 4;    // V tile staging of the aux warps' V^T pack
-constexpr uint32_t kSmemBytes = kStages * kStageBytes + kBarBytes + kAuxSmemBytes + 1024;
+constexpr uint32_t kColScaleBytes = 2 * kTileN * 4; // the epilogue's column scales, double-buffered by tile
+constexpr uint32_t kSmemBytes = kStages * kStageBytes + kBarBytes + kAuxSmemBytes + kColScaleBytes + 1024;
 constexpr float kInv256 = 1.f / 256.f;
 constexpr float kInv65536 = 1.f / 65536.f;
 
@@ -271,6 +277,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     constexpr bool kFwd = kMode == kModeFwd;
     constexpr bool kUpd = kMode == kModeBwdUpdate || kMode == kModeBwdUpdateVtq;
     extern __shared__ uint8_t smem_raw[];
+#ifdef SOS_EXPERIMENTS
+    __shared__ unsigned long long tmark_s[10];
+    if (threadIdx.x < 10) tmark_s[threadIdx.x] = 0;
+    if (threadIdx.x == 0) GEMM_MARK(0);
+#endif
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -279,6 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint64_t* tempty = tfull + 1;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
     float(*auxbuf)[65] = reinterpret_cast<float(*)[65]>(smem + kStages * kStageBytes + kBarBytes);
+    float* colscale = reinterpret_cast<float*>(smem + kStages * kStageBytes + kBarBytes + kAuxSmemBytes);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -304,9 +316,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     cluster_sync();  // barrier inits + TMEM address visible pair-wide
     tc_fence_after();
     const uint32_t tbase = *tslot;
+    if (threadIdx.x == 0) GEMM_MARK(1);
     // launched with programmatic stream serialization (split steps), the setup
     // above overlapped the previous kernel's tail; its results are visible from here
     griddep_wait();
+    if (threadIdx.x == 0) GEMM_MARK(2);
     // converged (sos_opt_set_stop): no CTA touches V or the optimiser state
     const bool stopped = kUpd && descent_stopped(args.scal, args.opt, args.use_stop);
     if (stopped && args.rowsig && blockIdx.x == 0)  // nothing changes: release every chunk at once
@@ -411,6 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                             mbar_wait(&full[stage], phase);
                             if (kExperiments && args.dbg && lane == 0) atomicAdd(args.dbg + 3, (unsigned long long)(SOS_CLOCK() - c0));
                         }
+                        if (kExperiments && lane == 0 && tile == cid && kb == 0) GEMM_MARK(3);
                         tc_fence_after();
                         const uint64_t sd = desc0 + (uint64_t)((stage * kStageBytes) >> 4);
                         const uint64_t bd = sd + (kABytes >> 4);
@@ -440,6 +455,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
                     if (elect_one()) umma_commit_2sm(tfull, 0x3);  // both CTAs' epilogues may drain
+                    if (kExperiments && lane == 0) GEMM_MARK(4);
                     __syncwarp();
                     acc_phase ^= 1;
                 }
@@ -453,15 +469,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         OptConsts oc{};
         if (kUpd) oc = opt_consts(args.opt);
         uint32_t acc_phase = 0;
-        for (int tile = cid; tile < args.ntiles; tile += ncl) {
+        int it = 0;
+        for (int tile = cid; tile < args.ntiles; tile += ncl, ++it) {
             const TileCoord tc = args.tiles[tile];
             const int64_t i = (int64_t)tc.a * kPairM + rank * 128 + q * 32 + lane;
+            // the tile's column scales u_j into shared memory while the MMAs run (one
+            // load per column instead of a dependent L2 round trip per 4 columns in
+            // every epilogue thread); double-buffered by tile parity: a thread can
+            // reach tile k+2 only after every thread passed tile k+1's barrier
+            float* cs = colscale + (it & 1) * kTileN;
+            {
+                const int et = (warp - 2) * 32 + lane;
+                if (et < tc.nb) cs[et] = slice_unit(__ldg(args.umaxB + tc.c0 + et));
+                asm volatile("bar.sync 3, %0;" ::"n"(kEpiThreads));
+            }
+            const float* csh = cs + h * kEpiCols;
             float sum[kEpiCols];
 #pragma unroll
             for (int t = 0; t < kEpiCols; ++t) sum[t] = 0.f;
             const int ncol = min(kEpiCols, tc.nb - h * kEpiCols);  // this warp's live columns (<= 0: none)
             for (int kb0 = 0; kb0 < args.num_kb; kb0 += args.seg_kb) {
                 mbar_wait(tfull, acc_phase);
+                if (kExperiments && warp == 2 && lane == 0 && tile == cid && kb0 == 0) GEMM_MARK(5);
                 tc_fence_after();
                 const uint32_t tq = tbase + ((uint32_t)(q * 32) << 16) + h * kEpiCols;
 #pragma unroll
@@ -482,27 +511,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 if (lane == 0) mbar_arrive_cluster(tempty, 0);
                 acc_phase ^= 1;
             }
+            if (kExperiments && warp == 2 && lane == 0 && tile == cid) GEMM_MARK(8);
             const int64_t cbase = (int64_t)tc.c0 + h * kEpiCols;
             const float ui = slice_unit(__ldg(args.umaxA + i));
+            if (kExperiments && warp == 2 && lane == 0 && tile == cid) GEMM_MARK(9);
             if (kFwd) {
                 // rows [256a, 256a+256) vs cols [c0, c0+nb): all above the diagonal iff c0 >= 256a + 256
                 const bool strictly_upper = (int64_t)tc.c0 >= (int64_t)tc.a * kPairM + kPairM;
                 if (i < args.N) {
+                    // 16-column chunks: live, inside N, and in the stored PT triangle (a
+                    // later row block means j < i for all 16 columns: weight 0)
+                    bool live[kEpiCols / 16];
 #pragma unroll
                     for (int ch = 0; ch < kEpiCols / 16; ++ch) {
                         const int64_t c0 = cbase + ch * 16;
-                        if (ch * 16 >= ncol || c0 >= args.N) break;
-                        // PT holds blocks i/64 <= j/64 only; a later row block means j < i
-                        // for all 16 columns (weight 0), and the diagonal tile's columns grow
-                        if ((i >> 6) > (c0 >> 6)) continue;
-                        const uint4* prow = reinterpret_cast<const uint4*>(args.pt + pt_entry(i, c0));
-                        const uint4* pu = reinterpret_cast<const uint4*>(args.umaxB + c0);
+                        live[ch] = ch * 16 < ncol && c0 < args.N && (i >> 6) <= (c0 >> 6);
+                    }
+                    // the pair ranks of the next chunk are in flight while this one scatters
+                    uint4 rk[2][4];
+                    if (live[0]) {
+                        const uint4* prow = reinterpret_cast<const uint4*>(args.pt + pt_entry(i, cbase));
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) rk[0][u] = __ldg(prow + u);
+                    }
+#pragma unroll
+                    for (int ch = 0; ch < kEpiCols / 16; ++ch) {
+                        if (ch + 1 < kEpiCols / 16 && live[ch + 1]) {
+                            const uint4* prow =
+                                reinterpret_cast<const uint4*>(args.pt + pt_entry(i, cbase + (ch + 1) * 16));
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) rk[(ch + 1) & 1][u] = __ldg(prow + u);
+                        }
+                        if (!live[ch]) continue;
+                        const int64_t c0 = cbase + ch * 16;
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const uint4 rk = __ldg(prow + u);
-                            const uint4 ub = __ldg(pu + u);
-                            const uint32_t rr[4] = {rk.x, rk.y, rk.z, rk.w};
-                            const uint32_t bb[4] = {ub.x, ub.y, ub.z, ub.w};
+                            const uint4 k4 = rk[ch & 1][u];
+                            const uint32_t rr[4] = {k4.x, k4.y, k4.z, k4.w};
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
                                 const int t = u * 4 + e;
@@ -510,7 +555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                                 const int64_t j = c0 + t;
                                 const float w = strictly_upper ? 2.f : (i < j ? 2.f : (i == j ? 1.f : 0.f));
                                 if (w != 0.f)
-                                    red_add_f32(args.coef + rr[e], w * ui * slice_unit(bb[e]) * sum[ch * 16 + t]);
+                                    red_add_f32(args.coef + rr[e], w * ui * csh[ch * 16 + t] * sum[ch * 16 + t]);
                             }
                         }
                     }
@@ -522,11 +567,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                                                        (q * 32 + lane) * kTileN + h * kEpiCols);
                 const float s4 = 4.f * ui;
 #pragma unroll
-                for (int u = 0; u < kEpiCols / 4; ++u) {
-                    const uint4 ub = __ldg(reinterpret_cast<const uint4*>(args.umaxB + cbase) + u);
-                    gr[u] = make_float4(s4 * slice_unit(ub.x) * sum[4 * u], s4 * slice_unit(ub.y) * sum[4 * u + 1],
-                                        s4 * slice_unit(ub.z) * sum[4 * u + 2], s4 * slice_unit(ub.w) * sum[4 * u + 3]);
-                }
+                for (int u = 0; u < kEpiCols / 4; ++u)
+                    gr[u] = make_float4(s4 * csh[4 * u] * sum[4 * u], s4 * csh[4 * u + 1] * sum[4 * u + 1],
+                                        s4 * csh[4 * u + 2] * sum[4 * u + 2], s4 * csh[4 * u + 3] * sum[4 * u + 3]);
                 __threadfence_block();
                 asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));  // whole tile in the ring
                 update_tile_epi<kMode == kModeBwdUpdateVtq>(args, oc, args.ring + (int64_t)blockIdx.x * kRingTile,
@@ -537,23 +580,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                     __threadfence_system();
                     atomicAdd(args.rowsig + tc.a / args.sig_blocks, 1u);
                 }
-            } else if (i < args.N) {
+            } else {
+                // gradient store (sos_backward, sos_loss_grad, split step).  A thread holds
+                // one row, so direct stores would put 32 rows in every warp store; each
+                // 16-column chunk goes through a per-warp shared-memory tile instead
+                // (XOR-swizzled: conflict-free reads, 2-way writes) and leaves as two
+                // full 64-byte row segments per warp store
+                float* wbuf = &auxbuf[0][0] + (warp - 2) * 32 * 16;
                 const float s4 = 4.f * ui;
+                const int64_t row0 = (int64_t)tc.a * kPairM + rank * 128 + q * 32;
 #pragma unroll
-                for (int u = 0; u < kEpiCols / 4; ++u) {
-                    if (4 * u >= ncol) break;
-                    const int64_t c0 = cbase + 4 * u;
-                    const uint4 ub = __ldg(reinterpret_cast<const uint4*>(args.umaxB + cbase) + u);
-                    const float o[4] = {s4 * slice_unit(ub.x) * sum[4 * u], s4 * slice_unit(ub.y) * sum[4 * u + 1],
-                                        s4 * slice_unit(ub.z) * sum[4 * u + 2], s4 * slice_unit(ub.w) * sum[4 * u + 3]};
-                    float* g = args.grad + i * args.r + c0;
-                    if (c0 + 4 <= args.r && ((reinterpret_cast<uintptr_t>(g) & 15) == 0)) {
-                        *reinterpret_cast<float4*>(g) = make_float4(o[0], o[1], o[2], o[3]);
-                    } else {
+                for (int ch = 0; ch < kEpiCols / 16; ++ch) {
+                    if (ch * 16 >= ncol) break;  // warp-uniform
 #pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            if (c0 + e < args.r) g[e] = o[e];
+                    for (int e = 0; e < 16; ++e) wbuf[lane * 16 + (e ^ (lane & 15))] = s4 * csh[ch * 16 + e] * sum[ch * 16 + e];
+                    __syncwarp();
+                    const int c = lane & 15;
+                    const int64_t col = cbase + ch * 16 + c;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const int rr = 2 * k + (lane >> 4);
+                        const int64_t row = row0 + rr;
+                        if (row < args.N && col < args.r && ch * 16 + c < ncol)
+                            args.grad[row * args.r + col] = wbuf[rr * 16 + (c ^ (rr & 15))];
                     }
+                    __syncwarp();
                 }
             }
         }
@@ -569,6 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
     }
 
+    if (kExperiments && warp == 2 && lane == 0) GEMM_MARK(6);
     tc_fence_before();
     __syncthreads();
     cluster_sync();  // all MMAs consumed and both epilogues done before freeing TMEM
@@ -576,6 +628,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         tmem_dealloc_2sm(tbase, 512);
     }
+#ifdef SOS_EXPERIMENTS
+    if (threadIdx.x == 0) {
+        GEMM_MARK(7);
+        if (args.trace && blockIdx.x == 0) {
+            const unsigned long long* m = tmark_s;
+            printf("k_gemmq<%d> cta0 (us): setup %.2f | griddep %.2f | first operands %.2f | last commit %.2f | "
+                   "first drain %.2f | drained %.2f | row scale %.2f | epilogue end %.2f | teardown %.2f\n", kMode,
+                   (m[1] - m[0]) * 1e-3, (m[2] - m[1]) * 1e-3, (m[3] - m[2]) * 1e-3, (m[4] - m[0]) * 1e-3,
+                   (m[5] - m[0]) * 1e-3, (m[8] - m[0]) * 1e-3, (m[9] - m[0]) * 1e-3, (m[6] - m[0]) * 1e-3,
+                   (m[7] - m[6]) * 1e-3);
+        }
+    }
+#endif
 }
 
 // ------------------------------------------------------------------ host --
@@ -675,6 +740,7 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
                 cudaMemset(dbg, 0, 8 * sizeof(unsigned long long));
             a.dbg = dbg;
         }
+        a.trace = env_int("SOS_GEMM_TRACE", 0);
         const int max_ctas = env_int("SOS_GEMM_CTAS", 0);  // cap the persistent grid
         if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
     }

@@ -167,6 +167,7 @@ struct Plan {
     bool narrow;           // narrow tiles at ragged column blocks
     int mid_grid;          // cooperative grid of k_mid (co-resident blocks)
     int mid_tiles;         // R blocks each k_mid block holds in shared memory
+    double* d_part;        // k_mid's per-block partial sums [mid_grid][2]
     float* d_grad;         // N x r gradient buffer of the split step
     uint8_t* d_rq;    // RQ
     unsigned* d_vrow; // max_k |V_ik| (float bits), rowsV

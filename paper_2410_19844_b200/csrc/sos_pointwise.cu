@@ -512,6 +512,7 @@ struct MidArgs {
     int colmax;
     uint8_t* VTQ;
     unsigned* zero_cols;
+    double* part;  // [gridDim][2] per-block partial sums of the loss and |p|^2
     int hold;   // every block holds its R blocks from phase B to C (else C gathers them again)
     int trace;  // experiment build only
 };
@@ -585,9 +586,9 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
             pn = lane < kMidThreads / 32 ? red[1][lane] : 0.0;
             l = warp_sum(l);
             pn = warp_sum(pn);
-            if (lane == 0) {
-                atomicAdd(&a.sc->loss, l);
-                atomicAdd(&a.sc->pnorm2, pn);
+            if (lane == 0) {  // per-block partial sums (fp64 atomics from every block serialise)
+                a.part[2 * blockIdx.x] = l;
+                a.part[2 * blockIdx.x + 1] = pn;
             }
         }
         for (int64_t e = gtid; e < a.Np; e += gstride) a.rrow[e] = 0u;
@@ -619,13 +620,32 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
     MID_MARK(1);
     grid.sync();
     MID_MARK(2);
-    // ---- B
-    if (blockIdx.x == 0 && t == 0) {
-        advance_step(a.opt);
-        double* L = a.losses_from_opt ? a.opt->losses : a.losses;
-        if (L) L[a.losses_from_opt ? a.opt->loss_idx++ : 0] = a.sc->loss;
+    // ---- B: every block sums the partials in the same order (deterministic, no
+    // extra barrier); block 0 publishes them for the kernels after k_mid
+    __shared__ double tot_s[2];
+    if (w == 0) {
+        double l = 0.0, pn = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) {
+            l += a.part[2 * b];
+            pn += a.part[2 * b + 1];
+        }
+        l = warp_sum(l);
+        pn = warp_sum(pn);
+        if (lane == 0) {
+            tot_s[0] = l;
+            tot_s[1] = pn;
+            if (blockIdx.x == 0) {
+                a.sc->loss = l;
+                a.sc->pnorm2 = pn;
+                advance_step(a.opt);
+                double* L = a.losses_from_opt ? a.opt->losses : a.losses;
+                if (L) L[a.losses_from_opt ? a.opt->loss_idx++ : 0] = l;
+            }
+        }
     }
-    const bool stopped = descent_stopped(a.sc, a.opt, 1);
+    __syncthreads();
+    const double tol = a.opt->stop_tol;
+    const bool stopped = tol > 0.0 && tot_s[0] <= tol * tot_s[1];
     const int64_t npairs = a.nkbN * (a.nkbN + 1) / 2;
     {
         const int64_t nkt = (a.rowsVT + 63) / 64;
@@ -757,6 +777,7 @@ void launch_mid(Plan& P, const float* p, const float* V, unsigned* vcol, bool co
     a.colmax = colmax ? 1 : 0;
     a.VTQ = P.d_vtq;
     a.zero_cols = zero_cols;
+    a.part = P.d_part;
     a.trace = 0;
 #ifdef SOS_EXPERIMENTS
     {

@@ -585,8 +585,8 @@ static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const fl
                               : DescendBufs{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1], d.vcol[b],
                                             P.tmap_vtq_b, nullptr};
     launch_gemm_bwd_update(P, V, st, &db);
-    launch_descend_fixup(P, V, d.vrowx[b], d.vrowx[b ^ 1], d.urow[b], d.urow[b ^ 1], d.vcol[b], d.vcol[b ^ 1], st);
-    if (vu) launch_descend_fixup_cols(P, V, d.vcol[b], d.vcol[b ^ 1], d.ucol[b ^ 1], d.vtq[b ^ 1], st);
+    launch_descend_fixup(P, V, d.vrowx[b], d.vrowx[b ^ 1], d.urow[b], d.urow[b ^ 1], d.vcol[b], d.vcol[b ^ 1],
+                         d.ucol[b ^ 1], vu ? d.vtq[b ^ 1] : nullptr, st);
     return check_launch("descend step");
 }
 

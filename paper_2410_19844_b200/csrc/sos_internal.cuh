@@ -315,11 +315,11 @@ void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st, const unsigned* vcol
 // vs K-blocks per CTA pair over the forward's actual grid)
 bool vtq_fits_aux(const Plan& P);
 void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBufs* db = nullptr);
-void launch_descend_fixup_cols(Plan& P, const float* V, const unsigned* vcol_cur, const unsigned* vcol_next,
-                               unsigned* ucol_next, uint8_t* vtq_next, cudaStream_t st);
+// sos_descend, long K: re-slice the rows (and with vtq_next the columns) whose new
+// maximum left the headroom window; one launch (sos_pointwise.cu)
 void launch_descend_fixup(Plan& P, const float* V, const unsigned* vrow_cur, unsigned* vrow_next,
                           const unsigned* urow_cur, unsigned* urow_next, const unsigned* vcol_cur, unsigned* vcol_next,
-                          cudaStream_t st);
+                          unsigned* ucol_next, uint8_t* vtq_next, cudaStream_t st);
 bool make_q_tmap(void* map, const uint8_t* base, int64_t rows_total, int64_t nkb, int box_rows);
 
 }  // namespace sos

@@ -860,102 +860,108 @@ void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop) {
 
 
 // ------------------------------------------------------- sos_descend fixup --
-// Before the forward of step t+1: the update of step t wrote the slices of each
-// updated row with the scale kHeadroom * (row max of V_t).  They stay exact to
-// ~22 bits while the new row max lies in [u/4, u], u = kHeadroom * old max; the
-// rare rows outside (growth beyond the headroom, or a large shrink) are re-sliced
-// here from V with their exact new maximum.  urow_next receives the scale the
-// forward must use for every row.  If the stopping rule held at step t the
-// update did not run, and everything of step t carries over.
-__global__ void __launch_bounds__(256) k_descend_fixup(const float* __restrict__ V, int64_t N, int64_t r,
-                                                       int64_t rowsV, int64_t nkbV, int64_t rowsVT,
-                                                       const unsigned* __restrict__ vrow_cur,
-                                                       unsigned* __restrict__ vrow_next,
-                                                       const unsigned* __restrict__ urow_cur,
-                                                       unsigned* __restrict__ urow_next,
-                                                       const unsigned* __restrict__ vcol_cur,
-                                                       unsigned* __restrict__ vcol_next, uint8_t* __restrict__ VQ,
-                                                       const Scalars* sc, const DevOpt* opt) {
-    if (descent_stopped(sc, opt, 1)) {
+// Before the forward of step t+1 (long K, fused update): the update of step t
+// wrote the slices of each updated row of V with the scale kHeadroom * (row
+// max of V_t), and (vtq_from_update) the V^T slices of each column with
+// kHeadroom * (column max of V_t).  They stay exact to ~22 bits while the new
+// maximum lies in [u/4, u], u = kHeadroom * old max; the rare rows / columns
+// outside (growth beyond the headroom, or a large shrink) are re-sliced here
+// from V with their exact new maximum, and urow_next / ucol_next receive the
+// scale each row / column was written with.  One warp per row, then one warp
+// per column (cols != 0), in a single launch: the common case is one load and
+// one store per warp.  If the stopping rule held at step t the update did not
+// run and everything of step t carries over.
+struct FixupArgs {
+    const float* V;
+    int64_t N, r, rowsV, nkbV, rowsVT, nkbN;
+    const unsigned *vrow_cur, *urow_cur, *vcol_cur;
+    unsigned *vrow_next, *urow_next, *vcol_next, *ucol_next;
+    uint8_t* VQ;
+    uint8_t* VTQ;  // nullptr: no column fixup (the forward packs V^T)
+    const Scalars* sc;
+    const DevOpt* opt;
+};
+__global__ void __launch_bounds__(256) k_descend_fixup(const FixupArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (descent_stopped(a.sc, a.opt, 1)) {
         const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rowsV; e += stride) {
-            vrow_next[e] = vrow_cur[e];
-            urow_next[e] = urow_cur[e];
+        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.rowsV; e += stride) {
+            a.vrow_next[e] = a.vrow_cur[e];
+            a.urow_next[e] = a.urow_cur[e];
         }
-        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rowsVT; e += stride)
-            vcol_next[e] = vcol_cur[e];
+        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.rowsVT; e += stride)
+            a.vcol_next[e] = a.vcol_cur[e];
         return;
     }
-    for (int64_t i = blockIdx.x; i < rowsV; i += gridDim.x) {
-        const float u = kHeadroom * __uint_as_float(vrow_cur[i]);
-        const unsigned mb = vrow_next[i];
-        const float mx = __uint_as_float(mb);
-        if (mx <= u && mx >= 0.25f * u) {
-            if (threadIdx.x == 0) urow_next[i] = __float_as_uint(u);
-            continue;
-        }
-        if (threadIdx.x == 0) urow_next[i] = mb;
-        const float c = slice_scale(mb);
-        for (int64_t cc = threadIdx.x; cc < nkbV * 4; cc += blockDim.x) {
-            const int64_t k0 = cc * 16;
-            float x[16];
+    const int64_t nrow = a.rowsV, ncol = a.VTQ ? a.r : 0;
+    for (int64_t w = warp; w < nrow + ncol; w += nwarps) {
+        if (w < nrow) {
+            const int64_t i = w;
+            const float u = kHeadroom * __uint_as_float(a.vrow_cur[i]);
+            const unsigned mb = a.vrow_next[i];
+            const float mx = __uint_as_float(mb);
+            const bool keep = mx <= u && mx >= 0.25f * u;
+            if (lane == 0) a.urow_next[i] = keep ? __float_as_uint(u) : mb;
+            if (keep) continue;
+            const float c = slice_scale(mb);
+            for (int64_t cc = lane; cc < a.nkbV * 4; cc += 32) {
+                const int64_t k0 = cc * 16;
+                float x[16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) x[e] = (i < N && k0 + e < r) ? V[i * r + k0 + e] : 0.f;
-            uint4 q[3];
-            slice16(x, c, q);
-            store_q16(VQ, cc >> 2, i, (int)(cc & 3), nkbV, rowsV, q);
+                for (int e = 0; e < 16; ++e) x[e] = (i < a.N && k0 + e < a.r) ? a.V[i * a.r + k0 + e] : 0.f;
+                uint4 q[3];
+                slice16(x, c, q);
+                store_q16(a.VQ, cc >> 2, i, (int)(cc & 3), a.nkbV, a.rowsV, q);
+            }
+        } else {
+            const int64_t k = w - nrow;
+            const float u = kHeadroom * __uint_as_float(a.vcol_cur[k]);
+            const unsigned mb = a.vcol_next[k];
+            const float mx = __uint_as_float(mb);
+            const bool keep = mx <= u && mx >= 0.25f * u;
+            if (lane == 0) a.ucol_next[k] = keep ? __float_as_uint(u) : mb;
+            if (keep) continue;
+            const float c = slice_scale(mb);
+            for (int64_t cc = lane; cc < a.nkbN * 4; cc += 32) {
+                const int64_t j0 = cc * 16;
+                float x[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) x[e] = j0 + e < a.N ? a.V[(j0 + e) * a.r + k] : 0.f;
+                uint4 q[3];
+                slice16(x, c, q);
+                store_q16(a.VTQ, cc >> 2, k, (int)(cc & 3), a.nkbN, a.rowsVT, q);
+            }
         }
     }
-}
-
-// The same for the V^T slices the update wrote for step t+1 (scale kHeadroom x
-// the old column maximum): a column whose new maximum left [u/4, u] is
-// re-sliced from V with its exact maximum (strided reads: rare); ucol_next
-// receives the scale the backward must unscale each VTQ row with.
-__global__ void __launch_bounds__(256) k_descend_fixup_cols(const float* __restrict__ V, int64_t N, int64_t r,
-                                                            int64_t nkbN, int64_t rowsVT,
-                                                            const unsigned* __restrict__ vcol_cur,
-                                                            const unsigned* __restrict__ vcol_next,
-                                                            unsigned* __restrict__ ucol_next, uint8_t* __restrict__ VTQ,
-                                                            const Scalars* sc, const DevOpt* opt) {
-    if (descent_stopped(sc, opt, 1)) return;  // no update ran: the next step reads nothing new
-    for (int64_t k = blockIdx.x; k < r; k += gridDim.x) {
-        const float u = kHeadroom * __uint_as_float(vcol_cur[k]);
-        const unsigned mb = vcol_next[k];
-        const float mx = __uint_as_float(mb);
-        if (mx <= u && mx >= 0.25f * u) {
-            if (threadIdx.x == 0) ucol_next[k] = __float_as_uint(u);
-            continue;
-        }
-        if (threadIdx.x == 0) ucol_next[k] = mb;
-        const float c = slice_scale(mb);
-        for (int64_t cc = threadIdx.x; cc < nkbN * 4; cc += blockDim.x) {
-            const int64_t j0 = cc * 16;
-            float x[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) x[e] = j0 + e < N ? V[(j0 + e) * r + k] : 0.f;
-            uint4 q[3];
-            slice16(x, c, q);
-            store_q16(VTQ, cc >> 2, k, (int)(cc & 3), nkbN, rowsVT, q);
-        }
-    }
-}
-
-void launch_descend_fixup_cols(Plan& P, const float* V, const unsigned* vcol_cur, const unsigned* vcol_next,
-                               unsigned* ucol_next, uint8_t* vtq_next, cudaStream_t st) {
-    LaunchScope ls(P, KK_PACK_V, st);
-    k_descend_fixup_cols<<<grid_for(P, P.r * 256, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.nkbN, P.rowsVT, vcol_cur,
-                                                                        vcol_next, ucol_next, vtq_next, P.d_scal,
-                                                                        P.d_opt);
 }
 
 void launch_descend_fixup(Plan& P, const float* V, const unsigned* vrow_cur, unsigned* vrow_next,
                           const unsigned* urow_cur, unsigned* urow_next, const unsigned* vcol_cur, unsigned* vcol_next,
-                          cudaStream_t st) {
+                          unsigned* ucol_next, uint8_t* vtq_next, cudaStream_t st) {
     LaunchScope ls(P, KK_PACK_V, st);
-    k_descend_fixup<<<grid_for(P, P.rowsV * 256, 256), 256, 0, st>>>(
-        V, P.idx->N, P.r, P.rowsV, P.nkbV, P.rowsVT, vrow_cur, vrow_next, urow_cur, urow_next, vcol_cur, vcol_next,
-        P.d_vq, P.d_scal, P.d_opt);
+    FixupArgs a;
+    a.V = V;
+    a.N = P.idx->N;
+    a.r = P.r;
+    a.rowsV = P.rowsV;
+    a.nkbV = P.nkbV;
+    a.rowsVT = P.rowsVT;
+    a.nkbN = P.nkbN;
+    a.vrow_cur = vrow_cur;
+    a.urow_cur = urow_cur;
+    a.vcol_cur = vcol_cur;
+    a.vrow_next = vrow_next;
+    a.urow_next = urow_next;
+    a.vcol_next = vcol_next;
+    a.ucol_next = ucol_next;
+    a.VQ = P.d_vq;
+    a.VTQ = vtq_next;
+    a.sc = P.d_scal;
+    a.opt = P.d_opt;
+    const int64_t warps = P.rowsV + (vtq_next ? P.r : 0);
+    k_descend_fixup<<<grid_for(P, warps * 32, 256), 256, 0, st>>>(a);
 }
 
 }  // namespace sos

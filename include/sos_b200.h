@@ -107,13 +107,17 @@ int sos_plan_create(const sos_index *idx, int64_t r, sos_plan **out);
  *   rmax_direct:  R row maxima by one gather pass over the pair-rank table
  *                 instead of the monomial-lattice DP (default by a cost model).
  *   narrow_tiles: tiles narrower than 160 columns where a column block is
- *                 partly outside the matrix (default 1). */
+ *                 partly outside the matrix (default 1).
+ *   tile_w:       column tile width of the GEMMs, -1 or 0 = auto (160, or 128
+ *                 for small problems where it saves a partial wave), else 96,
+ *                 128 or 160; the backward uses it only in split plans. */
 typedef struct {
     int split;
     int vtq_from_update;
     int vtq_in_aux;
     int rmax_direct;
     int narrow_tiles;
+    int tile_w;
 } sos_plan_opts;
 int sos_plan_create_ex(const sos_index *idx, int64_t r, const sos_plan_opts *opts, sos_plan **out);
 int sos_plan_destroy(sos_plan *plan);

@@ -34,7 +34,7 @@ class _OptParams(ctypes.Structure):
 
 class _PlanOpts(ctypes.Structure):
     _fields_ = [("split", ctypes.c_int), ("vtq_from_update", ctypes.c_int), ("vtq_in_aux", ctypes.c_int),
-                ("rmax_direct", ctypes.c_int), ("narrow_tiles", ctypes.c_int)]
+                ("rmax_direct", ctypes.c_int), ("narrow_tiles", ctypes.c_int), ("tile_w", ctypes.c_int)]
 
 
 _lib = None
@@ -158,9 +158,10 @@ class SosPlan:
 
     Keyword options (sos_plan_opts: None = the library's choice by size, else
     True / False): split, vtq_from_update, vtq_in_aux, rmax_direct,
-    narrow_tiles -- implementation variants of the same step."""
+    narrow_tiles; tile_w (None, 96, 128 or 160) -- implementation variants of
+    the same step."""
 
-    OPTS = ("split", "vtq_from_update", "vtq_in_aux", "rmax_direct", "narrow_tiles")
+    OPTS = ("split", "vtq_from_update", "vtq_in_aux", "rmax_direct", "narrow_tiles", "tile_w")
 
     def __init__(self, index: SosIndex, r: int, **opts):
         bad = set(opts) - set(self.OPTS)
@@ -169,7 +170,8 @@ class SosPlan:
         self.index = index
         self.r = r
         h = _vp()
-        o = _PlanOpts(*[-1 if opts.get(k) is None else int(bool(opts[k])) for k in self.OPTS])
+        o = _PlanOpts(*[-1 if opts.get(k) is None else (int(opts[k]) if k == "tile_w" else int(bool(opts[k])))
+                        for k in self.OPTS])
         _check(load().sos_plan_create_ex(index._h, r, ctypes.byref(o), ctypes.byref(h)))
         self._h = h
 

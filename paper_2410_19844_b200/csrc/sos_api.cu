@@ -192,24 +192,46 @@ static int64_t tile_group() {
 static int round_up32(int64_t x) { return (int)std::max<int64_t>(32, (x + 31) / 32 * 32); }
 
 // forward: upper triangle of the Gram matrix (columns j >= rows' block start);
-// backward: all of R V.  Columns tiled on the 160 grid; see TileCoord for the
-// narrow tiles
-static void build_tiles(int64_t row_blocks, int64_t ncols, bool upper, bool narrow, std::vector<TileCoord>& out) {
+// backward: all of R V.  Columns tiled on a W grid (W = 160, or narrower for
+// small problems, see pick_tile_width); see TileCoord for the narrow tiles
+static void build_tiles(int64_t row_blocks, int64_t ncols, bool upper, bool narrow, int W, std::vector<TileCoord>& out) {
     const int64_t GA = tile_group();
-    const int64_t col_blocks = (ncols + kTileN - 1) / kTileN;
+    const int64_t col_blocks = (ncols + W - 1) / W;
     for (int64_t g0 = 0; g0 < row_blocks; g0 += GA) {
         const int64_t g1 = std::min(row_blocks, g0 + GA);
         for (int64_t b = 0; b < col_blocks; ++b)
             for (int64_t a = g0; a < g1; ++a) {
-                int64_t c_start = b * kTileN, c_end = std::min(ncols, c_start + kTileN);
+                int64_t c_start = b * W, c_end = std::min(ncols, c_start + W);
                 if (upper) {
                     if (c_end <= a * kPairM) continue;              // wholly below the diagonal block
                     c_start = std::max(c_start, a * kPairM);        // skip columns left of it
                 }
-                if (!narrow) c_start = b * kTileN, c_end = c_start + kTileN;  // A/B: full 160-wide grid tiles
+                if (!narrow) c_start = b * W, c_end = c_start + W;  // A/B: full grid tiles
                 out.push_back(TileCoord{(int)a, (int)c_start, round_up32(c_end - c_start), 0});
             }
     }
+}
+
+// Column tile width.  A GEMM of T tiles on P CTA pairs runs ceil(T / P) waves of
+// W-wide tiles, so its MMA time goes as ceil(T(W) / P) * W: a small problem
+// whose 160-wide tiles overflow one wave by a little does better with narrower
+// tiles (config 2 backward: 104 tiles of 160 = 2 waves, 128 tiles of 128 = 2
+// waves of 0.8 the time; forward: 56 -> 72 tiles, still one wave).  The int8
+// pair MMA runs at full rate down to N = 128 (profiles/r1_mma2_pair_N_sweep.log),
+// so only 160 and 128 are candidates, and only for problems of at most 4 waves
+// (more tiles re-read their A panels more often).  forced: sos_plan_opts.tile_w.
+static int pick_tile_width(int64_t row_blocks, int64_t ncols, bool upper, bool narrow, int pairs, int forced) {
+    if (forced > 0) return forced;
+    auto cost = [&](int W, int64_t* waves) {
+        std::vector<TileCoord> t;
+        build_tiles(row_blocks, ncols, upper, narrow, W, t);
+        *waves = ((int64_t)t.size() + pairs - 1) / pairs;
+        return *waves * W;
+    };
+    int64_t w160 = 0, w128 = 0;
+    const int64_t c160 = cost(kTileN, &w160);
+    if (w160 > 4) return kTileN;
+    return cost(128, &w128) < c160 ? 128 : kTileN;
 }
 
 int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
@@ -220,10 +242,12 @@ static bool pick(int opt, bool dflt) { return opt < 0 ? dflt : opt != 0; }
 
 int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts, sos_plan** out) {
     if (!h || !out || r < 1) return fail(SOS_ERR_ARG, "bad argument");
-    sos_plan_opts o = {-1, -1, -1, -1, -1};
+    sos_plan_opts o = {-1, -1, -1, -1, -1, -1};
     if (opts) o = *opts;
     for (int v : {o.split, o.vtq_from_update, o.vtq_in_aux, o.rmax_direct, o.narrow_tiles})
         if (v < -1 || v > 1) return fail(SOS_ERR_ARG, "sos_plan_opts fields must be -1, 0 or 1");
+    if (!(o.tile_w == -1 || o.tile_w == 0 || o.tile_w == 96 || o.tile_w == 128 || o.tile_w == 160))
+        return fail(SOS_ERR_ARG, "sos_plan_opts.tile_w must be -1 (auto), 96, 128 or 160");
     *out = nullptr;
     int sms = 0;
     int rc = require_device(&sms);
@@ -240,15 +264,22 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
     P.rowsVT = ((r + kTileN - 1) / kTileN) * kTileN;
     P.nkbN = (N + kQK - 1) / kQK;  // K = j runs over the N monomials (rows stay padded to Np)
     P.narrow = pick(o.narrow_tiles, true);
-    std::vector<TileCoord> tf, tb;
-    build_tiles(Np / kPairM, N, true, P.narrow, tf);
-    build_tiles(Np / kPairM, r, false, P.narrow, tb);
-    P.ntiles_fwd = (int)tf.size();
-    P.ntiles_bwd = (int)tb.size();
     // short K: a tile's MMAs (~nkbN x 0.5 us) cannot hide the fused update
     // (~25 us per tile), so the split step stores the gradient and updates
     // with all SMs (profiles/r1_update_split_ab.log, r2_split_step_ab.log)
     P.split = pick(o.split, P.nkbN < kSplitKb);
+    {
+        // the fused update assumes every tile but a matrix-edge one is 160 wide, so
+        // narrower backward tiles only with the split step (gradient stored)
+        const int pairs = resident_gemm_pairs(sms);
+        P.tile_w_fwd = pick_tile_width(Np / kPairM, N, true, P.narrow, pairs, o.tile_w);
+        P.tile_w_bwd = P.split ? pick_tile_width(Np / kPairM, r, false, P.narrow, pairs, o.tile_w) : kTileN;
+    }
+    std::vector<TileCoord> tf, tb;
+    build_tiles(Np / kPairM, N, true, P.narrow, P.tile_w_fwd, tf);
+    build_tiles(Np / kPairM, r, false, P.narrow, P.tile_w_bwd, tb);
+    P.ntiles_fwd = (int)tf.size();
+    P.ntiles_bwd = (int)tb.size();
     // sos_descend: the update can write the next step's V^T slices when its
     // extra slicing work hides under a tile's MMAs (long K); for short K it
     // would lengthen the update-bound backward (profiles/r1_vtq_next_ab.log)

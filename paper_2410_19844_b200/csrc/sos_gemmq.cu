@@ -692,6 +692,7 @@ template <int kMode>
 static int resident_ctas(int num_sms) {
     static int cached = -1;
     if (cached < 0) {
+        cudaFuncSetAttribute(k_gemmq<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(num_sms & ~1);
         cfg.blockDim = dim3(kGemmThreads);
@@ -712,6 +713,8 @@ static int resident_ctas(int num_sms) {
     }
     return cached;
 }
+
+int resident_gemm_pairs(int num_sms) { return resident_ctas<kModeFwd>(num_sms) / 2; }
 
 template <int kMode>
 static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorMap& mb, GemmArgs a,

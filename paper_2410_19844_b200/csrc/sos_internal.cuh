@@ -165,6 +165,8 @@ struct Plan {
     bool vtq_in_aux;       // the forward's aux warps write VTQ (else k_pack_vtq before it)
     bool rmax_direct;      // R row maxima by one gather pass over PT (else the lattice DP)
     bool narrow;           // narrow tiles at ragged column blocks
+    int tile_w_fwd;        // column tile width of the forward / backward GEMM (160, or 128 for
+    int tile_w_bwd;        // small problems; the backward only in split plans)
     int mid_grid;          // cooperative grid of k_mid (co-resident blocks)
     int mid_tiles;         // R blocks each k_mid block holds in shared memory
     double* d_part;        // k_mid's per-block partial sums [mid_grid][2]
@@ -321,5 +323,7 @@ void launch_descend_fixup(Plan& P, const float* V, const unsigned* vrow_cur, uns
                           const unsigned* urow_cur, unsigned* urow_next, const unsigned* vcol_cur, unsigned* vcol_next,
                           unsigned* ucol_next, uint8_t* vtq_next, cudaStream_t st);
 bool make_q_tmap(void* map, const uint8_t* base, int64_t rows_total, int64_t nkb, int box_rows);
+// CTA pairs of the persistent GEMM grid (co-resident clusters)
+int resident_gemm_pairs(int num_sms);
 
 }  // namespace sos

@@ -130,3 +130,13 @@ def test_split_vs_fused_long_k(sos):
     # amplifies on entries with small |g| (R8); both variants are
     # checked against the fp64 oracle in tests/test_gpu_oracle_descent.py
     _same_descent(out[0], out[1], tol=1e-4, vtol=1e-5)
+
+
+def test_tile_width_128_vs_160(sos, ix):
+    """Column tiles 128 wide (chosen automatically for small problems that would
+    run a partial second wave at 160) vs 160: the same integer products, so a
+    bit-identical plain backward; the descent agrees to fp32 rounding."""
+    a = _run(sos, ix, tile_w=128)
+    b = _run(sos, ix, tile_w=160)
+    assert np.array_equal(a["grad"], b["grad"])
+    _same_descent(a, b)

@@ -13,7 +13,7 @@ if "--exp" in sys.argv:  # the -DSOS_EXPERIMENTS build (environment switches, pr
 
 n, d, r = (int(x) for x in sys.argv[1:4])
 steps = int(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4].isdigit() else 20
-opts = {k: bool(int(v)) for k, v in (a.split("=") for a in sys.argv[4:] if "=" in a)}
+opts = {k: (int(v) if k == "tile_w" else bool(int(v))) for k, v in (a.split("=") for a in sys.argv[4:] if "=" in a)}
 ix = sos.SosIndex(n, d)
 plan = sos.SosPlan(ix, r, **opts)
 rs = max(1, ix.N // 2)

@@ -230,7 +230,7 @@ static int pick_tile_width(int64_t row_blocks, int64_t ncols, bool upper, bool n
     };
     int64_t w160 = 0, w128 = 0;
     const int64_t c160 = cost(kTileN, &w160);
-    if (w160 > 4) return kTileN;
+    if (w160 > 4 || ncols <= 128) return kTileN;  // (<= 128 columns: the same single column block)
     return cost(128, &w128) < c160 ? 128 : kTileN;
 }
 

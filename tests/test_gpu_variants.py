@@ -129,7 +129,7 @@ def test_split_vs_fused_long_k(sos):
     # gradients by ~1e-7 relative, which Adam's g / sqrt(v) normalisation
     # amplifies on entries with small |g| (R8); both variants are
     # checked against the fp64 oracle in tests/test_gpu_oracle_descent.py
-    _same_descent(out[0], out[1], tol=1e-4, vtol=1e-5)
+    _same_descent(out[0], out[1], tol=1e-4, vtol=3e-5)
 
 
 def test_tile_width_128_vs_160(sos, ix):

@@ -83,3 +83,15 @@ def test_release_library_reads_no_tuning_environment(lib):
     blob = open(build.LIB, "rb").read()
     assert b"SOS_" not in blob
     assert hasattr(lib, "sos_plan_create_ex")
+
+
+@pytest.mark.slow
+def test_experiment_build_compiles_and_exports():
+    """The -DSOS_EXPERIMENTS build (environment probes and traces, loaded only by
+    tools with --exp) still compiles and exports the same ABI."""
+    from paper_2410_19844_b200 import build
+    path = build.build(experiments=True)
+    exp = ctypes.CDLL(path)
+    missing = [n for n in declared_functions() if not hasattr(exp, n)]
+    assert not missing, missing
+    assert b"SOS_GEMM_PROBE" in open(path, "rb").read()

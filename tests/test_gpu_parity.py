@@ -711,3 +711,24 @@ def test_boundary_shapes_forward_backward(sos, n, d, r):
     res = si.residual_probe(o.M, seed=200 + r)
     g = plan.backward(Vd, torch.from_numpy(res).cuda()).cpu().numpy()
     assert rel_l2(g, o.grad_rows(V, res, np.arange(o.N))) <= REL_TOL
+
+
+@pytest.mark.parametrize("variant", ["split", "fused"])
+@pytest.mark.parametrize("n,d,r", [(2, 2, 1), (7, 4, 1), (5, 3, 3), (1, 3, 2), (4, 3, 20)])
+def test_descend_tiny_shapes_vs_oracle(sos, n, d, r, variant):
+    """Degenerate sizes through sos_descend (r = 1: one square; N = 1: a
+    univariate form; rows shorter than a float4): 3 GD steps against the
+    oracle's GD, and the losses."""
+    o = oracle(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r, split=(variant == "split"))
+    W = si.planted_w(o.N, max(1, r // 2), seed=8)
+    p = o.forward(W).astype(np.float32)
+    V0 = si.v0(o.N, r, seed=9)
+    lr = 1e-2
+    plan.opt_init("gd", lr)
+    Vd = torch.from_numpy(V0.copy()).cuda()
+    ld = plan.descend(Vd, torch.from_numpy(p).cuda(), 3).cpu().numpy()
+    Vo, Lo = o.descent(V0, p, "gd", 3, lr)
+    assert rel_l2(Vd.cpu().numpy() - V0, Vo - V0) <= 1e-5
+    assert np.allclose(ld, Lo[:3], rtol=1e-5)

@@ -110,7 +110,12 @@ int sos_plan_create(const sos_index *idx, int64_t r, sos_plan **out);
  *                 partly outside the matrix (default 1).
  *   tile_w:       column tile width of the GEMMs, -1 or 0 = auto (160, or 128
  *                 for small problems where it saves a partial wave), else 96,
- *                 128 or 160; the backward uses it only in split plans. */
+ *                 128 or 160; the backward uses it only in split plans.
+ *   r_headroom:   (split = 0, sos_descend) after the first step of a call the R
+ *                 slices use 2x the previous step's exact R row maxima; the
+ *                 packer takes this step's exact maxima on the fly and re-slices
+ *                 the rare rows outside the window (default 1); 0 = exact row
+ *                 maxima every step (lattice DP or direct pass). */
 typedef struct {
     int split;
     int vtq_from_update;
@@ -118,6 +123,7 @@ typedef struct {
     int rmax_direct;
     int narrow_tiles;
     int tile_w;
+    int r_headroom;
 } sos_plan_opts;
 int sos_plan_create_ex(const sos_index *idx, int64_t r, const sos_plan_opts *opts, sos_plan **out);
 int sos_plan_destroy(sos_plan *plan);

@@ -34,7 +34,8 @@ class _OptParams(ctypes.Structure):
 
 class _PlanOpts(ctypes.Structure):
     _fields_ = [("split", ctypes.c_int), ("vtq_from_update", ctypes.c_int), ("vtq_in_aux", ctypes.c_int),
-                ("rmax_direct", ctypes.c_int), ("narrow_tiles", ctypes.c_int), ("tile_w", ctypes.c_int)]
+                ("rmax_direct", ctypes.c_int), ("narrow_tiles", ctypes.c_int), ("tile_w", ctypes.c_int),
+                ("r_headroom", ctypes.c_int)]
 
 
 _lib = None
@@ -158,10 +159,10 @@ class SosPlan:
 
     Keyword options (sos_plan_opts: None = the library's choice by size, else
     True / False): split, vtq_from_update, vtq_in_aux, rmax_direct,
-    narrow_tiles; tile_w (None, 96, 128 or 160) -- implementation variants of
-    the same step."""
+    narrow_tiles, r_headroom; tile_w (None, 96, 128 or 160) -- implementation
+    variants of the same step."""
 
-    OPTS = ("split", "vtq_from_update", "vtq_in_aux", "rmax_direct", "narrow_tiles", "tile_w")
+    OPTS = ("split", "vtq_from_update", "vtq_in_aux", "rmax_direct", "narrow_tiles", "tile_w", "r_headroom")
 
     def __init__(self, index: SosIndex, r: int, **opts):
         bad = set(opts) - set(self.OPTS)

@@ -242,9 +242,9 @@ static bool pick(int opt, bool dflt) { return opt < 0 ? dflt : opt != 0; }
 
 int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts, sos_plan** out) {
     if (!h || !out || r < 1) return fail(SOS_ERR_ARG, "bad argument");
-    sos_plan_opts o = {-1, -1, -1, -1, -1, -1};
+    sos_plan_opts o = {-1, -1, -1, -1, -1, -1, -1};
     if (opts) o = *opts;
-    for (int v : {o.split, o.vtq_from_update, o.vtq_in_aux, o.rmax_direct, o.narrow_tiles})
+    for (int v : {o.split, o.vtq_from_update, o.vtq_in_aux, o.rmax_direct, o.narrow_tiles, o.r_headroom})
         if (v < -1 || v > 1) return fail(SOS_ERR_ARG, "sos_plan_opts fields must be -1, 0 or 1");
     if (!(o.tile_w == -1 || o.tile_w == 0 || o.tile_w == 96 || o.tile_w == 128 || o.tile_w == 160))
         return fail(SOS_ERR_ARG, "sos_plan_opts.tile_w must be -1 (auto), 96, 128 or 160");
@@ -284,6 +284,7 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
     // extra slicing work hides under a tile's MMAs (long K); for short K it
     // would lengthen the update-bound backward (profiles/r1_vtq_next_ab.log)
     P.vtq_from_update = !P.split && pick(o.vtq_from_update, P.nkbN >= 128);
+    P.r_headroom = !P.split && pick(o.r_headroom, true);
     P.vtq_in_aux = pick(o.vtq_in_aux, vtq_fits_aux(P));
     P.rmax_direct = pick(o.rmax_direct, rmax_direct_default(h->ix));
     if (P.split) P.mid_grid = mid_grid_for(P.nkbN, P.rowsVT, M, sms, &P.mid_tiles);
@@ -307,7 +308,9 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
         (rc = dalloc(&P.d_tiles_bwd, std::max<size_t>(1, tb.size()) * sizeof(TileCoord))) ||
         (rc = dalloc(&P.d_rowsig, std::max<size_t>(1, P.sig_expect.size()) * sizeof(unsigned))) ||
         (P.split && (rc = dalloc(&P.d_grad, (size_t)N * r * sizeof(float)))) ||
-        (P.split && (rc = dalloc(&P.d_part, (size_t)2 * std::max(P.mid_grid, 1) * sizeof(double))))) {
+        (P.split && (rc = dalloc(&P.d_part, (size_t)2 * std::max(P.mid_grid, 1) * sizeof(double)))) ||
+        (P.r_headroom && (rc = dalloc(&P.d_rrowx, (size_t)2 * Np * sizeof(unsigned)))) ||
+        (P.r_headroom && (rc = dalloc(&P.d_urowr, (size_t)Np * sizeof(unsigned))))) {
         sos_plan_destroy(pl);
         return rc;
     }
@@ -323,7 +326,9 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
         cudaMemset(P.d_rq, 0, (size_t)kSlices * P.nkbN * Np * 64) != cudaSuccess ||  // padding rows stay 0
         cudaMemset(P.d_progress, 0, 2 * sizeof(unsigned long long)) != cudaSuccess ||  // GEMMs reset it themselves
         cudaMemset(P.d_dbuf, 0, (size_t)(4 * P.rowsV + 4 * P.rowsVT) * 4) != cudaSuccess ||
-        cudaMemset(P.d_opt, 0, sizeof(DevOpt)) != cudaSuccess) {
+        cudaMemset(P.d_opt, 0, sizeof(DevOpt)) != cudaSuccess ||
+        (P.r_headroom && (cudaMemset(P.d_rrowx, 0, (size_t)2 * Np * 4) != cudaSuccess ||
+                          cudaMemset(P.d_urowr, 0, (size_t)Np * 4) != cudaSuccess))) {
         sos_plan_destroy(pl);
         return fail(SOS_ERR_CUDA, "workspace init");
     }
@@ -371,6 +376,8 @@ int sos_plan_destroy(sos_plan* pl) {
     cudaFree(P.d_rowsig);
     cudaFree(P.d_grad);
     cudaFree(P.d_part);
+    cudaFree(P.d_rrowx);
+    cudaFree(P.d_urowr);
     if (P.copy_st) cudaStreamDestroy(P.copy_st);
     if (P.sig_ev) cudaEventDestroy(P.sig_ev);
     if (P.timing) {
@@ -608,13 +615,26 @@ static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const fl
     launch_residual(P, P.d_coef, p, P.d_res, st);
     // t += 1, losses[k] = L(V_t) (the call's array, from DevOpt); clear the next
     // maxima and the coefficient accumulator (read by the residual, done)
+    // R slices: after the first step of a call with the previous step's exact R
+    // row maxima (x kHeadroom, rare rows re-sliced: no DP on the step); the
+    // first step computes them exactly (DP or direct pass) and keeps them
+    const bool hr = P.r_headroom && !first;
+    unsigned* rr_cur = P.d_rrowx + (size_t)b * P.idx->Np;
+    unsigned* rr_prev = P.d_rrowx + (size_t)(b ^ 1) * P.idx->Np;
     launch_step_begin(P, nullptr, st, true, d.vrowx[b ^ 1], P.rowsV, d.vcol[b ^ 1], P.rowsVT, P.d_coef,
-                      P.rmax_direct);
-    launch_pack_r(P, P.d_res, st, 1, P.rmax_direct);
-    const DescendBufs db = vu ? DescendBufs{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1], d.ucol[b],
-                                            d.tmap_vtq[b], d.vtq[b ^ 1]}
-                              : DescendBufs{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1], d.vcol[b],
-                                            P.tmap_vtq_b, nullptr};
+                      hr ? rr_cur : P.rmax_direct ? P.d_rrow : nullptr);
+    if (hr) {
+        launch_pack_r_headroom(P, P.d_res, rr_prev, rr_cur, P.d_urowr, st);
+    } else {
+        launch_pack_r(P, P.d_res, st, 1, P.rmax_direct);
+        if (P.r_headroom)  // the next step's previous maxima
+            CK(cudaMemcpyAsync(rr_cur, P.d_rrow, (size_t)P.idx->Np * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    DescendBufs db = vu ? DescendBufs{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1], d.ucol[b],
+                                      d.tmap_vtq[b], d.vtq[b ^ 1], nullptr}
+                        : DescendBufs{d.vrowx[b], d.vcol[b], d.vrowx[b ^ 1], d.vcol[b ^ 1], d.vcol[b],
+                                      P.tmap_vtq_b, nullptr, nullptr};
+    if (hr) db.urow_r = P.d_urowr;
     launch_gemm_bwd_update(P, V, st, &db);
     launch_descend_fixup(P, V, d.vrowx[b], d.vrowx[b ^ 1], d.urow[b], d.urow[b ^ 1], d.vcol[b], d.vcol[b ^ 1],
                          d.ucol[b ^ 1], vu ? d.vtq[b ^ 1] : nullptr, st);

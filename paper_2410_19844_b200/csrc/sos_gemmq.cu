@@ -857,6 +857,7 @@ void launch_gemm_bwd(Plan& P, float* grad, cudaStream_t st, const unsigned* vcol
 // GEMM reads the packed copy VTQ, never V, so updating V in place is safe.
 void launch_gemm_bwd_update(Plan& P, float* V, cudaStream_t st, const DescendBufs* db) {
     GemmArgs a = bwd_args(P, db ? db->ucol_cur : nullptr);
+    if (db && db->urow_r) a.umaxA = db->urow_r;
     if (db) {
         a.vq_next = P.d_vq;
         a.rowsV = P.rowsV;

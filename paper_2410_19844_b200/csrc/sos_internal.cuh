@@ -165,11 +165,14 @@ struct Plan {
     bool vtq_in_aux;       // the forward's aux warps write VTQ (else k_pack_vtq before it)
     bool rmax_direct;      // R row maxima by one gather pass over PT (else the lattice DP)
     bool narrow;           // narrow tiles at ragged column blocks
+    bool r_headroom;       // sos_descend, fused step: R slices with the previous step's scales (no DP)
     int tile_w_fwd;        // column tile width of the forward / backward GEMM (160, or 128 for
     int tile_w_bwd;        // small problems; the backward only in split plans)
     int mid_grid;          // cooperative grid of k_mid (co-resident blocks)
     int mid_tiles;         // R blocks each k_mid block holds in shared memory
     double* d_part;        // k_mid's per-block partial sums [mid_grid][2]
+    unsigned* d_rrowx;     // sos_descend, long K: [2][Np] exact R row maxima (step parity)
+    unsigned* d_urowr;     // [Np] scales the RQ rows were written with (headroom or exact)
     float* d_grad;         // N x r gradient buffer of the split step
     uint8_t* d_rq;    // RQ
     unsigned* d_vrow; // max_k |V_ik| (float bits), rowsV
@@ -264,15 +267,20 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow = nu
 void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st, const unsigned* vcol = nullptr);
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st);
 // losses_from_opt: record into the loss array set for the current sos_descend call;
-// zero0 / zero1 (n0 / n1 words), zero_coef (M floats), zero_rrow (the R row
-// maxima): accumulators to clear for the next stage
+// zero0 / zero1 (n0 / n1 words), zero_coef (M floats), zero_r (Np words, R row
+// maxima accumulated by atomicMax): accumulators to clear for the next stage
 void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt = false,
                        unsigned* zero0 = nullptr, int64_t n0 = 0, unsigned* zero1 = nullptr, int64_t n1 = 0,
-                       float* zero_coef = nullptr, bool zero_rrow = false);
+                       float* zero_coef = nullptr, unsigned* zero_r = nullptr);
 void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop, bool rrow_zeroed = false);
 void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop);
 // maxima + RQ; rrow_zeroed: rrow already cleared on the stream (direct maxima)
 void launch_pack_r(Plan& P, const float* res, cudaStream_t st, int use_stop, bool rrow_zeroed = false);
+// sos_descend after its first step (long K): RQ sliced with kHeadroom x the
+// previous step's exact R row maxima, this step's exact maxima into rrow_cur
+// (cleared before), rows outside the window re-sliced; urow_r = scale per row
+void launch_pack_r_headroom(Plan& P, const float* res, const unsigned* rrow_prev, unsigned* rrow_cur,
+                            unsigned* urow_r, cudaStream_t st);
 // the cost model choosing the direct R maxima pass over the lattice DP
 bool rmax_direct_default(const Index& ix);
 // sos_descend: maxima buffers of the current and the next step
@@ -284,6 +292,7 @@ struct DescendBufs {
     const unsigned* ucol_cur;  // column scales the current VTQ was written with (backward B unscale)
     const uint8_t* tmap_vtq_cur;  // tensor map of the current VTQ buffer
     uint8_t* vtq_next;         // VTQ buffer the update writes for the next step
+    const unsigned* urow_r;    // scales the RQ rows were written with (nullptr: the exact rrow)
 };
 // plans with fewer K-blocks (N / 64) than this use the split step (Plan::split)
 constexpr int kSplitKb = 48;

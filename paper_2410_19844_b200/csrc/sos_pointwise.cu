@@ -225,10 +225,17 @@ __global__ void __launch_bounds__(256) k_rmax(const uint32_t* __restrict__ pt, c
 // K-block J and rows of J at K-block I (the transposed tile) -- are written from
 // it, so PT and the res gathers are read once for two blocks.  RQ rows at or
 // beyond nkb * 64 (padding of Np) are never written: zeroed at plan creation.
+// kHr (inside sos_descend after its first step): the row scales are not known
+// yet -- the slices use kHeadroom x the previous step's exact row maximum
+// (rrow_prev), and the exact maxima of this step's R rows are folded into
+// rrow_out (atomicMax, cleared by k_step_begin) from the tiles already in shared
+// memory; k_rfix then re-slices the rare rows whose maximum left [u/4, u].
+// This takes the lattice DP (0.32 ms at config 4) off the step.
+template <bool kHr>
 __global__ void __launch_bounds__(256, 6) k_pack_rq_sym(const uint32_t* __restrict__ pt, const float* __restrict__ res,
                                                      int64_t Np, int64_t nkb, const unsigned* __restrict__ rrow,
                                                      uint8_t* __restrict__ RQ, const Scalars* sc, const DevOpt* opt,
-                                                     int use_stop) {
+                                                     int use_stop, unsigned* __restrict__ rrow_out) {
     if (descent_stopped(sc, opt, use_stop)) return;
     __shared__ float tile[kPtW][kPtW + 1];  // [row in I][j in J], padded
     const int t = threadIdx.x;
@@ -254,20 +261,85 @@ __global__ void __launch_bounds__(256, 6) k_pack_rq_sym(const uint32_t* __restri
         const int r = t >> 2, c = t & 3;
         float x[16];
         uint4 q[3];
+        float mr = 0.f;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) x[e] = tile[r][c * 16 + e];
-        slice16(x, slice_scale(__ldg(rrow + I * kPtW + r)), q);
+        for (int e = 0; e < 16; ++e) {
+            x[e] = tile[r][c * 16 + e];
+            if (kHr) mr = fmaxf(mr, fabsf(x[e]));
+        }
+        const unsigned urI = kHr ? __float_as_uint(kHeadroom * __uint_as_float(__ldg(rrow + I * kPtW + r)))
+                                 : __ldg(rrow + I * kPtW + r);
+        slice16(x, slice_scale(urI), q);
         store_q16(RQ, J, I * kPtW + r, c, nkb, Np, q);
+        float mc = 0.f;
         if (I != J) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) x[e] = tile[c * 16 + e][r];
-            slice16(x, slice_scale(__ldg(rrow + J * kPtW + r)), q);
+            for (int e = 0; e < 16; ++e) {
+                x[e] = tile[c * 16 + e][r];
+                if (kHr) mc = fmaxf(mc, fabsf(x[e]));
+            }
+            const unsigned urJ = kHr ? __float_as_uint(kHeadroom * __uint_as_float(__ldg(rrow + J * kPtW + r)))
+                                     : __ldg(rrow + J * kPtW + r);
+            slice16(x, slice_scale(urJ), q);
             store_q16(RQ, I, J * kPtW + r, c, nkb, Np, q);
+        }
+        if (kHr) {  // exact maxima: rows of I over J's columns, rows of J over I's (4 threads per line)
+            mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 1));
+            mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 2));
+            mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, 1));
+            mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, 2));
+            if (c == 0) {
+                if (mr > 0.f) atomicMax(rrow_out + I * kPtW + r, __float_as_uint(mr));
+                if (I != J && mc > 0.f) atomicMax(rrow_out + J * kPtW + r, __float_as_uint(mc));
+            }
         }
         __syncthreads();
     }
 }
 
+// After k_pack_rq_sym<true>: row i's slices used u = kHeadroom * (previous
+// exact maximum); they are exact to ~22 bits while the new exact maximum lies
+// in [u/4, u] (the same window as V's, k_descend_fixup).  Outside it -- growth
+// beyond the headroom would overflow the top slice, a large shrink loses bits,
+// and the first step after a zero row -- one warp re-gathers row i through PT
+// and re-slices it with the exact maximum.  urow_r receives the scale each RQ
+// row was written with (the backward's A unscale).  A stopped descent carries
+// the previous maxima over (no backward runs).
+__global__ void __launch_bounds__(256) k_rfix(const uint32_t* __restrict__ pt, const float* __restrict__ res,
+                                              int64_t N, int64_t Np, int64_t nkb, const unsigned* __restrict__ rrow_prev,
+                                              unsigned* __restrict__ rrow_cur, unsigned* __restrict__ urow_r,
+                                              uint8_t* __restrict__ RQ, const Scalars* sc, const DevOpt* opt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (descent_stopped(sc, opt, 1)) {
+        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < Np; e += (int64_t)gridDim.x * blockDim.x)
+            rrow_cur[e] = rrow_prev[e];
+        return;
+    }
+    for (int64_t i = warp; i < N; i += nwarps) {
+        const float u = kHeadroom * __uint_as_float(rrow_prev[i]);
+        const unsigned mb = rrow_cur[i];
+        const float mx = __uint_as_float(mb);
+        const bool keep = mx <= u && mx >= 0.25f * u;
+        if (lane == 0) urow_r[i] = keep ? __float_as_uint(u) : mb;
+        if (keep) continue;
+        const float cs = slice_scale(mb);
+        for (int64_t cc = lane; cc < nkb * 4; cc += 32) {  // 16-column chunks of row i
+            const int64_t j0 = cc * 16;
+            float x[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int64_t j = j0 + e;
+                const uint32_t k = j < N ? pt[pt_entry_sym(i, j)] : kInvalidRank;
+                x[e] = k != kInvalidRank ? res[k] : 0.f;
+            }
+            uint4 q[3];
+            slice16(x, cs, q);
+            store_q16(RQ, cc >> 2, i, (int)(cc & 3), nkb, Np, q);
+        }
+    }
+}
 
 // -------------------------------------------------------------- launches ---
 static int grid_for(const Plan& P, int64_t work, int threads, int per_sm = 8) {
@@ -800,16 +872,16 @@ void launch_mid(Plan& P, const float* p, const float* V, unsigned* vcol, bool co
 }
 
 void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt, unsigned* zero0, int64_t n0,
-                       unsigned* zero1, int64_t n1, float* zero_coef, bool zero_rrow) {
+                       unsigned* zero1, int64_t n1, float* zero_coef, unsigned* zero_r) {
     LaunchScope ls(P, KK_UPDATE, st);
     const int64_t nc = zero_coef ? P.idx->M : 0;
-    const int64_t n2 = zero_rrow ? P.idx->Np : 0;
+    const int64_t n2 = zero_r ? P.idx->Np : 0;
     if (!zero0) n0 = 0;
     if (!zero1) n1 = 0;
     const int64_t nz = n0 + n1 + n2;
     const int blocks = nz || nc ? grid_for(P, std::max<int64_t>(nz, nc / 4), 256, 4) : 1;
     k_step_begin<<<blocks, 256, 0, st>>>(P.d_opt, P.d_scal, losses_from_opt ? nullptr : losses, losses_from_opt ? 1 : 0,
-                                         zero0, n0, zero1, n1, P.d_rrow, n2, zero_coef, nc);
+                                         zero0, n0, zero1, n1, zero_r, n2, zero_coef, nc);
 }
 
 // maxima (one read of V) + VQ (one elementwise pass)
@@ -854,8 +926,23 @@ void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     LaunchScope ls(P, KK_PACK_R, st);
     const int64_t npairs = P.nkbN * (P.nkbN + 1) / 2;
     const unsigned blocks = (unsigned)std::min<int64_t>(npairs, (int64_t)P.num_sms * 8);
-    k_pack_rq_sym<<<blocks, 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow, P.d_rq, P.d_scal, P.d_opt,
-                                          use_stop);
+    k_pack_rq_sym<false><<<blocks, 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow, P.d_rq, P.d_scal, P.d_opt,
+                                                 use_stop, nullptr);
+}
+
+void launch_pack_r_headroom(Plan& P, const float* res, const unsigned* rrow_prev, unsigned* rrow_cur,
+                            unsigned* urow_r, cudaStream_t st) {
+    const int64_t Np = P.idx->Np;
+    {
+        LaunchScope ls(P, KK_PACK_R, st);
+        const int64_t npairs = P.nkbN * (P.nkbN + 1) / 2;
+        const unsigned blocks = (unsigned)std::min<int64_t>(npairs, (int64_t)P.num_sms * 8);
+        k_pack_rq_sym<true><<<blocks, 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, rrow_prev, P.d_rq, P.d_scal,
+                                                    P.d_opt, 1, rrow_cur);
+    }
+    LaunchScope ls(P, KK_ABSMAX_R, st);
+    k_rfix<<<grid_for(P, P.idx->N * 32, 256), 256, 0, st>>>(P.idx->d_pt, res, P.idx->N, Np, P.nkbN, rrow_prev,
+                                                              rrow_cur, urow_r, P.d_rq, P.d_scal, P.d_opt);
 }
 
 

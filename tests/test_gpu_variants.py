@@ -140,3 +140,51 @@ def test_tile_width_128_vs_160(sos, ix):
     b = _run(sos, ix, tile_w=160)
     assert np.array_equal(a["grad"], b["grad"])
     _same_descent(a, b)
+
+
+def test_r_headroom_vs_exact(sos):
+    """Long-K descent (N = 8855, fused step): R sliced with 2x the previous
+    step's exact row maxima (k_pack_rq_sym<true> + k_rfix) vs exact maxima
+    every step (lattice DP).  The target p = 1.001 coef(V0) makes the first
+    residual tiny and GD (lr: the first step moves V by ~10 %) makes the next one
+    ~100x larger, so at the first headroom step every row leaves the window and
+    k_rfix re-slices all of them; later steps mostly keep their scales.  GD is
+    smooth in the gradient, so the two must agree to the slice precision."""
+    ix = sos.SosIndex(20, 4)
+    r = 96
+    V0 = torch.from_numpy(si.v0(ix.N, r, seed=31)).cuda()
+    probe = sos.SosPlan(ix, r, split=False)
+    coef0 = probe.forward(V0)
+    p = coef0 * 1.001
+    g0 = probe.backward(V0, coef0 - p)
+    lr = float(0.1 * V0.norm() / g0.norm())
+    probe.close()
+    out = []
+    for hr in (True, False):
+        plan = sos.SosPlan(ix, r, split=False, r_headroom=hr)
+        plan.opt_init("gd", lr)
+        V = V0.clone()
+        losses = plan.descend(V, p, 4).cpu().numpy()
+        out.append({"V3": V.cpu().numpy(), "dV": (V - V0).cpu().numpy(), "losses": losses})
+        plan.close()
+    assert out[1]["losses"][1] > 30 * out[1]["losses"][0]  # the residual grew: every row re-sliced
+    _same_descent(out[0], out[1], tol=1e-5, vtol=1e-6)
+
+
+def test_r_headroom_adam_vs_exact(sos):
+    """The same comparison on a planted target with Adam (the bench's setting)."""
+    ix = sos.SosIndex(20, 4)
+    r = 96
+    out = []
+    for hr in (True, False):
+        plan = sos.SosPlan(ix, r, split=False, r_headroom=hr)
+        V = torch.from_numpy(si.v0(ix.N, r, seed=31)).cuda()
+        W = torch.zeros(ix.N, r, device="cuda")
+        W[:, :48] = torch.from_numpy(si.planted_w(ix.N, 48, 32)).cuda()
+        p = plan.forward(W)
+        plan.opt_init("adam", 1e-3)
+        V3 = V.clone()
+        losses = plan.descend(V3, p, 5).cpu().numpy()
+        out.append({"V3": V3.cpu().numpy(), "dV": V3.cpu().numpy() - V.cpu().numpy(), "losses": losses})
+        plan.close()
+    _same_descent(out[0], out[1], tol=1e-4, vtol=3e-5)

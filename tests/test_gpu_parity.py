@@ -732,3 +732,25 @@ def test_descend_tiny_shapes_vs_oracle(sos, n, d, r, variant):
     Vo, Lo = o.descent(V0, p, "gd", 3, lr)
     assert rel_l2(Vd.cpu().numpy() - V0, Vo - V0) <= 1e-5
     assert np.allclose(ld, Lo[:3], rtol=1e-5)
+
+
+def test_forward_full_vector_config3(sos):
+    """BASELINE config 3 (N = r = 12376): the WHOLE coefficient vector (M =
+    1,352,078) against the oracle's pair loop, run on all host threads (~1 min
+    on the 16-core B200 host); relative L2 and the worst relative error over
+    the coefficients whose magnitude is at least the vector's rms."""
+    c = si.CONFIGS["c3_n12_2d12"]
+    o = oracle(c.n, c.d)
+    ix = sos.SosIndex(c.n, c.d)
+    plan = sos.SosPlan(ix, c.r)
+    V = si.v0(o.N, c.r, seed=3)
+    coef = plan.forward(torch.from_numpy(V).cuda()).cpu().numpy().astype(np.float64)
+    want = o.forward_threaded(V)
+    err = rel_l2(coef, want)
+    big = np.abs(want) >= np.sqrt(np.mean(want ** 2))
+    worst = float(np.max(np.abs(coef[big] - want[big]) / np.abs(want[big])))
+    print(f"config 3 full forward: rel L2 {err:.2e}, worst relative error on |coef| >= rms {worst:.2e}")
+    assert err <= REL_TOL
+    assert worst <= 1e-4
+    plan.close()
+    ix.close()

@@ -754,3 +754,21 @@ def test_forward_full_vector_config3(sos):
     assert worst <= 1e-4
     plan.close()
     ix.close()
+
+
+def test_backward_full_config2(sos):
+    """BASELINE config 2 (N = r = 2002): every row of 4RV against the oracle
+    (host threads), through the split plan's backward (128-wide column tiles)."""
+    c = si.CONFIGS["c2_n10_2d10"]
+    o = oracle(c.n, c.d)
+    ix = sos.SosIndex(c.n, c.d)
+    plan = sos.SosPlan(ix, c.r)
+    V = si.v0(o.N, c.r, seed=4)
+    res = si.residual_probe(o.M, seed=6)
+    g = plan.backward(torch.from_numpy(V).cuda(), torch.from_numpy(res).cuda()).cpu().numpy()
+    want = o.grad_rows_threaded(V.astype(np.float64), res, np.arange(o.N))
+    err = rel_l2(g, want)
+    print(f"config 2 full backward: rel L2 {err:.2e}")
+    assert err <= REL_TOL
+    plan.close()
+    ix.close()

@@ -26,6 +26,13 @@
  *     thread-local message.  On error no output is guaranteed to be written.
  *   - Requires a compute-capability 10.0 device (B200); there is no CPU path:
  *     without one every compute call returns SOS_ERR_DEVICE.
+ *   - Indexes and plans belong to the device that is current when they are
+ *     created; calls must be made with that device current.  Kernel launch
+ *     configurations (occupancy-derived grids, shared-memory attributes) are
+ *     cached once per process, so a process drives one device (bench.py runs
+ *     one process per GPU).
+ *   - Not thread-safe per plan: calls on one plan must not overlap; distinct
+ *     plans may be used from distinct host threads.
  */
 #ifndef SOS_B200_H
 #define SOS_B200_H

@@ -69,3 +69,39 @@ def test_fuzz_shape(sos, n, d, r):
     dv_s = Vs.cpu().numpy() - V
     dv_q = Vq.cpu().numpy() - V
     assert rel_l2(dv_q, dv_s) <= 1e-4
+
+
+def _variant_shapes(count=12, seed=77):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        n = int(rng.integers(2, 12))
+        d = int(rng.integers(1, 6))
+        N = math.comb(n + d - 1, d)
+        if N > 1200 or math.comb(n + 2 * d - 1, 2 * d) > 200_000:
+            continue
+        r = int(rng.integers(1, 600))
+        opts = [{"split": True}, {"split": False}, {"split": True, "tile_w": 128},
+                {"split": False, "rmax_direct": True, "vtq_from_update": True}][len(out) % 4]
+        out.append((n, d, r, opts))
+    return out
+
+
+@pytest.mark.parametrize("n,d,r,opts", _variant_shapes())
+def test_fuzz_descend_variants(sos, n, d, r, opts):
+    """Random shapes through sos_descend under each step variant (split step,
+    fused step, 128-wide tiles, direct R maxima + V^T slices from the update):
+    3 GD steps against the oracle's GD (V_3 - V_0 element-wise) and its losses."""
+    o = OracleIndex(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r, **opts)
+    V0 = si.v0(o.N, r, seed=n * 100 + r)
+    p = o.forward(si.planted_w(o.N, max(1, r // 3), seed=r + 1)).astype(np.float32)
+    _, g1, _, _ = o.loss_grad(V0, p)
+    lr = 0.02 * np.linalg.norm(V0) / max(np.linalg.norm(g1), 1e-30)
+    plan.opt_init("gd", lr)
+    Vd = torch.from_numpy(V0.copy()).cuda()
+    ld = plan.descend(Vd, torch.from_numpy(p).cuda(), 3).cpu().numpy()
+    Vo, Lo = o.descent(V0, p, "gd", 3, lr)
+    assert rel_l2(Vd.cpu().numpy() - V0, Vo - V0) <= 1e-5
+    assert np.allclose(ld, Lo[:3], rtol=1e-5)

@@ -266,7 +266,7 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
     P.narrow = pick(o.narrow_tiles, true);
     // short K: a tile's MMAs (~nkbN x 0.5 us) cannot hide the fused update
     // (~25 us per tile), so the split step stores the gradient and updates
-    // with all SMs (profiles/r1_update_split_ab.log, r2_split_step_ab.log)
+    // with all SMs (profiles/r1_update_split_ab.log, r2_split_vs_fused_shapes.log)
     P.split = pick(o.split, P.nkbN < kSplitKb);
     {
         // the fused update assumes every tile but a matrix-edge one is 160 wide, so

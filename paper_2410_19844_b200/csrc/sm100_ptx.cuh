@@ -98,6 +98,15 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// the same execution barrier without release semantics: it does not wait for
+// this thread's outstanding global stores / reductions to become visible (the
+// .release form emits MEMBAR.ALL.GPU -- at a GEMM's end that drained the last
+// tile's coefficient REDs before the CTA could exit).  Enough to order tcgen05
+// operations around it (tcgen05.fence::before/after_thread_sync); kernel
+// completion still publishes every store to the next grid.
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
 // arrive on the mbarrier at the same shared offset in CTA `cta` of the cluster
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
     asm volatile(

@@ -279,6 +279,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     extern __shared__ uint8_t smem_raw[];
 #ifdef SOS_EXPERIMENTS
     __shared__ unsigned long long tmark_s[10];
+    __shared__ unsigned long long wend_s[kGemmThreads / 32];
     if (threadIdx.x < 10) tmark_s[threadIdx.x] = 0;
     if (threadIdx.x == 0) GEMM_MARK(0);
 #endif
@@ -621,9 +622,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
 
     if (kExperiments && warp == 2 && lane == 0) GEMM_MARK(6);
+#ifdef SOS_EXPERIMENTS
+    if (args.trace && blockIdx.x < 2 && lane == 0) {  // per-warp end of the role loops, CTAs 0 and 1
+        unsigned long long now_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));
+        wend_s[warp] = now_;
+    }
+#endif
     tc_fence_before();
     __syncthreads();
-    cluster_sync();  // all MMAs consumed and both epilogues done before freeing TMEM
+    // all MMAs consumed and both epilogues' TMEM reads done before freeing TMEM
+    // (relaxed: no need to wait for the epilogues' global REDs / stores here)
+    cluster_sync_relaxed();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc_2sm(tbase, 512);
@@ -631,6 +641,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #ifdef SOS_EXPERIMENTS
     if (threadIdx.x == 0) {
         GEMM_MARK(7);
+        if (args.trace && blockIdx.x < 2) {
+            const unsigned long long t0 = wend_s[0];
+            double e[12];
+            for (int w = 0; w < 12; ++w) e[w] = (double)(long long)(wend_s[w] - t0) * 1e-3;
+            printf("k_gemmq<%d> cta%d warp ends rel. to warp 0 (us): %.2f %.2f %.2f %.2f %.2f %.2f %.2f %.2f %.2f "
+                   "%.2f %.2f %.2f\n", kMode, (int)blockIdx.x, e[0], e[1], e[2], e[3], e[4], e[5], e[6], e[7], e[8],
+                   e[9], e[10], e[11]);
+        }
         if (args.trace && blockIdx.x == 0) {
             const unsigned long long* m = tmark_s;
             printf("k_gemmq<%d> cta0 (us): setup %.2f | griddep %.2f | first operands %.2f | last commit %.2f | "

@@ -1,5 +1,5 @@
 """Device time per descent step for an arbitrary (n, d, r) (planted target, Adam):
-python tools/time_shape.py n d r [steps] [--kernels] [split=0|1 rmax_direct=0|1 ...]
+python tools/time_shape.py n d r [steps] [--kernels] [split=0|1 rmax_direct=0|1 ...] [lib=PATH]
 (key=value arguments are sos_plan_opts fields, for same-box A/B runs)"""
 import os, sys
 import numpy as np
@@ -10,10 +10,13 @@ import paper_2410_19844_b200 as sos
 if "--exp" in sys.argv:  # the -DSOS_EXPERIMENTS build (environment switches, probes, traces)
     from paper_2410_19844_b200 import build as _b
     sos.load(_b.build(experiments=True))
+for a in sys.argv:  # lib=PATH: an alternative build of the library (same-box A/B)
+    if a.startswith("lib="):
+        sos.load(a[4:])
 
 n, d, r = (int(x) for x in sys.argv[1:4])
 steps = int(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4].isdigit() else 20
-opts = {k: (int(v) if k == "tile_w" else bool(int(v))) for k, v in (a.split("=") for a in sys.argv[4:] if "=" in a)}
+opts = {k: (int(v) if k == "tile_w" else bool(int(v))) for k, v in (a.split("=") for a in sys.argv[4:] if "=" in a and not a.startswith("lib="))}
 ix = sos.SosIndex(n, d)
 plan = sos.SosPlan(ix, r, **opts)
 rs = max(1, ix.N // 2)

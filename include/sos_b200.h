@@ -115,9 +115,10 @@ int sos_plan_create(const sos_index *idx, int64_t r, sos_plan **out);
  *                 instead of the monomial-lattice DP (default by a cost model).
  *   narrow_tiles: tiles narrower than 160 columns where a column block is
  *                 partly outside the matrix (default 1).
- *   tile_w:       column tile width of the GEMMs, -1 or 0 = auto (160, or 128
- *                 for small problems where it saves a partial wave), else 96,
- *                 128 or 160; the backward uses it only in split plans.
+ *   tile_w:       column tile width of the GEMMs, -1 or 0 = auto (160, or
+ *                 narrower for small problems where it saves a partial wave),
+ *                 else a multiple of 16 in [32, 160]; the backward uses it
+ *                 only in split plans.
  *   r_headroom:   (split = 0, sos_descend) after the first step of a call the R
  *                 slices use 2x the previous step's exact R row maxima; the
  *                 packer takes this step's exact maxima on the fly and re-slices

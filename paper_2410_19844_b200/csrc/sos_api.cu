@@ -189,7 +189,9 @@ static int64_t tile_group() {
 #endif
     return 8;
 }
-static int round_up32(int64_t x) { return (int)std::max<int64_t>(32, (x + 31) / 32 * 32); }
+// MMA N of a tile: its live columns rounded up to 16 (UMMA M = 256 takes N % 16 == 0;
+// each CTA then supplies N/2 B rows, whole 8-row swizzle atoms)
+static int round_up16(int64_t x) { return (int)std::max<int64_t>(32, (x + 15) / 16 * 16); }
 
 // forward: upper triangle of the Gram matrix (columns j >= rows' block start);
 // backward: all of R V.  Columns tiled on a W grid (W = 160, or narrower for
@@ -207,31 +209,35 @@ static void build_tiles(int64_t row_blocks, int64_t ncols, bool upper, bool narr
                     c_start = std::max(c_start, a * kPairM);        // skip columns left of it
                 }
                 if (!narrow) c_start = b * W, c_end = c_start + W;  // A/B: full grid tiles
-                out.push_back(TileCoord{(int)a, (int)c_start, round_up32(c_end - c_start), 0});
+                out.push_back(TileCoord{(int)a, (int)c_start, round_up16(c_end - c_start), 0});
             }
     }
 }
 
-// Column tile width.  A GEMM of T tiles on P CTA pairs runs ceil(T / P) waves of
-// W-wide tiles, so its MMA time goes as ceil(T(W) / P) * W: a small problem
-// whose 160-wide tiles overflow one wave by a little does better with narrower
-// tiles (config 2 backward: 104 tiles of 160 = 2 waves, 128 tiles of 128 = 2
-// waves of 0.8 the time; forward: 56 -> 72 tiles, still one wave).  The int8
-// pair MMA runs at full rate down to N = 128 (profiles/r1_mma2_pair_N_sweep.log),
-// so only 160 and 128 are candidates, and only for problems of at most 4 waves
-// (more tiles re-read their A panels more often).  forced: sos_plan_opts.tile_w.
+// Column tile width.  A GEMM of T tiles on P CTA pairs runs ceil(T / P) waves,
+// and a wave of W-wide tiles takes ~W of MMA time plus a per-wave cost that does
+// not shrink with W (measured ~10 us at config 2b: 4 waves of 112 lose to 3 of
+// 160).  So the plan takes the narrowest width that does not add a wave to the
+// 160-wide tiling: config 2 backward 104 tiles of 160 -> 144 tiles of 112, both
+// 2 waves; forward 56 tiles of 160 -> 72 of 128, both one wave; config 1 one
+// wave at 160 or at 96.  The int8 pair MMA runs at full rate down to N = 128 and
+// loses little at 96 (profiles/r1_mma2_pair_N_sweep.log), so widths stop at 96
+// (multiples of 16: UMMA N with M = 256); only problems of at most 4 waves are
+// considered (more tiles re-read their A panels more often).  A/B:
+// profiles/r2_tile_width16_ab.log.  forced: sos_plan_opts.tile_w.
 static int pick_tile_width(int64_t row_blocks, int64_t ncols, bool upper, bool narrow, int pairs, int forced) {
     if (forced > 0) return forced;
-    auto cost = [&](int W, int64_t* waves) {
+    auto waves = [&](int W) {
         std::vector<TileCoord> t;
         build_tiles(row_blocks, ncols, upper, narrow, W, t);
-        *waves = ((int64_t)t.size() + pairs - 1) / pairs;
-        return *waves * W;
+        return ((int64_t)t.size() + pairs - 1) / pairs;
     };
-    int64_t w160 = 0, w128 = 0;
-    const int64_t c160 = cost(kTileN, &w160);
-    if (w160 > 4 || ncols <= 128) return kTileN;  // (<= 128 columns: the same single column block)
-    return cost(128, &w128) < c160 ? 128 : kTileN;
+    const int64_t w160 = waves(kTileN);
+    if (w160 > 4) return kTileN;
+    int bestW = kTileN;
+    for (int W = kTileN - 16; W >= 96; W -= 16)
+        if (waves(W) <= w160) bestW = W;
+    return bestW;
 }
 
 int sos_plan_create(const sos_index* h, int64_t r, sos_plan** out) {
@@ -246,8 +252,8 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
     if (opts) o = *opts;
     for (int v : {o.split, o.vtq_from_update, o.vtq_in_aux, o.rmax_direct, o.narrow_tiles, o.r_headroom})
         if (v < -1 || v > 1) return fail(SOS_ERR_ARG, "sos_plan_opts fields must be -1, 0 or 1");
-    if (!(o.tile_w == -1 || o.tile_w == 0 || o.tile_w == 96 || o.tile_w == 128 || o.tile_w == 160))
-        return fail(SOS_ERR_ARG, "sos_plan_opts.tile_w must be -1 (auto), 96, 128 or 160");
+    if (!(o.tile_w == -1 || o.tile_w == 0 || (o.tile_w >= 32 && o.tile_w <= kTileN && o.tile_w % 16 == 0)))
+        return fail(SOS_ERR_ARG, "sos_plan_opts.tile_w must be -1 / 0 (auto) or a multiple of 16 in [32, 160]");
     *out = nullptr;
     int sms = 0;
     int rc = require_device(&sms);

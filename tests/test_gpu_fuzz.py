@@ -82,7 +82,8 @@ def _variant_shapes(count=12, seed=77):
             continue
         r = int(rng.integers(1, 600))
         opts = [{"split": True}, {"split": False}, {"split": True, "tile_w": 128},
-                {"split": False, "rmax_direct": True, "vtq_from_update": True}][len(out) % 4]
+                {"split": False, "rmax_direct": True, "vtq_from_update": True},
+                {"split": True, "tile_w": 112}, {"split": False, "tile_w": 144}][len(out) % 6]
         out.append((n, d, r, opts))
     return out
 
@@ -90,7 +91,7 @@ def _variant_shapes(count=12, seed=77):
 @pytest.mark.parametrize("n,d,r,opts", _variant_shapes())
 def test_fuzz_descend_variants(sos, n, d, r, opts):
     """Random shapes through sos_descend under each step variant (split step,
-    fused step, 128-wide tiles, direct R maxima + V^T slices from the update):
+    fused step, 128 / 112 / 144-wide tiles, direct R maxima + V^T slices from the update):
     3 GD steps against the oracle's GD (V_3 - V_0 element-wise) and its losses."""
     o = OracleIndex(n, d)
     ix = sos.SosIndex(n, d)

@@ -132,12 +132,20 @@ def test_split_vs_fused_long_k(sos):
     _same_descent(out[0], out[1], tol=1e-4, vtol=3e-5)
 
 
-def test_tile_width_128_vs_160(sos, ix):
-    """Column tiles 128 wide (chosen automatically for small problems that would
-    run a partial second wave at 160) vs 160: the same integer products, so a
-    bit-identical plain backward; the descent agrees to fp32 rounding."""
-    a = _run(sos, ix, tile_w=128)
-    b = _run(sos, ix, tile_w=160)
+@pytest.fixture(scope="module")
+def run160(sos, ix):
+    return _run(sos, ix, tile_w=160)
+
+
+@pytest.mark.parametrize("w", [128, 112, 144, 96, 48])
+def test_tile_width_vs_160(sos, ix, run160, w):
+    """Column tiles W wide (narrower widths are chosen automatically for small
+    problems that would run a partial wave at 160; 112 and 144 are not multiples
+    of 32, so a CTA supplies an odd number of 8-row B atoms) vs 160: the same
+    integer products, so a bit-identical plain backward; the descent agrees to
+    fp32 rounding."""
+    a = _run(sos, ix, tile_w=w)
+    b = run160
     assert np.array_equal(a["grad"], b["grad"])
     _same_descent(a, b)
 
@@ -187,4 +195,8 @@ def test_r_headroom_adam_vs_exact(sos):
         losses = plan.descend(V3, p, 5).cpu().numpy()
         out.append({"V3": V3.cpu().numpy(), "dV": V3.cpu().numpy() - V.cpu().numpy(), "losses": losses})
         plan.close()
-    _same_descent(out[0], out[1], tol=1e-4, vtol=3e-5)
+    # Adam at the default eps with 5 steps: the forward's atomics reorder fp32 sums
+    # from run to run and Adam passes that rounding on unattenuated for entries with
+    # small |g| (R8); tools/hr_adam_probe.py measured V_5 1e-6 - 2.4e-5,
+    # dV 2e-6 - 4.4e-5 over 12 runs, so the bars are the R8 long-K ones
+    _same_descent(out[0], out[1], tol=2e-4, vtol=1e-4)

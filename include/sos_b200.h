@@ -117,7 +117,7 @@ int sos_plan_create(const sos_index *idx, int64_t r, sos_plan **out);
  *                 partly outside the matrix (default 1).
  *   tile_w:       column tile width of the GEMMs, -1 or 0 = auto (160, or
  *                 narrower for small problems where it saves a partial wave),
- *                 else a multiple of 16 in [32, 160]; the backward uses it
+ *                 else a multiple of 16 in [16, 160]; the backward uses it
  *                 only in split plans.
  *   r_headroom:   (split = 0, sos_descend) after the first step of a call the R
  *                 slices use 2x the previous step's exact R row maxima; the

@@ -159,7 +159,7 @@ class SosPlan:
 
     Keyword options (sos_plan_opts: None = the library's choice by size, else
     True / False): split, vtq_from_update, vtq_in_aux, rmax_direct,
-    narrow_tiles, r_headroom; tile_w (None, or a multiple of 16 in [32, 160]) -- implementation
+    narrow_tiles, r_headroom; tile_w (None, or a multiple of 16 in [16, 160]) -- implementation
     variants of the same step."""
 
     OPTS = ("split", "vtq_from_update", "vtq_in_aux", "rmax_direct", "narrow_tiles", "tile_w", "r_headroom")

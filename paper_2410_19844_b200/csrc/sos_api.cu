@@ -189,9 +189,10 @@ static int64_t tile_group() {
 #endif
     return 8;
 }
-// MMA N of a tile: its live columns rounded up to 16 (UMMA M = 256 takes N % 16 == 0;
-// each CTA then supplies N/2 B rows, whole 8-row swizzle atoms)
-static int round_up16(int64_t x) { return (int)std::max<int64_t>(32, (x + 15) / 16 * 16); }
+// MMA N of a tile: its live columns rounded up to 16 (UMMA M = 256 takes N % 16 == 0,
+// 16 <= N <= 256; each CTA then supplies N/2 B rows, whole 8-row swizzle atoms).
+// Never past the next multiple of 16: the next tile may start there.
+static int round_up16(int64_t x) { return (int)std::max<int64_t>(16, (x + 15) / 16 * 16); }
 
 // forward: upper triangle of the Gram matrix (columns j >= rows' block start);
 // backward: all of R V.  Columns tiled on a W grid (W = 160, or narrower for
@@ -235,7 +236,7 @@ static int pick_tile_width(int64_t row_blocks, int64_t ncols, bool upper, bool n
     const int64_t w160 = waves(kTileN);
     if (w160 > 4) return kTileN;
     int bestW = kTileN;
-    for (int W = kTileN - 16; W >= 96; W -= 16)
+    for (int W = kTileN - 16; W >= 16; W -= 16)
         if (waves(W) <= w160) bestW = W;
     return bestW;
 }
@@ -252,8 +253,8 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
     if (opts) o = *opts;
     for (int v : {o.split, o.vtq_from_update, o.vtq_in_aux, o.rmax_direct, o.narrow_tiles, o.r_headroom})
         if (v < -1 || v > 1) return fail(SOS_ERR_ARG, "sos_plan_opts fields must be -1, 0 or 1");
-    if (!(o.tile_w == -1 || o.tile_w == 0 || (o.tile_w >= 32 && o.tile_w <= kTileN && o.tile_w % 16 == 0)))
-        return fail(SOS_ERR_ARG, "sos_plan_opts.tile_w must be -1 / 0 (auto) or a multiple of 16 in [32, 160]");
+    if (!(o.tile_w == -1 || o.tile_w == 0 || (o.tile_w >= 16 && o.tile_w <= kTileN && o.tile_w % 16 == 0)))
+        return fail(SOS_ERR_ARG, "sos_plan_opts.tile_w must be -1 / 0 (auto) or a multiple of 16 in [16, 160]");
     *out = nullptr;
     int sms = 0;
     int rc = require_device(&sms);

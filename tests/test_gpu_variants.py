@@ -200,3 +200,25 @@ def test_r_headroom_adam_vs_exact(sos):
     # small |g| (R8); tools/hr_adam_probe.py measured V_5 1e-6 - 2.4e-5,
     # dV 2e-6 - 4.4e-5 over 12 runs, so the bars are the R8 long-K ones
     _same_descent(out[0], out[1], tol=2e-4, vtol=1e-4)
+
+
+@pytest.mark.parametrize("w", [16, 32, 48, 80, 112])
+def test_forward_tile_width_vs_160(sos, w):
+    """The forward's upper-triangle tiling at widths that do not divide 256: the
+    diagonal tile of row block a starts at column 256a and may hold only 16 live
+    columns (W = 48, a = 2: columns 512..527), so its MMA N must stop at the next
+    multiple of 16, where the following tile starts.  N = 1001 (4 row blocks):
+    the coefficient vectors agree to fp32 rounding (the scatter's atomics add in
+    another order) and the backward is bit-identical."""
+    ix = sos.SosIndex(11, 4)
+    r = 300
+    V = torch.from_numpy(si.v0(ix.N, r, seed=41)).cuda()
+    res = torch.from_numpy(si.residual_probe(ix.M, seed=42)).cuda()
+    out = []
+    for tw in (w, 160):
+        plan = sos.SosPlan(ix, r, tile_w=tw, split=True)
+        out.append((plan.forward(V).cpu().numpy().astype(np.float64), plan.backward(V, res).cpu().numpy()))
+        plan.close()
+    (ca, ga), (cb, gb) = out
+    assert np.linalg.norm(ca - cb) / np.linalg.norm(cb) <= 1e-6
+    assert np.array_equal(ga, gb)

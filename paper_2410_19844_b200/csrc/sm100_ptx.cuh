@@ -144,6 +144,8 @@ __device__ __forceinline__ void tma_load_3d_2sm(void* smem_dst, const void* tmap
         "l"(tmap), "r"(mbar), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+// the 128-byte line at p into L2
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }

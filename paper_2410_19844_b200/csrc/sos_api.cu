@@ -294,7 +294,7 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
     P.r_headroom = !P.split && pick(o.r_headroom, true);
     P.vtq_in_aux = pick(o.vtq_in_aux, vtq_fits_aux(P));
     P.rmax_direct = pick(o.rmax_direct, rmax_direct_default(h->ix));
-    if (P.split) P.mid_grid = mid_grid_for(P.nkbN, P.rowsVT, M, sms, &P.mid_tiles);
+    if (P.split) P.mid_grid = mid_grid_for(P.nkbN, P.rowsVT, M, sms, &P.mid_tiles, &P.mid_hold_v);
     // row chunks of the last step's V release = the raster's row groups
     P.sig_blocks = (int)tile_group();
     P.sig_expect.assign((size_t)((Np / kPairM + P.sig_blocks - 1) / P.sig_blocks), 0u);

@@ -743,7 +743,12 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
         configured = true;
     }
     int sms = resident_ctas<kMode>(P.num_sms);
-    a.skew_epoch = kSkewEpoch;
+    // bounded K-skew only when the operands do not fit in L2 anyway: for short K
+    // (both operand tensors <= kSkewMinBytes) the pacing is a soft grid barrier
+    // every kSkewEpoch K-blocks with nothing to gain (config 2: -5 % step time
+    // without it, profiles/r2_short_k_ab.log)
+    const bool pace = (double)(a.a_rows + a.b_rows) * a.num_kb * 64 * kSlices > kSkewMinBytes;
+    a.skew_epoch = pace ? kSkewEpoch : 1 << 30;
     a.skew_lag = kSkewLag;
     a.skew_sleep = 256;
     a.kserp = 1;

@@ -65,6 +65,7 @@ constexpr int kPtW = 64;          // pair-rank table block width (64 x 64 blocks
 // bounded K-skew between the CTAs of a GEMM (see the producer in sos_gemmq.cu)
 constexpr int kSkewEpoch = 8;     // K-blocks (of 64) per progress epoch (tools/gpu_skew2.sh)
 constexpr int kSkewLag = 1;       // epochs a CTA may run ahead of the slowest
+constexpr double kSkewMinBytes = 64.0 * (1 << 20);  // operand bytes (A + B slices) below which no pacing
 constexpr int kSkewMaxSpin = 8192;  // bounded wait (polls): a locality hint, never a deadlock
 constexpr uint32_t kInvalidRank = 0xFFFFFFFFu;
 constexpr int kMaxVars = 255;     // n + 2d <= 255 (variable indices are uint8)
@@ -91,15 +92,23 @@ struct DevOpt {
                             // step graph does not depend on it)
     float lr_c1;            // Adam constants of step t (device-managed, advance_step):
     float inv_sqrt_c2;      //   lr / (1 - b1^t) and 1 / sqrt(1 - b2^t)
+    double b1t, b2t;        // b1^t, b2^t as running products (device-managed; t = 0 after the
+                            // memset of sos_opt_init, when they are not read)
 };
 
 // t += 1 and the bias-correction constants of the new step (one thread, once per
 // step, before any update of that step reads them)
 __device__ __forceinline__ void advance_step(DevOpt* opt) {
     const long long t = opt->t + 1;
+    // b^t by one multiplication per step (two fp64 pow calls were ~2 us of one
+    // thread on the step's critical path); relative drift <= t * 2^-53
+    const double b1t = t == 1 ? (double)opt->b1 : opt->b1t * (double)opt->b1;
+    const double b2t = t == 1 ? (double)opt->b2 : opt->b2t * (double)opt->b2;
     opt->t = t;
-    opt->lr_c1 = (float)((double)opt->lr / (1.0 - pow((double)opt->b1, (double)t)));
-    opt->inv_sqrt_c2 = (float)(1.0 / sqrt(1.0 - pow((double)opt->b2, (double)t)));
+    opt->b1t = b1t;
+    opt->b2t = b2t;
+    opt->lr_c1 = (float)((double)opt->lr / (1.0 - b1t));
+    opt->inv_sqrt_c2 = (float)(1.0 / sqrt(1.0 - b2t));
 }
 
 // the device-side stopping rule of sos_step (sos_opt_set_stop), read after
@@ -170,6 +179,7 @@ struct Plan {
     int tile_w_bwd;        // small problems; the backward only in split plans)
     int mid_grid;          // cooperative grid of k_mid (co-resident blocks)
     int mid_tiles;         // R blocks each k_mid block holds in shared memory
+    int mid_hold_v;        // V tiles each k_mid block holds from its phase A to B
     double* d_part;        // k_mid's per-block partial sums [mid_grid][2]
     unsigned* d_rrowx;     // sos_descend, long K: [2][Np] exact R row maxima (step parity)
     unsigned* d_urowr;     // [Np] scales the RQ rows were written with (headroom or exact)
@@ -310,7 +320,7 @@ void launch_mid(Plan& P, const float* p, const float* V, unsigned* vcol, bool co
 void launch_update_rows(Plan& P, float* V, uint8_t* vq_next, const unsigned* vrow_cur, unsigned* vrow_next,
                         cudaStream_t st);
 // cooperative grid of k_mid (blocks) and the R blocks each holds (tiles_per_block)
-int mid_grid_for(int64_t nkbN, int64_t rowsVT, int64_t M, int num_sms, int* tiles_per_block);
+int mid_grid_for(int64_t nkbN, int64_t rowsVT, int64_t M, int num_sms, int* tiles_per_block, int* hold_v);
 // slices written by the update use kHeadroom x the current row maximum
 constexpr float kHeadroom = 2.f;
 

@@ -586,6 +586,8 @@ struct MidArgs {
     unsigned* zero_cols;
     double* part;  // [gridDim][2] per-block partial sums of the loss and |p|^2
     int hold;   // every block holds its R blocks from phase B to C (else C gathers them again)
+    int r_slots;  // shared-memory tiles before the held V tiles (max(R blocks held, 1))
+    int hold_v;   // V tiles every block holds from phase A to B (0: phase B reads V again)
     int trace;  // experiment build only
 };
 
@@ -600,6 +602,7 @@ __device__ __forceinline__ void block_pair(int64_t pr, int64_t& I, int64_t& J) {
 constexpr int kMidThreads = 256;
 constexpr size_t kMidTileBytes = (size_t)kPtW * (kPtW + 1) * sizeof(float);
 constexpr int kMidMaxHeld = 12;  // R blocks a k_mid block can hold in shared memory (~200 KB)
+constexpr int kMidMaxHeldV = 4;  // V tiles a k_mid block can hold from phase A to B
 
 // the 64 x 64 block {I <= J} of R (I's rows x J's columns) gathered through the
 // stored PT block into a padded shared-memory tile (plain loads: res is written
@@ -631,7 +634,7 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
 #ifdef SOS_EXPERIMENTS
-    unsigned long long tmark[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long tmark[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
     MID_MARK(0);
     extern __shared__ float smem_tiles[];  // R blocks held from phase B to C, 64 x 65 floats each
@@ -639,8 +642,22 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
     float(*tile0)[kPtW + 1] = reinterpret_cast<float(*)[kPtW + 1]>(smem_tiles);
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + t, gstride = (int64_t)gridDim.x * blockDim.x;
+    __shared__ float cpart[2][4][64];  // column maxima of two held V tiles, per 16-row group
+    const double tol = a.opt->stop_tol;  // constant during the kernel: loaded up front
+    // the step's bookkeeping (t += 1, the Adam constants, the loss record) is done
+    // by the last block, which has the least work, at its very end (step_record)
     // ---- A
     {
+        // this block's PT blocks into L2 now (read after the barrier; PT does not
+        // stay in L2 across the GEMMs of a step)
+        if (t < 128) {
+            const int64_t npairs = a.nkbN * (a.nkbN + 1) / 2;
+            for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+                int64_t I, J;
+                block_pair(pr, I, J);
+                prefetch_l2(a.pt + pt_entry(I * kPtW, J * kPtW) + t * 32);
+            }
+        }
         double l = 0.0, pn = 0.0;
         for (int64_t e = gtid; e < a.M; e += gstride) {
             const float pv = a.p[e];
@@ -663,10 +680,53 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
                 a.part[2 * blockIdx.x + 1] = pn;
             }
         }
+        MID_MARK(9);
         for (int64_t e = gtid; e < a.Np; e += gstride) a.rrow[e] = 0u;
         if (a.zero_cols)
             for (int64_t e = gtid; e < a.rowsVT; e += gstride) a.zero_cols[e] = 0u;
-        if (a.colmax) {
+        if (a.hold_v) {
+            // this block's V tiles (64 rows j x 64 columns k of V; tile b = jb * nkt + kt,
+            // b = blockIdx.x + h * gridDim.x) are read once, here, into shared memory and
+            // sliced from there in phase B; two tiles' loads are in flight together and
+            // the column maxima come from the registers (thread = column t & 63 of rows
+            // (t >> 6) + 4u, the same element order as pack_vtq_tile)
+            const int64_t nkt = (a.rowsVT + 63) / 64, ntv = a.nkbN * nkt;
+            float* vt = smem_tiles + (size_t)a.r_slots * kPtW * (kPtW + 1);
+            const int c = t & 63, g = t >> 6;
+            for (int h0 = 0; h0 < a.hold_v; h0 += 2) {
+                float x[2][16];
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int64_t b = blockIdx.x + (int64_t)(h0 + hh) * gridDim.x;
+                    const bool live = h0 + hh < a.hold_v && b < ntv;
+                    const int64_t j0 = (b / nkt) * 64 + g, k = (b % nkt) * 64 + c;
+#pragma unroll
+                    for (int u = 0; u < 16; ++u)
+                        x[hh][u] = live && j0 + 4 * u < a.N && k < a.r ? __ldg(a.V + (j0 + 4 * u) * a.r + k) : 0.f;
+                }
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    if (h0 + hh >= a.hold_v) break;
+                    float(*tl)[kPtW + 1] = reinterpret_cast<float(*)[kPtW + 1]>(vt + (size_t)(h0 + hh) * kPtW * (kPtW + 1));
+                    float mx = 0.f;
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        tl[g + 4 * u][c] = x[hh][u];
+                        mx = fmaxf(mx, fabsf(x[hh][u]));
+                    }
+                    cpart[hh][g][c] = mx;
+                }
+                __syncthreads();
+                if (a.colmax && t < 128) {
+                    const int hh = t >> 6;
+                    const int64_t b = blockIdx.x + (int64_t)(h0 + hh) * gridDim.x;
+                    const int64_t k = (b % nkt) * 64 + c;
+                    const float mc = fmaxf(fmaxf(cpart[hh][0][c], cpart[hh][1][c]), fmaxf(cpart[hh][2][c], cpart[hh][3][c]));
+                    if (h0 + hh < a.hold_v && b < ntv && k < a.r && mc > 0.f) atomicMax(a.vcol + k, __float_as_uint(mc));
+                }
+                __syncthreads();  // cpart reused
+            }
+        } else if (a.colmax) {
             // tile (64 rows of V) x (64 columns): thread = (column t & 63, 16-row group t >> 6)
             const int64_t nkc = (a.r + 63) / 64;
             const int c = t & 63, g = t >> 6;
@@ -693,37 +753,73 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
     grid.sync();
     MID_MARK(2);
     // ---- B: every block sums the partials in the same order (deterministic, no
-    // extra barrier); block 0 publishes them for the kernels after k_mid
+    // extra barrier); the last block publishes them for the kernels after k_mid
     __shared__ double tot_s[2];
-    if (w == 0) {
+    {
+        // all threads load the partials at once (a lane-strided loop in one warp was a
+        // chain of dependent L2 round trips, ~5 us at 592 blocks)
         double l = 0.0, pn = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) {
+#pragma unroll 4
+        for (int b = t; b < (int)gridDim.x; b += kMidThreads) {
             l += a.part[2 * b];
             pn += a.part[2 * b + 1];
         }
         l = warp_sum(l);
         pn = warp_sum(pn);
-        if (lane == 0) {
-            tot_s[0] = l;
-            tot_s[1] = pn;
-            if (blockIdx.x == 0) {
-                a.sc->loss = l;
-                a.sc->pnorm2 = pn;
-                advance_step(a.opt);
-                double* L = a.losses_from_opt ? a.opt->losses : a.losses;
-                if (L) L[a.losses_from_opt ? a.opt->loss_idx++ : 0] = l;
+        if (lane == 0) { red[0][w] = l; red[1][w] = pn; }  // red's phase-A readers passed the grid barrier
+        __syncthreads();
+        if (w == 0) {
+            l = lane < kMidThreads / 32 ? red[0][lane] : 0.0;
+            pn = lane < kMidThreads / 32 ? red[1][lane] : 0.0;
+            l = warp_sum(l);
+            pn = warp_sum(pn);
+            if (lane == 0) {
+                tot_s[0] = l;
+                tot_s[1] = pn;
+                if (blockIdx.x == gridDim.x - 1) {  // read by the kernels after k_mid
+                    a.sc->loss = l;
+                    a.sc->pnorm2 = pn;
+                }
             }
         }
     }
     __syncthreads();
-    const double tol = a.opt->stop_tol;
+    MID_MARK(6);
     const bool stopped = tol > 0.0 && tot_s[0] <= tol * tot_s[1];
     const int64_t npairs = a.nkbN * (a.nkbN + 1) / 2;
     {
-        const int64_t nkt = (a.rowsVT + 63) / 64;
-        for (int64_t b = blockIdx.x; b < a.nkbN * nkt; b += gridDim.x)
-            pack_vtq_tile<256>(a.V, a.N, a.r, a.rowsVT, a.nkbN, a.vcol, a.VTQ, b / nkt, (b % nkt) * 64, tile0, t);
+        const int64_t nkt = (a.rowsVT + 63) / 64, ntv = a.nkbN * nkt;
+        if (a.hold_v) {
+            // the V tiles held since phase A; thread = (VTQ row k0 + (t >> 2), 16-row chunk t & 3).
+            // vcol took atomics in phase A: plain loads, all issued before the slicing
+            const float* vt = smem_tiles + (size_t)a.r_slots * kPtW * (kPtW + 1);
+            const int kk = t >> 2, c = t & 3;
+            float sc[kMidMaxHeldV];
+#pragma unroll
+            for (int h = 0; h < kMidMaxHeldV; ++h) {
+                const int64_t b = blockIdx.x + (int64_t)h * gridDim.x, k = (b % nkt) * 64 + kk;
+                sc[h] = h < a.hold_v && b < ntv && k < a.r ? slice_scale(a.vcol[k]) : 0.f;
+            }
+#pragma unroll
+            for (int h = 0; h < kMidMaxHeldV; ++h) {
+                const int64_t b = blockIdx.x + (int64_t)h * gridDim.x;
+                if (h >= a.hold_v || b >= ntv) break;
+                const int64_t k = (b % nkt) * 64 + kk;
+                if (k >= a.rowsVT) continue;
+                const float(*tl)[kPtW + 1] = reinterpret_cast<const float(*)[kPtW + 1]>(vt + (size_t)h * kPtW * (kPtW + 1));
+                float xs[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) xs[u] = tl[c * 16 + u][kk];
+                uint4 q[3];
+                slice16(xs, sc[h], q);
+                store_q16(a.VTQ, b / nkt, k, c, a.nkbN, a.rowsVT, q);
+            }
+        } else {
+            for (int64_t b = blockIdx.x; b < ntv; b += gridDim.x)
+                pack_vtq_tile<256>(a.V, a.N, a.r, a.rowsVT, a.nkbN, a.vcol, a.VTQ, b / nkt, (b % nkt) * 64, tile0, t);
+        }
     }
+    MID_MARK(7);
     if (!stopped) {
         int slot = 0;
         for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++slot) {
@@ -751,9 +847,21 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
             if (!a.hold) __syncthreads();  // tile0 is reused by the next block pair
         }
     }
+    MID_MARK(8);
     for (int64_t e = gtid; e < a.M / 4; e += gstride) reinterpret_cast<float4*>(a.coef)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t e = (a.M / 4) * 4 + gtid; e < a.M; e += gstride) a.coef[e] = 0.f;
-    if (stopped) return;  // grid-uniform: every block leaves before the barrier
+    // t += 1 and the loss record, once per step (nothing in k_mid reads them)
+    auto step_record = [&]() {
+        if (blockIdx.x == gridDim.x - 1 && t == 0) {
+            advance_step(a.opt);
+            double* L = a.losses_from_opt ? a.opt->losses : a.losses;
+            if (L) L[a.losses_from_opt ? a.opt->loss_idx++ : 0] = tot_s[0];
+        }
+    };
+    if (stopped) {  // grid-uniform: every block leaves before the barrier
+        step_record();
+        return;
+    }
     MID_MARK(3);
     grid.sync();
     MID_MARK(4);
@@ -783,12 +891,17 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
         }
         if (!a.hold) __syncthreads();
     }
+    step_record();
     MID_MARK(5);
 #ifdef SOS_EXPERIMENTS
     if (a.trace && blockIdx.x == 0 && t == 0)
         printf("k_mid block0 (us): A %.2f | sync %.2f | B %.2f | sync %.2f | C %.2f\n", (tmark[1] - tmark[0]) * 1e-3,
                (tmark[2] - tmark[1]) * 1e-3, (tmark[3] - tmark[2]) * 1e-3, (tmark[4] - tmark[3]) * 1e-3,
                (tmark[5] - tmark[4]) * 1e-3);
+    if (a.trace && blockIdx.x == 0 && t == 0)
+        printf("k_mid block0 detail (us): A residual %.2f | B partials %.2f | B vtq %.2f | B r-gather %.2f | B coef0 %.2f\n",
+               (tmark[9] - tmark[0]) * 1e-3, (tmark[6] - tmark[2]) * 1e-3, (tmark[7] - tmark[6]) * 1e-3,
+               (tmark[8] - tmark[7]) * 1e-3, (tmark[3] - tmark[8]) * 1e-3);
 #endif
 }
 
@@ -797,19 +910,22 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
 // block holds ceil(npairs / grid) R blocks in shared memory -- or, when that
 // exceeds kMidMaxHeld (long K), one block at a time with phase C gathering
 // again (tiles_per_block = 0).  Returns the grid (blocks).
-int mid_grid_for(int64_t nkbN, int64_t rowsVT, int64_t M, int num_sms, int* tiles_per_block) {
+int mid_grid_for(int64_t nkbN, int64_t rowsVT, int64_t M, int num_sms, int* tiles_per_block, int* hold_v) {
     const int64_t npairs = nkbN * (nkbN + 1) / 2;
-    const int64_t work = std::max<int64_t>({npairs, nkbN * ((rowsVT + 63) / 64), (M + 1023) / 1024, 1});
-    auto grid_for_smem = [&](size_t smem) {
+    const int64_t ntv = nkbN * ((rowsVT + 63) / 64);
+    const int64_t work = std::max<int64_t>({npairs, ntv, (M + 1023) / 1024, 1});
+    auto blocks_per_sm = [&](size_t smem) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int nb = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_mid, kMidThreads, smem) != cudaSuccess || nb < 1) {
             cudaGetLastError();
             nb = 1;
         }
-        return (int)std::min<int64_t>(work, (int64_t)num_sms * std::min(nb, 4));
+        return std::min(nb, 4);
     };
+    auto grid_for_smem = [&](size_t smem) { return (int)std::min<int64_t>(work, (int64_t)num_sms * blocks_per_sm(smem)); };
     int tpb = 1, grid = grid_for_smem(kMidTileBytes);
+    *hold_v = 0;
     for (int it = 0; it < 8; ++it) {
         const int need = (int)((npairs + grid - 1) / grid);
         if (need <= tpb) break;
@@ -821,6 +937,11 @@ int mid_grid_for(int64_t nkbN, int64_t rowsVT, int64_t M, int num_sms, int* tile
         grid = grid_for_smem((size_t)tpb * kMidTileBytes);
     }
     *tiles_per_block = tpb;
+    // the V tiles of phase A held for phase B, when they fit beside the R blocks
+    // without shrinking the grid
+    const int hv = (int)((ntv + grid - 1) / grid);
+    if (hv <= kMidMaxHeldV && (int64_t)num_sms * blocks_per_sm((size_t)(tpb + hv) * kMidTileBytes) >= grid) *hold_v = hv;
+    blocks_per_sm((size_t)(tpb + *hold_v) * kMidTileBytes);  // leaves the attribute at the launch's size
     return grid;
 }
 
@@ -861,7 +982,9 @@ void launch_mid(Plan& P, const float* p, const float* V, unsigned* vcol, bool co
     cfg.gridDim = dim3(P.mid_grid);
     cfg.blockDim = dim3(kMidThreads);
     a.hold = P.mid_tiles > 0 ? 1 : 0;
-    cfg.dynamicSmemBytes = (size_t)std::max(P.mid_tiles, 1) * kMidTileBytes;
+    a.r_slots = std::max(P.mid_tiles, 1);
+    a.hold_v = P.mid_hold_v;
+    cfg.dynamicSmemBytes = (size_t)(a.r_slots + a.hold_v) * kMidTileBytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;

@@ -589,6 +589,7 @@ struct MidArgs {
     int r_slots;  // shared-memory tiles before the held V tiles (max(R blocks held, 1))
     int hold_v;   // V tiles every block holds from phase A to B (0: phase B reads V again)
     int trace;  // experiment build only
+    unsigned long long* dbg;  // experiment build, trace: per-phase maxima over blocks
 };
 
 __device__ __forceinline__ void block_pair(int64_t pr, int64_t& I, int64_t& J) {
@@ -624,13 +625,20 @@ __device__ __forceinline__ void gather_r_tile(const uint32_t* __restrict__ pt, c
 
 #ifdef SOS_EXPERIMENTS
 // SOS_MID_TRACE=1 (experiment build): block 0 prints the phase boundaries of k_mid
-#define MID_MARK(k) do { if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) { \
+#define MID_MARK(k) do { if (a.trace && threadIdx.x == 0) { \
     unsigned long long now_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_)); tmark[k] = now_; } } while (0)
 #else
 #define MID_MARK(k) do { } while (0)
 #endif
 
-__global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
+#ifdef SOS_EXPERIMENTS
+// the trace code would raise the register count to 94 (2 blocks per SM): keep the
+// release build's 4 blocks per SM so that traces describe the same grid
+#define SOS_MID_BOUNDS __launch_bounds__(kMidThreads, 4)
+#else
+#define SOS_MID_BOUNDS __launch_bounds__(kMidThreads)
+#endif
+__global__ void SOS_MID_BOUNDS k_mid(const MidArgs a) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
 #ifdef SOS_EXPERIMENTS
@@ -902,6 +910,24 @@ __global__ void __launch_bounds__(kMidThreads) k_mid(const MidArgs a) {
         printf("k_mid block0 detail (us): A residual %.2f | B partials %.2f | B vtq %.2f | B r-gather %.2f | B coef0 %.2f\n",
                (tmark[9] - tmark[0]) * 1e-3, (tmark[6] - tmark[2]) * 1e-3, (tmark[7] - tmark[6]) * 1e-3,
                (tmark[8] - tmark[7]) * 1e-3, (tmark[3] - tmark[8]) * 1e-3);
+    if (a.trace && a.dbg) {  // slowest block per phase: (ns << 16) | block
+        const unsigned long long id = blockIdx.x;
+        if (t == 0) {
+            atomicMax(a.dbg + 0, ((tmark[1] - tmark[0]) << 16) | id);
+            atomicMax(a.dbg + 1, ((tmark[3] - tmark[2]) << 16) | id);
+            atomicMax(a.dbg + 2, ((tmark[7] - tmark[6]) << 16) | id);
+            atomicMax(a.dbg + 3, ((tmark[8] - tmark[7]) << 16) | id);
+            atomicMax(a.dbg + 4, ((tmark[5] - tmark[4]) << 16) | id);
+            atomicMax(a.dbg + 5, ((tmark[9] - tmark[0]) << 16) | id);
+        }
+        grid.sync();
+        if (blockIdx.x == 0 && t == 0) {
+            const char* nm[6] = {"A", "B", "B vtq", "B r-gather", "C", "A residual"};
+            printf("k_mid slowest blocks (us@block):");
+            for (int k = 0; k < 6; ++k) printf(" %s %.2f@%llu |", nm[k], (a.dbg[k] >> 16) * 1e-3, a.dbg[k] & 0xffff);
+            printf(" grid %d hold_v %d r_slots %d\n", (int)gridDim.x, a.hold_v, a.r_slots);
+        }
+    }
 #endif
 }
 
@@ -972,10 +998,15 @@ void launch_mid(Plan& P, const float* p, const float* V, unsigned* vcol, bool co
     a.zero_cols = zero_cols;
     a.part = P.d_part;
     a.trace = 0;
+    a.dbg = nullptr;
 #ifdef SOS_EXPERIMENTS
     {
         const char* e = getenv("SOS_MID_TRACE");
         a.trace = e && atoi(e) ? 1 : 0;
+        static unsigned long long* dbg = nullptr;
+        if (a.trace && !dbg) cudaMalloc(&dbg, 8 * sizeof(unsigned long long));
+        if (a.trace) cudaMemsetAsync(dbg, 0, 8 * sizeof(unsigned long long), st);
+        a.dbg = dbg;
     }
 #endif
     cudaLaunchConfig_t cfg = {};

@@ -264,6 +264,11 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
     P.idx = &h->ix;
     P.r = r;
     P.num_sms = sms;
+    {
+        int dev = 0, l2 = 0;
+        cudaGetDevice(&dev);
+        P.l2_bytes = cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) == cudaSuccess ? l2 : 0;
+    }
     const int64_t Np = h->ix.Np, N = h->ix.N, M = h->ix.M;
     const int64_t colBlocksV = (N + kTileN - 1) / kTileN;
     P.rowsV = std::max(Np, colBlocksV * kTileN);

@@ -229,6 +229,7 @@ struct Plan {
     cudaEvent_t sig_ev;
     int64_t launches;
     int num_sms;
+    int64_t l2_bytes;      // L2 size (the split update keeps V, m, v in L2 when they fit)
     Timing* timing;
 };
 

@@ -430,7 +430,7 @@ __device__ __forceinline__ float adam_or_gd(bool adam, float x, float g, float& 
 __global__ void __launch_bounds__(kUpdThreads) k_update_rows(
     const float* __restrict__ grad, float* V, float* __restrict__ m, float* __restrict__ v, int64_t N, int64_t r,
     int adam, const DevOpt* opt, const Scalars* sc, uint8_t* __restrict__ vq_next, int64_t rowsV, int64_t nkbV,
-    const unsigned* __restrict__ vrow_cur, unsigned* __restrict__ vrow_next) {
+    const unsigned* __restrict__ vrow_cur, unsigned* __restrict__ vrow_next, int keep_l2) {
     extern __shared__ float4 stage4[];  // the block's span (flat), when r <= kUpdSmemR
     __shared__ float rmax_s[kUpdRows];
     griddep_wait();  // launched with programmatic stream serialization after the backward
@@ -442,6 +442,9 @@ __global__ void __launch_bounds__(kUpdThreads) k_update_rows(
         return;
     }
     const DevOpt o = *opt;
+    // evict_last keeps V, m, v in L2 from step to step when they fit in it (keep_l2:
+    // config 2 +1.9 %, N = 2926 +2.8 %, profiles/r2_short_k_ab.log), else evict_first
+    const uint64_t pol = keep_l2 ? l2_evict_last_policy() : l2_evict_first_policy();
     const bool in_smem = r <= kUpdSmemR;
     const int64_t base = i0 * r, len = nr * r, n4 = len >> 2;
     const float4* g4 = reinterpret_cast<const float4*>(grad + base);
@@ -455,10 +458,10 @@ __global__ void __launch_bounds__(kUpdThreads) k_update_rows(
             const int64_t q = q0 + kUpdThreads * u;
             if (q < n4) {
                 gv[u] = __ldcs(g4 + q);
-                x[u] = __ldcs(V4 + q);
+                x[u] = ld_f4_hint(V4 + q, pol);
                 if (adam) {
-                    mm[u] = __ldcs(m4 + q);
-                    vv[u] = __ldcs(v4 + q);
+                    mm[u] = ld_f4_hint(m4 + q, pol);
+                    vv[u] = ld_f4_hint(v4 + q, pol);
                 }
             }
         }
@@ -472,13 +475,14 @@ __global__ void __launch_bounds__(kUpdThreads) k_update_rows(
                 xn.y = adam_or_gd(true, x[u].y, gv[u].y, mm[u].y, vv[u].y, o);
                 xn.z = adam_or_gd(true, x[u].z, gv[u].z, mm[u].z, vv[u].z, o);
                 xn.w = adam_or_gd(true, x[u].w, gv[u].w, mm[u].w, vv[u].w, o);
-                __stcs(m4 + q, mm[u]);
-                __stcs(v4 + q, vv[u]);
+                st_f4_hint(m4 + q, mm[u], pol);
+                st_f4_hint(v4 + q, vv[u], pol);
             } else {
                 xn = make_float4(x[u].x - o.lr * gv[u].x, x[u].y - o.lr * gv[u].y, x[u].z - o.lr * gv[u].z,
                                  x[u].w - o.lr * gv[u].w);
             }
-            V4[q] = xn;  // default policy: L2-resident for the next k_mid
+            if (keep_l2) st_f4_hint(V4 + q, xn, pol);  // read again by the next k_mid
+            else V4[q] = xn;
             if (in_smem) stage4[q] = xn;
         }
     }
@@ -547,7 +551,8 @@ void launch_update_rows(Plan& P, float* V, uint8_t* vq_next, const unsigned* vro
     cfg.attrs = at;
     cfg.numAttrs = ls.a ? 0 : 1;
     cudaLaunchKernelEx(&cfg, k_update_rows, (const float*)P.d_grad, V, P.d_m, P.d_v, N, P.r, (int)(P.opt_kind == 1),
-                       (const DevOpt*)P.d_opt, (const Scalars*)P.d_scal, vq_next, P.rowsV, P.nkbV, vrow_cur, vrow_next);
+                       (const DevOpt*)P.d_opt, (const Scalars*)P.d_scal, vq_next, P.rowsV, P.nkbV, vrow_cur, vrow_next,
+                       (double)N * P.r * 12 <= (double)P.l2_bytes ? 1 : 0);
 }
 
 // --------------------------------------------------- split step: k_mid ----

@@ -649,6 +649,7 @@ __global__ void SOS_MID_BOUNDS k_mid(const MidArgs a) {
 #ifdef SOS_EXPERIMENTS
     unsigned long long tmark[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
+    griddep_wait();  // launched with programmatic stream serialization after the forward
     MID_MARK(0);
     extern __shared__ float smem_tiles[];  // R blocks held from phase B to C, 64 x 65 floats each
     __shared__ double red[2][kMidThreads / 32];
@@ -1022,12 +1023,18 @@ void launch_mid(Plan& P, const float* p, const float* V, unsigned* vcol, bool co
     a.hold_v = P.mid_hold_v;
     cfg.dynamicSmemBytes = (size_t)(a.r_slots + a.hold_v) * kMidTileBytes;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_mid, a);
+    cfg.numAttrs = ls.a ? 1 : 2;
+    if (cudaLaunchKernelEx(&cfg, k_mid, a) != cudaSuccess && cfg.numAttrs == 2) {
+        cudaGetLastError();
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, k_mid, a);
+    }
 }
 
 void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_from_opt, unsigned* zero0, int64_t n0,

@@ -230,6 +230,7 @@ struct Plan {
     int64_t launches;
     int num_sms;
     int64_t l2_bytes;      // L2 size (the split update keeps V, m, v in L2 when they fit)
+    int upd_rows;          // rows per block of the split update (0: not chosen yet)
     Timing* timing;
 };
 

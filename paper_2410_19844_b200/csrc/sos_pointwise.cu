@@ -7,6 +7,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -408,10 +409,10 @@ __global__ void k_step_begin(DevOpt* opt, const Scalars* sc, double* losses, int
 }
 
 // ------------------------------------------------- split step: update ----
-// GD / Adam on a block of kUpdRows whole rows of V, in two
-// passes.  Pass 1 is purely elementwise: the block's rows are one contiguous
-// span of V, m, v and the gradient (16-byte aligned: the block starts at a row
-// multiple of 4), streamed as float4 with kUpdU of them in flight per array and
+// GD / Adam on a block of `rows` (1, 2 or 4) whole rows of V, in
+// two passes.  Pass 1 is purely elementwise: the block's rows are one contiguous
+// span of V, m, v and the gradient (16-byte aligned: rows * r is a multiple of
+// 4), streamed as float4 with kUpdU of them in flight per array and
 // thread; the new values also go to a shared-memory copy of the span (or, for
 // rows longer than kUpdSmemR, are re-read from L2).  Pass 2 takes the EXACT
 // maximum of each new row (one warp per row) and slices the rows into the next
@@ -419,7 +420,7 @@ __global__ void k_step_begin(DevOpt* opt, const Scalars* sc, double* losses, int
 // scale, no fixup kernel.  (The column maxima of V_{t+1}, for its V^T slices,
 // are taken by the next k_mid.)  A stopped descent (sos_opt_set_stop) leaves V,
 // m, v and VQ unchanged and carries the row maxima over.
-constexpr int kUpdRows = 4, kUpdThreads = 256, kUpdU = 2;
+constexpr int kUpdRows = 4, kUpdThreads = 256, kUpdU = 2;  // kUpdRows: the most rows per block
 constexpr int64_t kUpdSmemR = 4096;  // rows up to this length are staged in shared memory (64 KB)
 __device__ __forceinline__ float adam_or_gd(bool adam, float x, float g, float& m, float& v, const DevOpt& o) {
     if (!adam) return x - o.lr * g;
@@ -430,13 +431,13 @@ __device__ __forceinline__ float adam_or_gd(bool adam, float x, float g, float& 
 __global__ void __launch_bounds__(kUpdThreads) k_update_rows(
     const float* __restrict__ grad, float* V, float* __restrict__ m, float* __restrict__ v, int64_t N, int64_t r,
     int adam, const DevOpt* opt, const Scalars* sc, uint8_t* __restrict__ vq_next, int64_t rowsV, int64_t nkbV,
-    const unsigned* __restrict__ vrow_cur, unsigned* __restrict__ vrow_next, int keep_l2) {
+    const unsigned* __restrict__ vrow_cur, unsigned* __restrict__ vrow_next, int keep_l2, int rows) {
     extern __shared__ float4 stage4[];  // the block's span (flat), when r <= kUpdSmemR
     __shared__ float rmax_s[kUpdRows];
     griddep_wait();  // launched with programmatic stream serialization after the backward
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int64_t i0 = (int64_t)blockIdx.x * kUpdRows;
-    const int nr = (int)(N - i0 < kUpdRows ? N - i0 : kUpdRows);
+    const int64_t i0 = (int64_t)blockIdx.x * rows;
+    const int nr = (int)(N - i0 < rows ? N - i0 : rows);
     if (descent_stopped(sc, opt, 1)) {
         if (vrow_next && t < nr) vrow_next[i0 + t] = vrow_cur[i0 + t];
         return;
@@ -533,13 +534,35 @@ __global__ void __launch_bounds__(kUpdThreads) k_update_rows(
 void launch_update_rows(Plan& P, float* V, uint8_t* vq_next, const unsigned* vrow_cur, unsigned* vrow_next,
                         cudaStream_t st) {
     LaunchScope ls(P, KK_UPDATE, st);
-    const int64_t N = P.idx->N, blocks = (N + kUpdRows - 1) / kUpdRows;
-    const size_t smem = P.r <= kUpdSmemR ? (size_t)kUpdRows * P.r * sizeof(float) : 0;
-    static size_t configured = 48 * 1024;
-    if (smem > configured) {
+    static bool configured = false;
+    if (!configured) {
         cudaFuncSetAttribute(k_update_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kUpdRows * kUpdSmemR * 4));
-        configured = kUpdRows * kUpdSmemR * 4;
+        configured = true;
     }
+    // rows per block: of 1, 2, 4 (rows * r a multiple of 4), the one whose last wave
+    // is fullest (r = 4004: 4 rows = 64 KB per block ran 501 blocks on 444 slots,
+    // 1.13 waves; 1 row, 2002 blocks on 592 slots); ties -> more rows
+    const int64_t N = P.idx->N;
+    int rows = P.upd_rows;
+    double best = -1.0;
+    for (int R = kUpdRows; R >= 1 && !P.upd_rows; R >>= 1) {
+        if ((R * P.r) % 4) continue;
+        const size_t sm = P.r <= kUpdSmemR ? (size_t)R * P.r * sizeof(float) : 0;
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_update_rows, kUpdThreads, sm) != cudaSuccess || nb < 1) {
+            cudaGetLastError();
+            nb = 1;
+        }
+        const double blocks = (double)((N + R - 1) / R), slots = (double)P.num_sms * nb;
+        const double eff = blocks / (std::ceil(blocks / slots) * slots);
+        if (eff > best + 1e-9) {
+            best = eff;
+            rows = R;
+        }
+    }
+    P.upd_rows = rows;  // once per plan
+    const int64_t blocks = (N + rows - 1) / rows;
+    const size_t smem = P.r <= kUpdSmemR ? (size_t)rows * P.r * sizeof(float) : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);
     cfg.blockDim = dim3(kUpdThreads);
@@ -552,7 +575,7 @@ void launch_update_rows(Plan& P, float* V, uint8_t* vq_next, const unsigned* vro
     cfg.numAttrs = ls.a ? 0 : 1;
     cudaLaunchKernelEx(&cfg, k_update_rows, (const float*)P.d_grad, V, P.d_m, P.d_v, N, P.r, (int)(P.opt_kind == 1),
                        (const DevOpt*)P.d_opt, (const Scalars*)P.d_scal, vq_next, P.rowsV, P.nkbV, vrow_cur, vrow_next,
-                       (double)N * P.r * 12 <= (double)P.l2_bytes ? 1 : 0);
+                       (double)N * P.r * 12 <= (double)P.l2_bytes ? 1 : 0, rows);
 }
 
 // --------------------------------------------------- split step: k_mid ----

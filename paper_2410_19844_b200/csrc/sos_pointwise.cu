@@ -7,6 +7,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <vector>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -343,9 +344,27 @@ __global__ void __launch_bounds__(256) k_rfix(const uint32_t* __restrict__ pt, c
 }
 
 // -------------------------------------------------------------- launches ---
-static int grid_for(const Plan& P, int64_t work, int threads, int per_sm = 8) {
+// blocks of `fn` that fit on one SM at once (occupancy API, cached per kernel)
+static int resident_per_sm(const void* fn, int threads, size_t smem) {
+    struct Entry { const void* fn; int threads; size_t smem; int nb; };
+    static std::vector<Entry> cache;
+    for (const Entry& e : cache)
+        if (e.fn == fn && e.threads == threads && e.smem == smem) return e.nb;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem) != cudaSuccess || nb < 1) {
+        cudaGetLastError();
+        nb = 1;
+    }
+    cache.push_back(Entry{fn, threads, smem, nb});
+    return nb;
+}
+// grid of a grid-stride kernel: enough blocks for the work, but never more than
+// fit on the GPU at once (more would run a partial second wave with the same
+// per-block work: the R packer at config 4 ran 1184 blocks on 888 slots)
+template <typename F>
+static int grid_for(const Plan& P, F* fn, int64_t work, int threads, int per_sm = 64, size_t smem = 0) {
     int64_t b = (work + threads - 1) / threads;
-    int64_t cap = (int64_t)P.num_sms * per_sm;
+    const int64_t cap = (int64_t)P.num_sms * std::min(per_sm, resident_per_sm((const void*)fn, threads, smem));
     if (b > cap) b = cap;
     if (b < 1) b = 1;
     return (int)b;
@@ -359,19 +378,19 @@ void launch_vmax(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, unsig
     cudaMemsetAsync(vcol, 0, P.rowsVT * sizeof(unsigned), st);
     LaunchScope ls(P, KK_ABSMAX_V, st);
     const int64_t tiles = ((N + 63) / 64) * ((P.r + 1023) / 1024);
-    k_vmax<<<grid_for(P, tiles * 256, 256), 256, 0, st>>>(V, N, P.r, vrow, vcol);
+    k_vmax<<<grid_for(P, k_vmax, tiles * 256, 256), 256, 0, st>>>(V, N, P.r, vrow, vcol);
 }
 
 void launch_pack_vtq(Plan& P, const float* V, cudaStream_t st, const unsigned* vcol) {
     LaunchScope ls(P, KK_PACK_V, st);
     const int64_t blocks = P.nkbN * ((P.rowsVT + 63) / 64);
-    k_pack_vtq<<<grid_for(P, blocks * 256, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.rowsVT, P.nkbN,
+    k_pack_vtq<<<grid_for(P, k_pack_vtq, blocks * 256, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.rowsVT, P.nkbN,
                                                                vcol ? vcol : P.d_vcol, P.d_vtq);
 }
 
 void launch_residual(Plan& P, const float* coef, const float* p, float* res, cudaStream_t st) {
     LaunchScope ls(P, KK_RESIDUAL, st);
-    k_residual<<<grid_for(P, P.idx->M, 256, 4), 256, 0, st>>>(coef, p, res, P.idx->M, P.d_scal);
+    k_residual<<<grid_for(P, k_residual, P.idx->M, 256, 4), 256, 0, st>>>(coef, p, res, P.idx->M, P.d_scal);
 }
 
 // rrow_zeroed: the caller cleared rrow in the same stream (k_step_begin inside
@@ -380,7 +399,7 @@ void launch_rmax(Plan& P, const float* res, cudaStream_t st, int use_stop, bool 
     LaunchScope ls(P, KK_ABSMAX_R, st);
     if (!rrow_zeroed) cudaMemsetAsync(P.d_rrow, 0, (size_t)P.idx->Np * sizeof(unsigned), st);
     const int64_t nkb = P.idx->Np / kPtW, npairs = nkb * (nkb + 1) / 2;
-    const unsigned blocks = (unsigned)std::min<int64_t>(npairs, (int64_t)P.num_sms * 8);
+    const unsigned blocks = grid_for(P, k_rmax, npairs * 256, 256);
     k_rmax<<<blocks, 256, 0, st>>>(P.idx->d_pt, res, nkb, P.d_rrow, P.d_scal, P.d_opt, use_stop);
 }
 
@@ -1068,7 +1087,7 @@ void launch_step_begin(Plan& P, double* losses, cudaStream_t st, bool losses_fro
     if (!zero0) n0 = 0;
     if (!zero1) n1 = 0;
     const int64_t nz = n0 + n1 + n2;
-    const int blocks = nz || nc ? grid_for(P, std::max<int64_t>(nz, nc / 4), 256, 4) : 1;
+    const int blocks = nz || nc ? grid_for(P, k_step_begin, std::max<int64_t>(nz, nc / 4), 256, 4) : 1;
     k_step_begin<<<blocks, 256, 0, st>>>(P.d_opt, P.d_scal, losses_from_opt ? nullptr : losses, losses_from_opt ? 1 : 0,
                                          zero0, n0, zero1, n1, zero_r, n2, zero_coef, nc);
 }
@@ -1079,7 +1098,7 @@ void launch_pack_v(Plan& P, const float* V, cudaStream_t st, unsigned* vrow, uns
     launch_vmax(P, V, st, vrow, vcol);
     LaunchScope ls(P, KK_PACK_V, st);
     const int64_t work = P.rowsV * P.nkbV * 4;
-    k_pack_vq<<<grid_for(P, work, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.rowsV, P.nkbV, vrow, P.d_vq);
+    k_pack_vq<<<grid_for(P, k_pack_vq, work, 256), 256, 0, st>>>(V, P.idx->N, P.r, P.rowsV, P.nkbV, vrow, P.d_vq);
 }
 
 // row maxima + RQ: the row maxima come from the lattice DP (sos_index.cu, a
@@ -1114,7 +1133,7 @@ void launch_pack_rq(Plan& P, const float* res, cudaStream_t st, int use_stop) {
     const int64_t Np = P.idx->Np;
     LaunchScope ls(P, KK_PACK_R, st);
     const int64_t npairs = P.nkbN * (P.nkbN + 1) / 2;
-    const unsigned blocks = (unsigned)std::min<int64_t>(npairs, (int64_t)P.num_sms * 8);
+    const unsigned blocks = grid_for(P, k_pack_rq_sym<false>, npairs * 256, 256);
     k_pack_rq_sym<false><<<blocks, 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, P.d_rrow, P.d_rq, P.d_scal, P.d_opt,
                                                  use_stop, nullptr);
 }
@@ -1125,12 +1144,12 @@ void launch_pack_r_headroom(Plan& P, const float* res, const unsigned* rrow_prev
     {
         LaunchScope ls(P, KK_PACK_R, st);
         const int64_t npairs = P.nkbN * (P.nkbN + 1) / 2;
-        const unsigned blocks = (unsigned)std::min<int64_t>(npairs, (int64_t)P.num_sms * 8);
+        const unsigned blocks = grid_for(P, k_pack_rq_sym<true>, npairs * 256, 256);
         k_pack_rq_sym<true><<<blocks, 256, 0, st>>>(P.idx->d_pt, res, Np, P.nkbN, rrow_prev, P.d_rq, P.d_scal,
                                                     P.d_opt, 1, rrow_cur);
     }
     LaunchScope ls(P, KK_ABSMAX_R, st);
-    k_rfix<<<grid_for(P, P.idx->N * 32, 256), 256, 0, st>>>(P.idx->d_pt, res, P.idx->N, Np, P.nkbN, rrow_prev,
+    k_rfix<<<grid_for(P, k_rfix, P.idx->N * 32, 256), 256, 0, st>>>(P.idx->d_pt, res, P.idx->N, Np, P.nkbN, rrow_prev,
                                                               rrow_cur, urow_r, P.d_rq, P.d_scal, P.d_opt);
 }
 
@@ -1237,7 +1256,7 @@ void launch_descend_fixup(Plan& P, const float* V, const unsigned* vrow_cur, uns
     a.sc = P.d_scal;
     a.opt = P.d_opt;
     const int64_t warps = P.rowsV + (vtq_next ? P.r : 0);
-    k_descend_fixup<<<grid_for(P, warps * 32, 256), 256, 0, st>>>(a);
+    k_descend_fixup<<<grid_for(P, k_descend_fixup, warps * 32, 256), 256, 0, st>>>(a);
 }
 
 }  // namespace sos

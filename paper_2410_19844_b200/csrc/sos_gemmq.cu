@@ -79,6 +79,8 @@ struct GemmArgs {
     unsigned long long* dbg;   // experiments: SOS_GEMM_STATS per-role wait cycles
     int trace;                 // experiments: SOS_GEMM_TRACE phase times of CTA 0
     int kserp;                 // walk K backwards on odd local tiles (L2 reuse across waves)
+    int skip_red;              // experiments: SOS_FWD_SKIP (wrong results): forward REDs skipped on
+                               // 1 = tiles touching the diagonal, 2 = all tiles
     int probe;                 // experiments: SOS_GEMM_PROBE (wrong results): 1 = K-blocks mod 8,
                                // 2 = also tile 0, 4 = 2 with B loaded only on the first ring pass
     // kModeBwdUpdate(Vtq): the optimiser step of PAPER.md:221, applied by the epilogue warps
@@ -519,7 +521,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             if (kFwd) {
                 // rows [256a, 256a+256) vs cols [c0, c0+nb): all above the diagonal iff c0 >= 256a + 256
                 const bool strictly_upper = (int64_t)tc.c0 >= (int64_t)tc.a * kPairM + kPairM;
-                if (i < args.N) {
+                const bool skip = kExperiments && (args.skip_red == 2 || (args.skip_red == 1 && !strictly_upper));
+                if (i < args.N && !skip) {
                     // 16-column chunks: live, inside N, and in the stored PT triangle (a
                     // later row block means j < i for all 16 columns: weight 0)
                     bool live[kEpiCols / 16];
@@ -759,6 +762,7 @@ static cudaError_t launchq(const Plan& P, const CUtensorMap& ma, const CUtensorM
         a.skew_lag = lag;
         a.skew_sleep = env_int("SOS_SKEW_SLEEP", 256);
         a.probe = env_int("SOS_GEMM_PROBE", 0);
+        a.skip_red = env_int("SOS_FWD_SKIP", 0);
         a.kserp = env_int("SOS_KSERP", 1);
         static unsigned long long* dbg = nullptr;
         if (env_int("SOS_GEMM_STATS", 0)) {

@@ -7,6 +7,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 #include <cmath>
 #include <cstdio>
@@ -348,6 +349,8 @@ __global__ void __launch_bounds__(256) k_rfix(const uint32_t* __restrict__ pt, c
 static int resident_per_sm(const void* fn, int threads, size_t smem) {
     struct Entry { const void* fn; int threads; size_t smem; int nb; };
     static std::vector<Entry> cache;
+    static std::mutex mu;  // distinct plans may launch from distinct host threads
+    std::lock_guard<std::mutex> lock(mu);
     for (const Entry& e : cache)
         if (e.fn == fn && e.threads == threads && e.smem == smem) return e.nb;
     int nb = 0;

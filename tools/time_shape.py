@@ -14,6 +14,14 @@ for a in sys.argv:  # lib=PATH: an alternative build of the library (same-box A/
     if a.startswith("lib="):
         sos.load(a[4:])
 
+for a in sys.argv:  # persist=MB: cudaLimitPersistingL2CacheSize for the run (L2 set-aside experiment)
+    if a.startswith("persist="):
+        from cuda.bindings import runtime as _rt
+        torch.cuda.init()
+        print("persist:", _rt.cudaDeviceSetLimit(_rt.cudaLimit.cudaLimitPersistingL2CacheSize, int(a[8:]) << 20),
+              _rt.cudaDeviceGetLimit(_rt.cudaLimit.cudaLimitPersistingL2CacheSize))
+sys.argv = [a for a in sys.argv if not a.startswith("persist=")]
+
 n, d, r = (int(x) for x in sys.argv[1:4])
 steps = int(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4].isdigit() else 20
 opts = {k: (int(v) if k == "tile_w" else bool(int(v))) for k, v in (a.split("=") for a in sys.argv[4:] if "=" in a and not a.startswith("lib="))}

@@ -123,7 +123,12 @@ int sos_plan_create(const sos_index *idx, int64_t r, sos_plan **out);
  *                 slices use 2x the previous step's exact R row maxima; the
  *                 packer takes this step's exact maxima on the fly and re-slices
  *                 the rare rows outside the window (default 1); 0 = exact row
- *                 maxima every step (lattice DP or direct pass). */
+ *                 maxima every step (lattice DP or direct pass).
+ *   tiny:         sos_descend (and sos_solve_host) run all their steps in ONE
+ *                 cooperative kernel of fp32 CUDA-core tiles with grid barriers
+ *                 between forward, residual, backward and update (default for
+ *                 small problems, N^2 r <= 2e7, e.g. N = r <= 271); other
+ *                 calls are unchanged. */
 typedef struct {
     int split;
     int vtq_from_update;
@@ -132,6 +137,7 @@ typedef struct {
     int narrow_tiles;
     int tile_w;
     int r_headroom;
+    int tiny;
 } sos_plan_opts;
 int sos_plan_create_ex(const sos_index *idx, int64_t r, const sos_plan_opts *opts, sos_plan **out);
 int sos_plan_destroy(sos_plan *plan);
@@ -155,7 +161,8 @@ int64_t sos_plan_launch_count(const sos_plan *plan);
 #define SOS_KERNEL_UPDATE 7   /* step bookkeeping (Adam t, loss record); the split step's row-block update
                                  (otherwise the update runs inside GEMM_BWD) */
 #define SOS_KERNEL_MID 8      /* the split step's cooperative kernel: residual, loss, R maxima, V^T and R slices */
-#define SOS_KERNEL_COUNT 9
+#define SOS_KERNEL_TINY 9     /* a tiny plan's whole sos_descend call (one cooperative kernel) */
+#define SOS_KERNEL_COUNT 10
 int sos_plan_timing(sos_plan *plan, int enable);
 int sos_plan_timing_read(sos_plan *plan, int kernel, double *total_ms, int64_t *launches);
 

@@ -35,7 +35,7 @@ class _OptParams(ctypes.Structure):
 class _PlanOpts(ctypes.Structure):
     _fields_ = [("split", ctypes.c_int), ("vtq_from_update", ctypes.c_int), ("vtq_in_aux", ctypes.c_int),
                 ("rmax_direct", ctypes.c_int), ("narrow_tiles", ctypes.c_int), ("tile_w", ctypes.c_int),
-                ("r_headroom", ctypes.c_int)]
+                ("r_headroom", ctypes.c_int), ("tiny", ctypes.c_int)]
 
 
 _lib = None
@@ -159,10 +159,10 @@ class SosPlan:
 
     Keyword options (sos_plan_opts: None = the library's choice by size, else
     True / False): split, vtq_from_update, vtq_in_aux, rmax_direct,
-    narrow_tiles, r_headroom; tile_w (None, or a multiple of 16 in [16, 160]) -- implementation
+    narrow_tiles, r_headroom, tiny; tile_w (None, or a multiple of 16 in [16, 160]) -- implementation
     variants of the same step."""
 
-    OPTS = ("split", "vtq_from_update", "vtq_in_aux", "rmax_direct", "narrow_tiles", "tile_w", "r_headroom")
+    OPTS = ("split", "vtq_from_update", "vtq_in_aux", "rmax_direct", "narrow_tiles", "tile_w", "r_headroom", "tiny")
 
     def __init__(self, index: SosIndex, r: int, **opts):
         bad = set(opts) - set(self.OPTS)
@@ -191,7 +191,7 @@ class SosPlan:
     def launch_count(self) -> int:
         return int(load().sos_plan_launch_count(self._h))
 
-    KERNELS = ("vmax", "pack_v", "gemm_fwd", "residual", "rmax", "pack_r", "gemm_bwd", "update", "mid")
+    KERNELS = ("vmax", "pack_v", "gemm_fwd", "residual", "rmax", "pack_r", "gemm_bwd", "update", "mid", "tiny")
 
     def timing(self, enable: bool):
         """Start (clears old records) / stop per-kernel CUDA-event timing."""

@@ -11,7 +11,7 @@ LIB = os.path.join(HERE, "libsos_b200.so")
 # experiment build (-DSOS_EXPERIMENTS): the environment switches and probes of
 # DESIGN.md 5.4; never loaded by the package unless a tool asks for it
 LIB_EXP = os.path.join(HERE, "libsos_b200_exp.so")
-SOURCES = ["sos_api.cu", "sos_index.cu", "sos_pointwise.cu", "sos_gemmq.cu"]
+SOURCES = ["sos_api.cu", "sos_index.cu", "sos_pointwise.cu", "sos_gemmq.cu", "sos_tiny.cu"]
 HEADERS = ["sm100_ptx.cuh", "sos_internal.cuh", "sos_slice.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -249,9 +249,9 @@ static bool pick(int opt, bool dflt) { return opt < 0 ? dflt : opt != 0; }
 
 int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts, sos_plan** out) {
     if (!h || !out || r < 1) return fail(SOS_ERR_ARG, "bad argument");
-    sos_plan_opts o = {-1, -1, -1, -1, -1, -1, -1};
+    sos_plan_opts o = {-1, -1, -1, -1, -1, -1, -1, -1};
     if (opts) o = *opts;
-    for (int v : {o.split, o.vtq_from_update, o.vtq_in_aux, o.rmax_direct, o.narrow_tiles, o.r_headroom})
+    for (int v : {o.split, o.vtq_from_update, o.vtq_in_aux, o.rmax_direct, o.narrow_tiles, o.r_headroom, o.tiny})
         if (v < -1 || v > 1) return fail(SOS_ERR_ARG, "sos_plan_opts fields must be -1, 0 or 1");
     if (!(o.tile_w == -1 || o.tile_w == 0 || (o.tile_w >= 16 && o.tile_w <= kTileN && o.tile_w % 16 == 0)))
         return fail(SOS_ERR_ARG, "sos_plan_opts.tile_w must be -1 / 0 (auto) or a multiple of 16 in [16, 160]");
@@ -300,6 +300,10 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
     P.vtq_in_aux = pick(o.vtq_in_aux, vtq_fits_aux(P));
     P.rmax_direct = pick(o.rmax_direct, rmax_direct_default(h->ix));
     if (P.split) P.mid_grid = mid_grid_for(P.nkbN, P.rowsVT, M, sms, &P.mid_tiles, &P.mid_hold_v);
+    // tiny plans: the whole descent in one cooperative kernel (sos_tiny.cu) for
+    // small N and r, where the split step's four launches are latency-bound
+    P.tiny_grid = tiny_grid_for(N, r, sms);
+    P.tiny = P.tiny_grid > 0 && pick(o.tiny, (double)N * N * r <= kTinyMaxWork);
     // row chunks of the last step's V release = the raster's row groups
     P.sig_blocks = (int)tile_group();
     P.sig_expect.assign((size_t)((Np / kPairM + P.sig_blocks - 1) / P.sig_blocks), 0u);
@@ -319,8 +323,9 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
         (rc = dalloc(&P.d_tiles_fwd, std::max<size_t>(1, tf.size()) * sizeof(TileCoord))) ||
         (rc = dalloc(&P.d_tiles_bwd, std::max<size_t>(1, tb.size()) * sizeof(TileCoord))) ||
         (rc = dalloc(&P.d_rowsig, std::max<size_t>(1, P.sig_expect.size()) * sizeof(unsigned))) ||
-        (P.split && (rc = dalloc(&P.d_grad, (size_t)N * r * sizeof(float)))) ||
-        (P.split && (rc = dalloc(&P.d_part, (size_t)2 * std::max(P.mid_grid, 1) * sizeof(double)))) ||
+        ((P.split || P.tiny) && (rc = dalloc(&P.d_grad, (size_t)N * r * sizeof(float)))) ||
+        ((P.split || P.tiny) &&
+         (rc = dalloc(&P.d_part, (size_t)2 * std::max({P.mid_grid, P.tiny_grid, 1}) * sizeof(double)))) ||
         (P.r_headroom && (rc = dalloc(&P.d_rrowx, (size_t)2 * Np * sizeof(unsigned)))) ||
         (P.r_headroom && (rc = dalloc(&P.d_urowr, (size_t)Np * sizeof(unsigned))))) {
         sos_plan_destroy(pl);
@@ -678,6 +683,13 @@ static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps
     CK(cudaMemsetAsync(&P.d_opt->loss_idx, 0, sizeof(long long), st));
     P.h_losses = losses_dev;  // pageable source: staged synchronously by the copy below
     CK(cudaMemcpyAsync(&P.d_opt->losses, &P.h_losses, sizeof(double*), cudaMemcpyHostToDevice, st));
+    if (P.tiny) {  // every step in one cooperative kernel (sos_tiny.cu)
+        CK(cudaMemsetAsync(P.d_coef, 0, (size_t)P.idx->M * 4, st));
+        CK(cudaMemsetAsync(P.d_grad, 0, (size_t)P.idx->N * P.r * 4, st));
+        if (launch_tiny_descend(P, V_dev, p_dev, steps, st))
+            return fail(SOS_ERR_CUDA, "tiny descend launch: %s", cudaGetErrorString(cudaGetLastError()));
+        return check_launch("tiny descend");
+    }
     // step 0 starts from the exact maxima and slices of the caller's V
     launch_pack_v(P, V_dev, st, d.vrowx[0], d.vcol[0]);
     if (!P.split) CK(cudaMemcpyAsync(d.urow[0], d.vrowx[0], P.rowsV * 4, cudaMemcpyDeviceToDevice, st));
@@ -773,7 +785,7 @@ int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t ste
     // ship V back in row chunks while the last step's backward still runs (needs
     // stream memory operations; otherwise one copy after the last step)
     // (the split update of short-K plans does not release chunks: one copy at the end)
-    const PFN_wait_value32 wait = steps > 0 && !P.split ? wait_value_fn() : nullptr;
+    const PFN_wait_value32 wait = steps > 0 && !P.split && !P.tiny ? wait_value_fn() : nullptr;
     bool overlap = wait != nullptr;
     if (overlap && !P.copy_st)
         overlap = cudaStreamCreateWithFlags(&P.copy_st, cudaStreamNonBlocking) == cudaSuccess &&

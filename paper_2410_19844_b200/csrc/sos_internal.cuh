@@ -33,7 +33,7 @@ namespace sos {
 
 // kernel kinds for per-launch event timing (sos_plan_timing_read)
 enum KernelKind { KK_ABSMAX_V = 0, KK_PACK_V, KK_GEMM_FWD, KK_RESIDUAL, KK_ABSMAX_R, KK_PACK_R, KK_GEMM_BWD,
-                  KK_UPDATE, KK_MID, KK_COUNT };
+                  KK_UPDATE, KK_MID, KK_TINY, KK_COUNT };
 
 struct TimingRec { int kind; cudaEvent_t a, b; };
 struct Timing {
@@ -180,6 +180,8 @@ struct Plan {
     int mid_grid;          // cooperative grid of k_mid (co-resident blocks)
     int mid_tiles;         // R blocks each k_mid block holds in shared memory
     int mid_hold_v;        // V tiles each k_mid block holds from its phase A to B
+    bool tiny;             // sos_descend runs all its steps in k_tiny_descend (small N, r)
+    int tiny_grid;         // its cooperative grid (0: the problem is not tiny-capable)
     double* d_part;        // k_mid's per-block partial sums [mid_grid][2]
     unsigned* d_rrowx;     // sos_descend, long K: [2][Np] exact R row maxima (step parity)
     unsigned* d_urowr;     // [Np] scales the RQ rows were written with (headroom or exact)
@@ -308,6 +310,10 @@ struct DescendBufs {
 };
 // plans with fewer K-blocks (N / 64) than this use the split step (Plan::split)
 constexpr int kSplitKb = 48;
+// tiny plans (one cooperative kernel per sos_descend call) by default while N^2 r
+// is at most this: measured crossover with the split step between N = r = 286
+// (32.2K vs 31.8K steps/s) and 330 (25.8K vs 29.5K), profiles/r2_tiny_ab.log
+constexpr double kTinyMaxWork = 2.0e7;
 // split step, between forward and backward: residual + loss, step bookkeeping
 // (t += 1, loss record: losses[0], or the sos_descend array from DevOpt with
 // losses_from_opt), with colmax the exact column maxima of V (atomicMax into
@@ -323,6 +329,8 @@ void launch_update_rows(Plan& P, float* V, uint8_t* vq_next, const unsigned* vro
                         cudaStream_t st);
 // cooperative grid of k_mid (blocks) and the R blocks each holds (tiles_per_block)
 int mid_grid_for(int64_t nkbN, int64_t rowsVT, int64_t M, int num_sms, int* tiles_per_block, int* hold_v);
+int tiny_grid_for(int64_t N, int64_t r, int num_sms);
+int launch_tiny_descend(Plan& P, float* V, const float* p, int64_t steps, cudaStream_t st);
 // slices written by the update use kHeadroom x the current row maximum
 constexpr float kHeadroom = 2.f;
 

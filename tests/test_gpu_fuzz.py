@@ -71,7 +71,7 @@ def test_fuzz_shape(sos, n, d, r):
     assert rel_l2(dv_q, dv_s) <= 1e-4
 
 
-def _variant_shapes(count=12, seed=77):
+def _variant_shapes(count=14, seed=77):
     rng = np.random.default_rng(seed)
     out = []
     while len(out) < count:
@@ -81,9 +81,11 @@ def _variant_shapes(count=12, seed=77):
         if N > 1200 or math.comb(n + 2 * d - 1, 2 * d) > 200_000:
             continue
         r = int(rng.integers(1, 600))
-        opts = [{"split": True}, {"split": False}, {"split": True, "tile_w": 128},
-                {"split": False, "rmax_direct": True, "vtq_from_update": True},
-                {"split": True, "tile_w": 112}, {"split": False, "tile_w": 144}][len(out) % 6]
+        opts = [{"split": True, "tiny": False}, {"split": False, "tiny": False}, {"tiny": True},
+                {"split": True, "tile_w": 128, "tiny": False},
+                {"split": False, "rmax_direct": True, "vtq_from_update": True, "tiny": False},
+                {"split": True, "tile_w": 112, "tiny": False}, {"split": False, "tile_w": 144, "tiny": False},
+                ][len(out) % 7]
         out.append((n, d, r, opts))
     return out
 
@@ -91,7 +93,8 @@ def _variant_shapes(count=12, seed=77):
 @pytest.mark.parametrize("n,d,r,opts", _variant_shapes())
 def test_fuzz_descend_variants(sos, n, d, r, opts):
     """Random shapes through sos_descend under each step variant (split step,
-    fused step, 128 / 112 / 144-wide tiles, direct R maxima + V^T slices from the update):
+    fused step, the one-kernel tiny descent, 128 / 112 / 144-wide tiles, direct R
+    maxima + V^T slices from the update):
     3 GD steps against the oracle's GD (V_3 - V_0 element-wise) and its losses."""
     o = OracleIndex(n, d)
     ix = sos.SosIndex(n, d)

@@ -1,0 +1,128 @@
+"""Tiny plans (sos_plan_opts.tiny, paper_2410_19844_b200/csrc/sos_tiny.cu): the
+whole sos_descend call in one cooperative kernel of fp32 CUDA-core tiles.  It
+follows the same iteration as the oracle's or_descent (Eq. 2):
+losses[t] = L(V_t), then the GD / Adam update with step index t + 1."""
+import math
+
+import numpy as np
+import pytest
+
+import seeded_inputs as si
+from oracle import OracleIndex
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sos():
+    import paper_2410_19844_b200 as m
+    m.load()
+    return m
+
+
+def rel_l2(got, want):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    den = np.linalg.norm(want)
+    return np.linalg.norm(got - want) / (den if den > 0 else 1.0)
+
+
+def _problem(o, r, seed):
+    V0 = si.v0(o.N, r, seed=seed)
+    p = o.forward(si.planted_w(o.N, max(1, r // 2), seed=seed + 1)).astype(np.float32)
+    return V0, p
+
+
+@pytest.mark.parametrize("n,d,r,kind", [(8, 4, 330, "adam"), (8, 4, 330, "gd"), (4, 3, 20, "adam"),
+                                        (20, 2, 97, "adam"), (3, 5, 33, "gd")])
+def test_tiny_descent_vs_oracle(sos, n, d, r, kind):
+    """Config 1 (N = r = 330: ragged 32-blocks), config 0, a quartic with r not a
+    multiple of 32, and a shape with N < 32: 4 steps element-wise against the
+    oracle's descent (V_4 - V_0 within 1e-5 for GD, 1e-4 for Adam, whose first
+    steps are ~lr * sign(g) and amplify rounding of small gradients), losses 1e-5."""
+    o = OracleIndex(n, d)
+    ix = sos.SosIndex(n, d)
+    plan = sos.SosPlan(ix, r, tiny=True)
+    V0, p = _problem(o, r, seed=n * 10 + r)
+    if kind == "gd":
+        _, g1, _, _ = o.loss_grad(V0, p)
+        lr = 0.02 * np.linalg.norm(V0) / max(np.linalg.norm(g1), 1e-30)
+    else:
+        lr = 1e-3
+    plan.opt_init(kind, lr)
+    Vd = torch.from_numpy(V0.copy()).cuda()
+    ld = plan.descend(Vd, torch.from_numpy(p).cuda(), 4).cpu().numpy()
+    assert plan.launch_count == 1  # the whole call is one kernel
+    Vo, Lo = o.descent(V0, p, kind, 4, lr)
+    assert rel_l2(Vd.cpu().numpy() - V0, Vo - V0) <= (1e-5 if kind == "gd" else 1e-4)
+    assert np.allclose(ld, Lo[:4], rtol=1e-5)
+
+
+def test_tiny_vs_split_long_run(sos):
+    """200 Adam steps of the tiny kernel against the split (tensor-core) step on
+    the same quartic: the trajectories agree to fp32-class precision."""
+    ix = sos.SosIndex(20, 2)  # N = 210
+    r = 150
+    W = torch.from_numpy(si.planted_w(ix.N, 75, 5)).cuda()
+    ref = sos.SosPlan(ix, 75, tiny=False)
+    p = ref.forward(W)
+    V0 = torch.from_numpy(si.v0(ix.N, r, seed=6)).cuda()
+    out = {}
+    for tiny in (True, False):
+        plan = sos.SosPlan(ix, r, tiny=tiny)
+        plan.opt_init("adam", 1e-3)
+        V = V0.clone()
+        losses = plan.descend(V, p, 200).cpu().numpy()
+        out[tiny] = (V.cpu().numpy(), losses)
+        plan.close()
+    (Vt, Lt), (Vs, Ls) = out[True], out[False]
+    assert Lt[-1] < 0.1 * Lt[0]
+    assert rel_l2(Lt, Ls) <= 1e-4
+    assert rel_l2(Vt - V0.cpu().numpy(), Vs - V0.cpu().numpy()) <= 1e-3
+
+
+def test_tiny_stopping_rule(sos):
+    """The device-side stopping rule inside the kernel: once
+    ||coef - p||^2 <= tol ||p||^2, V freezes and the recorded loss stays put."""
+    ix = sos.SosIndex(6, 2)  # N = 21
+    r = 21
+    plan = sos.SosPlan(ix, r, tiny=True)
+    W = torch.from_numpy(si.planted_w(ix.N, 10, 3)).cuda()
+    p = sos.SosPlan(ix, 10).forward(W)
+    V = torch.from_numpy(si.v0(ix.N, r, seed=4)).cuda()
+    plan.opt_init("adam", 1e-2)
+    plan.set_stop(1e-4)
+    pn = float((p.double() ** 2).sum())
+    losses = plan.descend(V, p, 3000).cpu().numpy()
+    hit = np.nonzero(losses <= 1e-4 * pn)[0]
+    assert hit.size > 0, losses[-1] / pn
+    k = hit[0]
+    # V frozen from the first step under the tolerance: the loss is recomputed every
+    # step (coefficient atomics in a different order), so equal to fp32 rounding
+    assert np.allclose(losses[k:], losses[k], rtol=1e-5, atol=0)
+    Vf = V.clone()
+    plan.descend(V, p, 5)
+    assert torch.equal(V, Vf)
+
+
+def test_tiny_is_default_for_small_problems(sos):
+    ix = sos.SosIndex(20, 2)  # the paper's n = 20 quartic: N = r = 210
+    plan = sos.SosPlan(ix, 210)
+    plan.opt_init("adam", 1e-3)
+    V = torch.from_numpy(si.v0(ix.N, 210, seed=1)).cuda()
+    p = torch.zeros(ix.M, device="cuda")
+    n0 = plan.launch_count
+    plan.descend(V, p, 10)
+    assert plan.launch_count - n0 == 1
+
+
+def test_tiny_not_default_for_larger_problems(sos):
+    ix = sos.SosIndex(8, 4)  # config 1, N = r = 330: the split step (4 launches per step)
+    plan = sos.SosPlan(ix, 330)
+    plan.opt_init("adam", 1e-3)
+    V = torch.from_numpy(si.v0(ix.N, 330, seed=1)).cuda()
+    p = torch.zeros(ix.M, device="cuda")
+    n0 = plan.launch_count
+    plan.descend(V, p, 4)
+    assert plan.launch_count - n0 > 4

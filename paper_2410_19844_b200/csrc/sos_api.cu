@@ -302,7 +302,7 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
     if (P.split) P.mid_grid = mid_grid_for(P.nkbN, P.rowsVT, M, sms, &P.mid_tiles, &P.mid_hold_v);
     // tiny plans: the whole descent in one cooperative kernel (sos_tiny.cu) for
     // small N and r, where the split step's four launches are latency-bound
-    P.tiny_grid = tiny_grid_for(N, r, sms);
+    P.tiny_grid = tiny_grid_for(sms);
     P.tiny = P.tiny_grid > 0 && pick(o.tiny, (double)N * N * r <= kTinyMaxWork);
     // row chunks of the last step's V release = the raster's row groups
     P.sig_blocks = (int)tile_group();

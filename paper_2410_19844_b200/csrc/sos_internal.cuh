@@ -329,7 +329,7 @@ void launch_update_rows(Plan& P, float* V, uint8_t* vq_next, const unsigned* vro
                         cudaStream_t st);
 // cooperative grid of k_mid (blocks) and the R blocks each holds (tiles_per_block)
 int mid_grid_for(int64_t nkbN, int64_t rowsVT, int64_t M, int num_sms, int* tiles_per_block, int* hold_v);
-int tiny_grid_for(int64_t N, int64_t r, int num_sms);
+int tiny_grid_for(int num_sms);
 int launch_tiny_descend(Plan& P, float* V, const float* p, int64_t steps, cudaStream_t st);
 // slices written by the update use kHeadroom x the current row maximum
 constexpr float kHeadroom = 2.f;

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "sm100_ptx.cuh"
 #include "sos_internal.cuh"
@@ -54,7 +55,14 @@ struct TinyArgs {
     int64_t steps;
     int nbN, nbR;  // 32-blocks of rows / of r
     int chF, chB;  // K-chunks per work item of F (over r) and of B (over N)
+    int trace;     // experiment build: block 0 prints the phase times of step 10
 };
+#ifdef SOS_EXPERIMENTS
+#define TINY_MARK(k) do { if (a.trace && step == 10 && blockIdx.x == 0 && t == 0) { \
+    unsigned long long now_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_)); tm[k] = now_; } } while (0)
+#else
+#define TINY_MARK(k) do { } while (0)
+#endif
 
 __device__ __forceinline__ double tiny_warp_sum(double v) {
 #pragma unroll
@@ -86,7 +94,11 @@ __global__ void __launch_bounds__(kTinyThreads, 4) k_tiny_descend(const TinyArgs
     const int64_t N = a.N, r = a.r;
     const int64_t nfwd = (int64_t)a.nbN * (a.nbN + 1) / 2, nbwd = (int64_t)a.nbN * a.nbR;
     const double tol = a.opt->stop_tol;
+#ifdef SOS_EXPERIMENTS
+    unsigned long long tm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#endif
     for (int64_t step = 0; step < a.steps; ++step) {
+        TINY_MARK(0);
         // ---- F: Gram tiles {I <= J} scattered into coef
         if (blockIdx.x == 0 && t == 0) advance_step(a.opt);  // read by U, after three barriers
         const int64_t sF = (a.nbR + a.chF - 1) / a.chF;  // K-slices per Gram tile
@@ -124,7 +136,9 @@ __global__ void __launch_bounds__(kTinyThreads, 4) k_tiny_descend(const TinyArgs
                 }
             }
         }
+        TINY_MARK(1);
         grid.sync();
+        TINY_MARK(2);
         // ---- L: residual, loss, |p|^2; coef cleared for the next step (each
         // coefficient is read and cleared by the same thread)
         {
@@ -144,7 +158,9 @@ __global__ void __launch_bounds__(kTinyThreads, 4) k_tiny_descend(const TinyArgs
                 a.part[2 * blockIdx.x + 1] = pn;
             }
         }
+        TINY_MARK(3);
         grid.sync();
+        TINY_MARK(4);
         // ---- B: totals (same order in every block), stopping rule, grad tiles
         {
             double l = 0.0, pn = 0.0;
@@ -168,6 +184,7 @@ __global__ void __launch_bounds__(kTinyThreads, 4) k_tiny_descend(const TinyArgs
             if (L) L[a.opt->loss_idx++] = tot_s[0];
         }
         if (stopped) continue;  // grid-uniform: the next step's F (coef is clear)
+
         const int64_t sB = (a.nbN + a.chB - 1) / a.chB;  // K-slices per gradient tile
         for (int64_t w = blockIdx.x; w < nbwd * sB; w += gridDim.x) {
             const int64_t b = w / sB, j_lo = (w % sB) * a.chB * kT, j_hi = min(N, j_lo + (int64_t)a.chB * kT);
@@ -205,7 +222,9 @@ __global__ void __launch_bounds__(kTinyThreads, 4) k_tiny_descend(const TinyArgs
                 if (i < N && c < r) red_add_f32(a.grad + i * r + c, 4.f * acc[q]);
             }
         }
+        TINY_MARK(5);
         grid.sync();  // every block has read V; the gradient is complete
+        TINY_MARK(6);
         // ---- U: the update (elementwise), gradient buffer cleared
         {
             const DevOpt o = *a.opt;
@@ -224,14 +243,21 @@ __global__ void __launch_bounds__(kTinyThreads, 4) k_tiny_descend(const TinyArgs
                 }
             }
         }
+        TINY_MARK(7);
         grid.sync();  // V_{t+1} complete before the next F
+        TINY_MARK(8);
+#ifdef SOS_EXPERIMENTS
+        if (a.trace && step == 10 && blockIdx.x == 0 && t == 0)
+            printf("k_tiny step (us): F %.2f | sync %.2f | L %.2f | sync %.2f | B %.2f | sync %.2f | U %.2f | sync %.2f "
+                   "(grid %d, chF %d, chB %d)\n", (tm[1] - tm[0]) * 1e-3, (tm[2] - tm[1]) * 1e-3, (tm[3] - tm[2]) * 1e-3,
+                   (tm[4] - tm[3]) * 1e-3, (tm[5] - tm[4]) * 1e-3, (tm[6] - tm[5]) * 1e-3, (tm[7] - tm[6]) * 1e-3,
+                   (tm[8] - tm[7]) * 1e-3, (int)gridDim.x, a.chF, a.chB);
+#endif
     }
 }
 
 // blocks of the cooperative grid: all that fit at once
-int tiny_grid_for(int64_t N, int64_t r, int num_sms) {
-    (void)N;
-    (void)r;
+int tiny_grid_for(int num_sms) {
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tiny_descend, kTinyThreads, 0) != cudaSuccess || nb < 1) {
         cudaGetLastError();
@@ -265,8 +291,21 @@ int launch_tiny_descend(Plan& P, float* V, const float* p, int64_t steps, cudaSt
     const int64_t G = P.tiny_grid, nf = (int64_t)a.nbN * (a.nbN + 1) / 2, nbw = (int64_t)a.nbN * a.nbR;
     a.chF = (int)std::max<int64_t>(1, (nf * a.nbR + G - 1) / G);
     a.chB = (int)std::max<int64_t>(1, (nbw * a.nbN + G - 1) / G);
+    a.trace = 0;
+    unsigned grid = (unsigned)P.tiny_grid;
+#ifdef SOS_EXPERIMENTS
+    {
+        const char* e = getenv("SOS_TINY_TRACE");
+        a.trace = e && atoi(e) ? 1 : 0;
+        const char* g = getenv("SOS_TINY_GRID");  // blocks per SM (<= the occupancy limit)
+        if (g && atoi(g) > 0) grid = std::min<unsigned>(grid, (unsigned)(atoi(g) * P.num_sms));
+        const char* c = getenv("SOS_TINY_CH");  // "F,B" chunks per work item
+        if (c) sscanf(c, "%d,%d", &a.chF, &a.chB);
+    }
+#endif
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(P.tiny_grid);
+    cfg.gridDim = dim3(grid);
+
     cfg.blockDim = dim3(kTinyThreads);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];

@@ -87,6 +87,26 @@ def step_flops(N: int, r: int) -> dict:
     return {"fwd": fwd, "bwd": bwd, "step": fwd + bwd}
 
 
+# fp32 CUDA-core peak for tiny plans (one cooperative kernel of fp32 FMA tiles per
+# sos_descend call): 148 SMs x 128 FP32 lanes x 2 flops x 1965 MHz (clocks.max.sm,
+# B200_PROFILING.md); B300_MICROARCH.md measures the 3-register FFMA at half that
+# issue rate (rt_SMSP = 2), so the practical ceiling is ~37 TFLOP/s
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def tiny_roofline(flops: dict, tiny_ms: float, steps_covered: int) -> dict:
+    """A tiny plan's whole descent is one kernel: achieved = the step's algorithmic
+    fp32 flops / its time per step (the timed launches covered steps_covered
+    steps), against the fp32 FMA peak (bound "alu"; the kernel is latency-bound at
+    these sizes, so the fraction is small)."""
+    per_step_s = tiny_ms / 1e3 / max(1, steps_covered)
+    achieved = flops["step"] / per_step_s / 1e12
+    return {"bound": "alu", "kernel": "k_tiny_descend (whole sos_descend call, fp32 CUDA-core FMA tiles)",
+            "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
+            "traffic": None, "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 flops x 1965 MHz",
+            "flops_per_step": flops["step"]}
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -413,10 +433,11 @@ def run_ours(args):
     value = ws * args.steps / (ms / 1e3)
     bwd_ms, bwd_n = kt["gemm_bwd"]
     fwd_ms, fwd_n = kt["gemm_fwd"]
+    tiny_ms, tiny_n = kt.get("tiny", (0.0, 0))
     total_kernel_ms = sum(v[0] for v in kt.values())
     peak_tensor = peaks["bf16_tflops_sustained"] * I8_OVER_BF16 / N_PRODUCTS
-    achieved_bwd = flops["bwd"] / (bwd_ms / bwd_n / 1e3) / 1e12
-    achieved_fwd = flops["fwd"] / (fwd_ms / fwd_n / 1e3) / 1e12
+    achieved_bwd = flops["bwd"] / (bwd_ms / bwd_n / 1e3) / 1e12 if bwd_n else None
+    achieved_fwd = flops["fwd"] / (fwd_ms / fwd_n / 1e3) / 1e12 if fwd_n else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -431,14 +452,18 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "fp32-equiv (3 x s8 slices, exact s32 accumulation)",
-        "precision": "tensor-core GEMMs on three int8 slices per fp32 value with exact s32 accumulation "
-                     "(fp32-class: ~1e-7 relative vs fp64); residual, loss (fp64 sums), V and Adam state in fp32",
+        "vs_baseline": None,
+        "dtype": "f32 (CUDA-core FMA, tiny plan)" if tiny_n else "fp32-equiv (3 x s8 slices, exact s32 accumulation)",
+        "precision": ("fp32 FMA tiles on CUDA cores (tiny plan: one cooperative kernel per sos_descend call); loss "
+                      "fp64 sums" if tiny_n else
+                      "tensor-core GEMMs on three int8 slices per fp32 value with exact s32 accumulation "
+                      "(fp32-class: ~1e-7 relative vs fp64); residual, loss (fp64 sums), V and Adam state in fp32"),
         "data": "synthetic (seeded Gaussian V0 and planted W, BASELINE.json recipe)",
         "config": config_block(cfg, args, ws),
         "effective_tflops": eff_tflops,
-        "tensor_roofline_frac_step": eff_tflops / peak_tensor,
-        "roofline": {"bound": "tensor", "kernel": "k_gemmq<bwd+update> (4RV, Adam)", "achieved": achieved_bwd,
+        "tensor_roofline_frac_step": None if tiny_n else eff_tflops / peak_tensor,
+        "roofline": tiny_roofline(flops, tiny_ms, args.steps if inline else min(args.steps, 50)) if tiny_n else {
+                     "bound": "tensor", "kernel": "k_gemmq<bwd+update> (4RV, Adam)", "achieved": achieved_bwd,
                      "peak": peak_tensor, "unit": "TFLOP/s", "frac": achieved_bwd / peak_tensor,
                      "traffic": traffic,
                      "peak_source": f"{peak_src} bf16_tflops_sustained {peaks['bf16_tflops_sustained']} x "

@@ -35,12 +35,14 @@ def _problem(o, r, seed):
 
 
 @pytest.mark.parametrize("n,d,r,kind", [(8, 4, 330, "adam"), (8, 4, 330, "gd"), (4, 3, 20, "adam"),
-                                        (20, 2, 97, "adam"), (3, 5, 33, "gd")])
+                                        (20, 2, 97, "adam"), (3, 5, 33, "gd"), (1, 3, 1, "gd"),
+                                        (2, 1, 1, "adam"), (5, 2, 64, "gd"), (7, 3, 65, "adam")])
 def test_tiny_descent_vs_oracle(sos, n, d, r, kind):
     """Config 1 (N = r = 330: ragged 32-blocks), config 0, a quartic with r not a
     multiple of 32, and a shape with N < 32: 4 steps element-wise against the
     oracle's descent (V_4 - V_0 within 1e-5 for GD, 1e-4 for Adam, whose first
-    steps are ~lr * sign(g) and amplify rounding of small gradients), losses 1e-5."""
+    steps are ~lr * sign(g) and amplify rounding of small gradients), losses 1e-5;
+    degenerate N = 1 / r = 1, and tile-edge shapes (N = 15, r = 64; N = 84, r = 65)."""
     o = OracleIndex(n, d)
     ix = sos.SosIndex(n, d)
     plan = sos.SosPlan(ix, r, tiny=True)

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) k_rmax(const uint32_t* __restrict__ pt, c
                                               int64_t nkb, unsigned* __restrict__ rrow, const Scalars* sc,
                                               const DevOpt* opt, int use_stop) {
     if (descent_stopped(sc, opt, use_stop)) return;
-    __shared__ float tile[kPtW][kPtW + 1];
+    __shared__ __align__(16) float tile[kPtW * kPtW];  // slots swizzled (rt_slot)
     const int t = threadIdx.x;
     const int64_t npairs = nkb * (nkb + 1) / 2;
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
@@ -195,20 +195,23 @@ __global__ void __launch_bounds__(256) k_rmax(const uint32_t* __restrict__ pt, c
         for (int u = 0; u < 4; ++u) {
             const int e = (u * 256 + t) * 4;
             const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + e));
-            float* d = &tile[e >> 6][e & 63];
-            d[0] = k.x != kInvalidRank ? fabsf(__ldg(res + k.x)) : 0.f;
-            d[1] = k.y != kInvalidRank ? fabsf(__ldg(res + k.y)) : 0.f;
-            d[2] = k.z != kInvalidRank ? fabsf(__ldg(res + k.z)) : 0.f;
-            d[3] = k.w != kInvalidRank ? fabsf(__ldg(res + k.w)) : 0.f;
+            rt_store4(tile, e >> 6, (e & 63) >> 2,
+                      make_float4(k.x != kInvalidRank ? fabsf(__ldg(res + k.x)) : 0.f,
+                                  k.y != kInvalidRank ? fabsf(__ldg(res + k.y)) : 0.f,
+                                  k.z != kInvalidRank ? fabsf(__ldg(res + k.z)) : 0.f,
+                                  k.w != kInvalidRank ? fabsf(__ldg(res + k.w)) : 0.f));
         }
         __syncthreads();
-        // thread t: row (t & 63) of the block if t < 64 ... four threads per line
+        // thread t: row (t >> 2) of I across columns 16 (t & 3) .. +15, and column
+        // (t >> 2) of the block = row of J across rows 16 (t & 3) .. +15
         const int line = t >> 2, part = t & 3;
+        float x[16];
+        rt_row16(tile, line, part, x);
         float mr = 0.f, mc = 0.f;
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-            mr = fmaxf(mr, tile[line][part * 16 + e]);   // row `line` of I
-            mc = fmaxf(mc, tile[part * 16 + e][line]);   // column `line` = row of J
+            mr = fmaxf(mr, x[e]);                               // row `line` of I
+            mc = fmaxf(mc, rt_at(tile, part * 16 + e, line));   // column `line` = row of J
         }
         mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 1));
         mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 2));
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(256, 6) k_pack_rq_sym(const uint32_t* __restri
                                                      uint8_t* __restrict__ RQ, const Scalars* sc, const DevOpt* opt,
                                                      int use_stop, unsigned* __restrict__ rrow_out) {
     if (descent_stopped(sc, opt, use_stop)) return;
-    __shared__ float tile[kPtW][kPtW + 1];  // [row in I][j in J], padded
+    __shared__ __align__(16) float tile[kPtW * kPtW];  // [row in I][j in J], slots swizzled (rt_slot)
     const int t = threadIdx.x;
     const int64_t npairs = nkb * (nkb + 1) / 2;
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
@@ -254,21 +257,19 @@ __global__ void __launch_bounds__(256, 6) k_pack_rq_sym(const uint32_t* __restri
         for (int u = 0; u < 4; ++u) {
             const int e = (u * 256 + t) * 4;
             const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + e));
-            float* d = &tile[e >> 6][e & 63];
-            d[0] = k.x != kInvalidRank ? __ldg(res + k.x) : 0.f;
-            d[1] = k.y != kInvalidRank ? __ldg(res + k.y) : 0.f;
-            d[2] = k.z != kInvalidRank ? __ldg(res + k.z) : 0.f;
-            d[3] = k.w != kInvalidRank ? __ldg(res + k.w) : 0.f;
+            rt_store4(tile, e >> 6, (e & 63) >> 2,
+                      make_float4(k.x != kInvalidRank ? __ldg(res + k.x) : 0.f, k.y != kInvalidRank ? __ldg(res + k.y) : 0.f,
+                                  k.z != kInvalidRank ? __ldg(res + k.z) : 0.f, k.w != kInvalidRank ? __ldg(res + k.w) : 0.f));
         }
         __syncthreads();
         const int r = t >> 2, c = t & 3;
         float x[16];
         uint4 q[3];
         float mr = 0.f;
+        rt_row16(tile, r, c, x);
+        if (kHr) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            x[e] = tile[r][c * 16 + e];
-            if (kHr) mr = fmaxf(mr, fabsf(x[e]));
+            for (int e = 0; e < 16; ++e) mr = fmaxf(mr, fabsf(x[e]));
         }
         const unsigned urI = kHr ? __float_as_uint(kHeadroom * __uint_as_float(__ldg(rrow + I * kPtW + r)))
                                  : __ldg(rrow + I * kPtW + r);
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(256, 6) k_pack_rq_sym(const uint32_t* __restri
         if (I != J) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-                x[e] = tile[c * 16 + e][r];
+                x[e] = rt_at(tile, c * 16 + e, r);
                 if (kHr) mc = fmaxf(mc, fabsf(x[e]));
             }
             const unsigned urJ = kHr ? __float_as_uint(kHeadroom * __uint_as_float(__ldg(rrow + J * kPtW + r)))
@@ -656,20 +657,18 @@ constexpr int kMidMaxHeld = 12;  // R blocks a k_mid block can hold in shared me
 constexpr int kMidMaxHeldV = 4;  // V tiles a k_mid block can hold from phase A to B
 
 // the 64 x 64 block {I <= J} of R (I's rows x J's columns) gathered through the
-// stored PT block into a padded shared-memory tile (plain loads: res is written
-// in the same kernel)
+// stored PT block into a swizzled shared-memory tile (rt_slot; the first 4096
+// floats of a 64 x 65 slot; plain loads: res is written in the same kernel)
 __device__ __forceinline__ void gather_r_tile(const uint32_t* __restrict__ pt, const float* res, int64_t I, int64_t J,
-                                              float (*tile)[kPtW + 1], int t) {
+                                              float* tile, int t) {
     const uint32_t* p0 = pt + pt_entry(I * kPtW, J * kPtW);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int e = (u * 256 + t) * 4;
         const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + e));
-        float* d = &tile[e >> 6][e & 63];
-        d[0] = k.x != kInvalidRank ? res[k.x] : 0.f;
-        d[1] = k.y != kInvalidRank ? res[k.y] : 0.f;
-        d[2] = k.z != kInvalidRank ? res[k.z] : 0.f;
-        d[3] = k.w != kInvalidRank ? res[k.w] : 0.f;
+        rt_store4(tile, e >> 6, (e & 63) >> 2,
+                  make_float4(k.x != kInvalidRank ? res[k.x] : 0.f, k.y != kInvalidRank ? res[k.y] : 0.f,
+                              k.z != kInvalidRank ? res[k.z] : 0.f, k.w != kInvalidRank ? res[k.w] : 0.f));
     }
 }
 
@@ -884,16 +883,17 @@ __global__ void SOS_MID_BOUNDS k_mid(const MidArgs a) {
         for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++slot) {
             int64_t I, J;
             block_pair(pr, I, J);
-            float(*tile)[kPtW + 1] =
-                a.hold ? reinterpret_cast<float(*)[kPtW + 1]>(smem_tiles + slot * kPtW * (kPtW + 1)) : tile0;
+            float* tile = a.hold ? smem_tiles + slot * kPtW * (kPtW + 1) : &tile0[0][0];
             gather_r_tile(a.pt, a.res, I, J, tile, t);
             __syncthreads();
             const int line = t >> 2, part = t & 3;
+            float x[16];
+            rt_row16(tile, line, part, x);
             float mr = 0.f, mc = 0.f;
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-                mr = fmaxf(mr, fabsf(tile[line][part * 16 + e]));
-                mc = fmaxf(mc, fabsf(tile[part * 16 + e][line]));
+                mr = fmaxf(mr, fabsf(x[e]));
+                mc = fmaxf(mc, fabsf(rt_at(tile, part * 16 + e, line)));
             }
             mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 1));
             mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 2));
@@ -929,8 +929,7 @@ __global__ void SOS_MID_BOUNDS k_mid(const MidArgs a) {
     for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x, ++slot) {
         int64_t I, J;
         block_pair(pr, I, J);
-        float(*tile)[kPtW + 1] =
-            a.hold ? reinterpret_cast<float(*)[kPtW + 1]>(smem_tiles + slot * kPtW * (kPtW + 1)) : tile0;
+        float* tile = a.hold ? smem_tiles + slot * kPtW * (kPtW + 1) : &tile0[0][0];
         if (!a.hold) {
             gather_r_tile(a.pt, a.res, I, J, tile, t);
             __syncthreads();
@@ -938,13 +937,12 @@ __global__ void SOS_MID_BOUNDS k_mid(const MidArgs a) {
         const int rr = t >> 2, c = t & 3;
         float x[16];
         uint4 q[3];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) x[e] = tile[rr][c * 16 + e];
+        rt_row16(tile, rr, c, x);
         slice16(x, slice_scale(a.rrow[I * kPtW + rr]), q);
         store_q16(a.RQ, J, I * kPtW + rr, c, a.nkbN, a.Np, q);
         if (I != J) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) x[e] = tile[c * 16 + e][rr];
+            for (int e = 0; e < 16; ++e) x[e] = rt_at(tile, c * 16 + e, rr);
             slice16(x, slice_scale(a.rrow[J * kPtW + rr]), q);
             store_q16(a.RQ, I, J * kPtW + rr, c, a.nkbN, a.Np, q);
         }

@@ -71,6 +71,39 @@ __device__ __forceinline__ void store_q16(uint8_t* base, int64_t kb, int64_t row
     for (int s = 0; s < 3; ++s) *reinterpret_cast<uint4*>(base + q_offset(s, kb, row, c, nkb, rows_total)) = q[s];
 }
 
+// A 64 x 64 fp32 tile of R in shared memory (16 KB, no padding), its 16-byte
+// slots XOR-swizzled so that the three access patterns of the R packers are
+// free of bank conflicts with 256 threads:
+//   * the gather: thread t stores float4 slot (t & 15) of row 16u + (t >> 4)
+//     (a quarter-warp: one row, 8 consecutive slots);
+//   * rt_row16: thread (r = t >> 2, c = t & 3) loads row r, columns 16c .. 16c+15
+//     as four float4 (a quarter-warp: rows {2m, 2m+1} x c = 0..3);
+//   * rt_at column reads: thread (r, c) reads row 16c + e, column r (a warp:
+//     rows 16c + e for c = 0..3 x 8 consecutive columns).
+// slot = col4 ^ g(row) ^ 2 (col4 >> 3): the col4 term separates c from c + 2 in
+// a row read, bit 0 of g = row & 1 separates its two rows, bits 1-2 of g =
+// (row >> 4) & 3 separate the four rows of a column read.
+__device__ __forceinline__ int rt_slot(int row, int col4) {
+    return col4 ^ ((row & 1) | (((row >> 4) & 3) << 1)) ^ (((col4 >> 3) & 1) << 1);
+}
+__device__ __forceinline__ void rt_store4(float* tile, int row, int col4, float4 v) {
+    reinterpret_cast<float4*>(tile + row * 64)[rt_slot(row, col4)] = v;
+}
+__device__ __forceinline__ float rt_at(const float* tile, int row, int col) {
+    return tile[row * 64 + rt_slot(row, col >> 2) * 4 + (col & 3)];
+}
+__device__ __forceinline__ void rt_row16(const float* tile, int row, int c, float (&x)[16]) {
+    const float4* p = reinterpret_cast<const float4*>(tile + row * 64);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float4 w = p[rt_slot(row, 4 * c + k)];
+        x[4 * k] = w.x;
+        x[4 * k + 1] = w.y;
+        x[4 * k + 2] = w.z;
+        x[4 * k + 3] = w.w;
+    }
+}
+
 // VTQ row k (a column of V), K = j (a row of V): a 64 (j) x 64 (k) tile of V is
 // transposed through shared memory; thread (k, chunk c) writes 16 j's.  Used by
 // k_pack_vtq, k_mid (kThreads = 256, __syncthreads) and by the aux warps of the

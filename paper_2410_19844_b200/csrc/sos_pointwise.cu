@@ -193,9 +193,10 @@ __global__ void __launch_bounds__(256) k_rmax(const uint32_t* __restrict__ pt, c
         const uint32_t* p0 = pt + pt_entry(I * kPtW, J * kPtW);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int e = (u * 256 + t) * 4;
-            const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + e));
-            rt_store4(tile, e >> 6, (e & 63) >> 2,
+            int row, col4;
+            rt_gather_pos(t, u, row, col4);
+            const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + row * 64 + col4 * 4));
+            rt_store4<kGatherBlocks>(tile, row, col4,
                       make_float4(k.x != kInvalidRank ? fabsf(__ldg(res + k.x)) : 0.f,
                                   k.y != kInvalidRank ? fabsf(__ldg(res + k.y)) : 0.f,
                                   k.z != kInvalidRank ? fabsf(__ldg(res + k.z)) : 0.f,
@@ -206,12 +207,12 @@ __global__ void __launch_bounds__(256) k_rmax(const uint32_t* __restrict__ pt, c
         // (t >> 2) of the block = row of J across rows 16 (t & 3) .. +15
         const int line = t >> 2, part = t & 3;
         float x[16];
-        rt_row16(tile, line, part, x);
+        rt_row16<kGatherBlocks>(tile, line, part, x);
         float mr = 0.f, mc = 0.f;
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
             mr = fmaxf(mr, x[e]);                               // row `line` of I
-            mc = fmaxf(mc, rt_at(tile, part * 16 + e, line));   // column `line` = row of J
+            mc = fmaxf(mc, rt_at<kGatherBlocks>(tile, part * 16 + e, line));   // column `line` = row of J
         }
         mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 1));
         mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 2));
@@ -255,9 +256,10 @@ __global__ void __launch_bounds__(256, 6) k_pack_rq_sym(const uint32_t* __restri
         const uint32_t* p0 = pt + pt_entry(I * kPtW, J * kPtW);  // 64 rows x 64 ranks, contiguous
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int e = (u * 256 + t) * 4;
-            const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + e));
-            rt_store4(tile, e >> 6, (e & 63) >> 2,
+            int row, col4;
+            rt_gather_pos(t, u, row, col4);
+            const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + row * 64 + col4 * 4));
+            rt_store4<kGatherBlocks>(tile, row, col4,
                       make_float4(k.x != kInvalidRank ? __ldg(res + k.x) : 0.f, k.y != kInvalidRank ? __ldg(res + k.y) : 0.f,
                                   k.z != kInvalidRank ? __ldg(res + k.z) : 0.f, k.w != kInvalidRank ? __ldg(res + k.w) : 0.f));
         }
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(256, 6) k_pack_rq_sym(const uint32_t* __restri
         float x[16];
         uint4 q[3];
         float mr = 0.f;
-        rt_row16(tile, r, c, x);
+        rt_row16<kGatherBlocks>(tile, r, c, x);
         if (kHr) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) mr = fmaxf(mr, fabsf(x[e]));
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(256, 6) k_pack_rq_sym(const uint32_t* __restri
         if (I != J) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-                x[e] = rt_at(tile, c * 16 + e, r);
+                x[e] = rt_at<kGatherBlocks>(tile, c * 16 + e, r);
                 if (kHr) mc = fmaxf(mc, fabsf(x[e]));
             }
             const unsigned urJ = kHr ? __float_as_uint(kHeadroom * __uint_as_float(__ldg(rrow + J * kPtW + r)))
@@ -663,10 +665,10 @@ __device__ __forceinline__ void gather_r_tile(const uint32_t* __restrict__ pt, c
                                               float* tile, int t) {
     const uint32_t* p0 = pt + pt_entry(I * kPtW, J * kPtW);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 4; ++u) {  // row-major map: at config 2 (res ~370 KB) faster than rt_gather_pos
         const int e = (u * 256 + t) * 4;
         const uint4 k = __ldg(reinterpret_cast<const uint4*>(p0 + e));
-        rt_store4(tile, e >> 6, (e & 63) >> 2,
+        rt_store4<kGatherRows>(tile, e >> 6, (e & 63) >> 2,
                   make_float4(k.x != kInvalidRank ? res[k.x] : 0.f, k.y != kInvalidRank ? res[k.y] : 0.f,
                               k.z != kInvalidRank ? res[k.z] : 0.f, k.w != kInvalidRank ? res[k.w] : 0.f));
     }
@@ -888,12 +890,12 @@ __global__ void SOS_MID_BOUNDS k_mid(const MidArgs a) {
             __syncthreads();
             const int line = t >> 2, part = t & 3;
             float x[16];
-            rt_row16(tile, line, part, x);
+            rt_row16<kGatherRows>(tile, line, part, x);
             float mr = 0.f, mc = 0.f;
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
                 mr = fmaxf(mr, fabsf(x[e]));
-                mc = fmaxf(mc, fabsf(rt_at(tile, part * 16 + e, line)));
+                mc = fmaxf(mc, fabsf(rt_at<kGatherRows>(tile, part * 16 + e, line)));
             }
             mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 1));
             mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, 2));
@@ -937,12 +939,12 @@ __global__ void SOS_MID_BOUNDS k_mid(const MidArgs a) {
         const int rr = t >> 2, c = t & 3;
         float x[16];
         uint4 q[3];
-        rt_row16(tile, rr, c, x);
+        rt_row16<kGatherRows>(tile, rr, c, x);
         slice16(x, slice_scale(a.rrow[I * kPtW + rr]), q);
         store_q16(a.RQ, J, I * kPtW + rr, c, a.nkbN, a.Np, q);
         if (I != J) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) x[e] = rt_at(tile, c * 16 + e, rr);
+            for (int e = 0; e < 16; ++e) x[e] = rt_at<kGatherRows>(tile, c * 16 + e, rr);
             slice16(x, slice_scale(a.rrow[J * kPtW + rr]), q);
             store_q16(a.RQ, I, J * kPtW + rr, c, a.nkbN, a.Np, q);
         }

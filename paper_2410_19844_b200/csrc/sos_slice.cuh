@@ -72,31 +72,54 @@ __device__ __forceinline__ void store_q16(uint8_t* base, int64_t kb, int64_t row
 }
 
 // A 64 x 64 fp32 tile of R in shared memory (16 KB, no padding), its 16-byte
-// slots XOR-swizzled so that the three access patterns of the R packers are
-// free of bank conflicts with 256 threads:
-//   * the gather: thread t stores float4 slot (t & 15) of row 16u + (t >> 4)
-//     (a quarter-warp: one row, 8 consecutive slots);
+// slots XOR-swizzled so that the access patterns of the R packers are free of
+// bank conflicts with 256 threads:
+//   * the gather of PT block ranks, two thread maps (kGather):
+//       kGatherRows: thread t stores slot (t & 15) of row 16u + (t >> 4) (a
+//         quarter-warp: one row x 8 consecutive slots) -- k_mid;
+//       kGatherBlocks (rt_gather_pos): a quarter-warp stores rows {2m, 2m+1} x 4
+//         consecutive slots -- k_pack_rq_sym, k_rmax;
 //   * rt_row16: thread (r = t >> 2, c = t & 3) loads row r, columns 16c .. 16c+15
 //     as four float4 (a quarter-warp: rows {2m, 2m+1} x c = 0..3);
 //   * rt_at column reads: thread (r, c) reads row 16c + e, column r (a warp:
 //     rows 16c + e for c = 0..3 x 8 consecutive columns).
 // slot = col4 ^ g(row) ^ 2 (col4 >> 3): the col4 term separates c from c + 2 in
-// a row read, bit 0 of g = row & 1 separates its two rows, bits 1-2 of g =
-// (row >> 4) & 3 separate the four rows of a column read.
+// a row read; rows 2m and 2m+1 differ in bit 0 of g (row reads) and, for
+// kGatherBlocks, also in bit 2 (its gather); bits 1-2 of g take 4 distinct values
+// on rows 16c + e, c = 0..3 (column reads).
+enum { kGatherRows = 0, kGatherBlocks = 1 };
+template <int kGather>
 __device__ __forceinline__ int rt_slot(int row, int col4) {
-    return col4 ^ ((row & 1) | (((row >> 4) & 3) << 1)) ^ (((col4 >> 3) & 1) << 1);
+    const int g = kGather == kGatherBlocks
+                      ? (row & 1) | (((row >> 4) & 1) << 1) | ((((row >> 5) ^ row) & 1) << 2)
+                      : (row & 1) | (((row >> 4) & 3) << 1);
+    return col4 ^ g ^ (((col4 >> 3) & 1) << 1);
 }
+// kGatherBlocks' thread -> (row, 4-column group) map: iteration u (0..3) of warp w
+// covers rows 8 (b >> 2) .. +7 x column groups 4 (b & 3) .. +3, b = 8u + w, so one
+// warp-wide gather touches 8 rows x 4 columns (stride 4).  Pair ranks of nearby
+// rows and columns share or neighbour their product monomials: ~11 distinct
+// 32-byte sectors of res per 32 gathers at config 4 against ~18.7 for 2 rows x 16
+// column groups (tools/gather_sectors.py); the PT loads stay 64-byte row segments.
+__device__ __forceinline__ void rt_gather_pos(int t, int u, int& row, int& col4) {
+    const int b = u * 8 + (t >> 5), l = t & 31;
+    row = 8 * (b >> 2) + (l >> 2);
+    col4 = 4 * (b & 3) + (l & 3);
+}
+template <int kGather>
 __device__ __forceinline__ void rt_store4(float* tile, int row, int col4, float4 v) {
-    reinterpret_cast<float4*>(tile + row * 64)[rt_slot(row, col4)] = v;
+    reinterpret_cast<float4*>(tile + row * 64)[rt_slot<kGather>(row, col4)] = v;
 }
+template <int kGather>
 __device__ __forceinline__ float rt_at(const float* tile, int row, int col) {
-    return tile[row * 64 + rt_slot(row, col >> 2) * 4 + (col & 3)];
+    return tile[row * 64 + rt_slot<kGather>(row, col >> 2) * 4 + (col & 3)];
 }
+template <int kGather>
 __device__ __forceinline__ void rt_row16(const float* tile, int row, int c, float (&x)[16]) {
     const float4* p = reinterpret_cast<const float4*>(tile + row * 64);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const float4 w = p[rt_slot(row, 4 * c + k)];
+        const float4 w = p[rt_slot<kGather>(row, 4 * c + k)];
         x[4 * k] = w.x;
         x[4 * k + 1] = w.y;
         x[4 * k + 2] = w.z;

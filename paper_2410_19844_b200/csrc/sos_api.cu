@@ -12,6 +12,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <cstddef>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "../../include/sos_b200.h"
@@ -72,14 +74,55 @@ static uint64_t binom_u64(int x, int k) {
     return (uint64_t)c;
 }
 
+#ifdef SOS_EXPERIMENTS
+// Experiment build only: every device allocation of the library sits between
+// two kGuardBytes margins of 0xFF bytes (NaN as fp32, so a read past a float
+// buffer poisons the result it feeds); sos_exp_check_guards() reports the
+// allocations whose margins changed, i.e. writes past plan- or index-owned
+// scratch (tests/test_gpu_guard.py).  The shipped library allocates plainly.
+constexpr size_t kGuardBytes = 1 << 16;  // keeps cudaMalloc's 256-byte alignment
+struct GuardRec { char* base; size_t bytes; };
+static std::mutex g_guard_mu;
+static std::map<void*, GuardRec> g_guards;
+#endif
+
 template <class T>
 static int dalloc(T** p, size_t bytes) {
+#ifdef SOS_EXPERIMENTS
+    char* base = nullptr;
+    if (cudaMalloc(reinterpret_cast<void**>(&base), bytes + 2 * kGuardBytes) != cudaSuccess ||
+        cudaMemset(base, 0xFF, bytes + 2 * kGuardBytes) != cudaSuccess) {
+        cudaGetLastError();
+        if (base) cudaFree(base);
+        *p = nullptr;
+        return fail(SOS_ERR_NOMEM, "cudaMalloc(%zu) failed", bytes);
+    }
+    *p = reinterpret_cast<T*>(base + kGuardBytes);
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    g_guards[*p] = GuardRec{base, bytes};
+    return SOS_OK;
+#else
     if (cudaMalloc(reinterpret_cast<void**>(p), bytes) != cudaSuccess) {
         cudaGetLastError();
         *p = nullptr;
         return fail(SOS_ERR_NOMEM, "cudaMalloc(%zu) failed", bytes);
     }
     return SOS_OK;
+#endif
+}
+
+// frees what dalloc returned (nullptr is fine)
+static void dfree(void* p) {
+#ifdef SOS_EXPERIMENTS
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    auto it = g_guards.find(p);
+    if (it == g_guards.end()) return;
+    cudaFree(it->second.base);
+    g_guards.erase(it);
+#else
+    cudaFree(p);
+#endif
 }
 
 extern "C" {
@@ -137,10 +180,10 @@ int sos_build_index(int n, int d, sos_index** out) {
 
 int sos_index_destroy(sos_index* h) {
     if (!h) return SOS_OK;
-    cudaFree(h->ix.d_binom);
-    cudaFree(h->ix.d_ms);
-    cudaFree(h->ix.d_alpha);
-    cudaFree(h->ix.d_pt);
+    dfree(h->ix.d_binom);
+    dfree(h->ix.d_ms);
+    dfree(h->ix.d_alpha);
+    dfree(h->ix.d_pt);
     delete h;
     return SOS_OK;
 }
@@ -367,34 +410,34 @@ int sos_plan_create_ex(const sos_index* h, int64_t r, const sos_plan_opts* opts,
 int sos_plan_destroy(sos_plan* pl) {
     if (!pl) return SOS_OK;
     Plan& P = pl->P;
-    cudaFree(P.d_vq);
-    cudaFree(P.d_vtq);
-    cudaFree(P.d_vtq2);
-    cudaFree(P.d_rq);
-    cudaFree(P.d_vrow);
-    cudaFree(P.d_vcol);
-    cudaFree(P.d_rrow);
-    cudaFree(P.d_dbuf);
-    cudaFree(P.d_opt);
-    cudaFree(P.d_rlev);
-    cudaFree(P.d_hV);
-    cudaFree(P.d_hp);
-    cudaFree(P.d_hl);
+    dfree(P.d_vq);
+    dfree(P.d_vtq);
+    dfree(P.d_vtq2);
+    dfree(P.d_rq);
+    dfree(P.d_vrow);
+    dfree(P.d_vcol);
+    dfree(P.d_rrow);
+    dfree(P.d_dbuf);
+    dfree(P.d_opt);
+    dfree(P.d_rlev);
+    dfree(P.d_hV);
+    dfree(P.d_hp);
+    dfree(P.d_hl);
     if (P.gexec) cudaGraphExecDestroy(P.gexec);
-    cudaFree(P.d_coef);
-    cudaFree(P.d_res);
-    cudaFree(P.d_m);
-    cudaFree(P.d_v);
-    cudaFree(P.d_scal);
-    cudaFree(P.d_ring);
-    cudaFree(P.d_progress);
-    cudaFree(P.d_tiles_fwd);
-    cudaFree(P.d_tiles_bwd);
-    cudaFree(P.d_rowsig);
-    cudaFree(P.d_grad);
-    cudaFree(P.d_part);
-    cudaFree(P.d_rrowx);
-    cudaFree(P.d_urowr);
+    dfree(P.d_coef);
+    dfree(P.d_res);
+    dfree(P.d_m);
+    dfree(P.d_v);
+    dfree(P.d_scal);
+    dfree(P.d_ring);
+    dfree(P.d_progress);
+    dfree(P.d_tiles_fwd);
+    dfree(P.d_tiles_bwd);
+    dfree(P.d_rowsig);
+    dfree(P.d_grad);
+    dfree(P.d_part);
+    dfree(P.d_rrowx);
+    dfree(P.d_urowr);
     if (P.copy_st) cudaStreamDestroy(P.copy_st);
     if (P.sig_ev) cudaEventDestroy(P.sig_ev);
     if (P.timing) {
@@ -601,7 +644,7 @@ static int ensure_vtq2(Plan& P) {
     if (rc) return rc;
     if (cudaMemset(P.d_vtq2, 0, bytes) != cudaSuccess ||
         !make_q_tmap(P.tmap_vtq2_b, P.d_vtq2, P.rowsVT, P.nkbN, kHalfN)) {
-        cudaFree(P.d_vtq2);
+        dfree(P.d_vtq2);
         P.d_vtq2 = nullptr;
         return fail(SOS_ERR_CUDA, "second VTQ buffer");
     }
@@ -770,7 +813,7 @@ int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t ste
     // device staging buffers live with the plan (no per-call cudaMalloc / cudaFree)
     if (!P.d_hV && ((rc = dalloc(&P.d_hV, vb)) || (rc = dalloc(&P.d_hp, pb)))) return rc;
     if (P.hl_cap < steps) {
-        cudaFree(P.d_hl);
+        dfree(P.d_hl);
         P.d_hl = nullptr;
         P.hl_cap = 0;
         if ((rc = dalloc(&P.d_hl, sizeof(double) * steps))) return rc;
@@ -814,5 +857,46 @@ int sos_solve_host(sos_plan* pl, float* V_host, const float* p_host, int64_t ste
         return fail(SOS_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
     return SOS_OK;
 }
+
+#ifdef SOS_EXPERIMENTS
+// Experiment build only (not in include/sos_b200.h): number of live device
+// allocations of the library whose guard margins are no longer all 0xFF; the
+// first one is described in sos_last_error().  Synchronises the device.
+int sos_exp_check_guards(int64_t* n_allocs) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail(SOS_ERR_CUDA, "%s", cudaGetErrorString(cudaGetLastError()));
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    std::vector<unsigned char> h(kGuardBytes);
+    int bad = 0;
+    for (const auto& kv : g_guards) {
+        const GuardRec& g = kv.second;
+        for (int side = 0; side < 2; ++side) {
+            const char* src = side ? g.base + kGuardBytes + g.bytes : g.base;
+            if (cudaMemcpy(h.data(), src, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+                return fail(SOS_ERR_CUDA, "guard read: %s", cudaGetErrorString(cudaGetLastError()));
+            size_t k = 0;
+            while (k < kGuardBytes && h[k] == 0xFF) ++k;
+            if (k < kGuardBytes) {
+                if (!bad++)
+                    fail(SOS_ERR_CUDA, "write %s a %zu-byte allocation (margin byte %zu)", side ? "past the end of" : "before",
+                         g.bytes, k);
+                break;
+            }
+        }
+    }
+    if (n_allocs) *n_allocs = (int64_t)g_guards.size();
+    return bad ? -bad : SOS_OK;
+}
+
+// Experiment build only: negative control for the check above -- writes one
+// zero byte just past the end of the largest live allocation.
+int sos_exp_poke_guard(void) {
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    const GuardRec* big = nullptr;
+    for (const auto& kv : g_guards)
+        if (!big || kv.second.bytes > big->bytes) big = &kv.second;
+    if (!big) return fail(SOS_ERR_ARG, "no live allocation");
+    return cudaMemset(big->base + kGuardBytes + big->bytes, 0, 1) == cudaSuccess ? SOS_OK : fail(SOS_ERR_CUDA, "poke");
+}
+#endif
 
 }  // extern "C"

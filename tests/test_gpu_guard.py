@@ -185,3 +185,21 @@ def test_guard_bands_long_k_default_plan(sos, kind):
     headroom R scales, K-skew pacing off / on by operand size); r = 3001 is off
     every tile and vector multiple."""
     _descend_guarded(sos, 16, 4, 3001, {}, kind)
+
+
+@pytest.mark.timeout(900)
+def test_scratch_guards_experiment_build():
+    """The library's own allocations (index tables, slices, scales, staging,
+    optimiser state): tools/scratch_guard_check.py runs every call on ragged
+    shapes in every variant through the -DSOS_EXPERIMENTS build, whose
+    allocations sit between 64 KB margins and start as NaN bytes, and fails on
+    a changed margin, a non-finite result or a difference from the shipped
+    library.  A subprocess: this process has the shipped library loaded."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, os.path.join(root, "tools", "scratch_guard_check.py")],
+                         capture_output=True, text=True, timeout=850)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert "0 problems" in res.stdout

@@ -5,7 +5,7 @@ ragged shapes in every implementation variant, then asks the library which
 margins changed (sos_exp_check_guards) and checks that every result is finite
 and equals the shipped library's -- a scratch buffer read before it is written,
 or read past its end into a float margin, would put a NaN into a result.
-python tools/scratch_guard_check.py [quick]    (exit code 0 = clean)
+python tools/scratch_guard_check.py [quick|big]    (exit code 0 = clean; big = configs 3 and 4 only)
 """
 import ctypes, os, subprocess, sys
 import numpy as np
@@ -24,6 +24,8 @@ if EXP:
 SHAPES = [(5, 3, 37), (7, 3, 85), (7, 4, 163), (9, 4, 321), (9, 4, 700), (11, 4, 1001)]
 if "quick" not in sys.argv:
     SHAPES += [(16, 4, 3001)]  # N = 3876: the long-K default plan
+if "big" in sys.argv:  # configs 3 and 4 alone, default plan, Adam (what bench.py times)
+    SHAPES = [(12, 6, 12376), (17, 5, 20349)]
 VARIANTS = [dict(), dict(tiny=True), dict(tiny=False, split=True), dict(tiny=False, split=False),
             dict(tiny=False, split=False, narrow_tiles=False, rmax_direct=False),
             dict(tiny=False, split=False, vtq_in_aux=False, vtq_from_update=False, r_headroom=False),
@@ -59,13 +61,16 @@ def run(n, d, r, opts, kind):
     return [o.detach().double().cpu().numpy().ravel() for o in out]
 
 
+N_BIG = "big" in sys.argv
+
+
 def main():
     results, bad = {}, 0
     for (n, d, r) in SHAPES:
         for vi, opts in enumerate(VARIANTS):
-            if n >= 16 and vi not in (0, 2, 4):
+            if n >= 16 and vi not in (0, 2, 4) or N_BIG and vi:
                 continue
-            for kind in ("adam", "gd"):
+            for kind in ("adam",) if N_BIG else ("adam", "gd"):
                 key = f"{n},{d},{r},{vi},{kind}"
                 o = run(n, d, r, opts, kind)
                 if not all(np.isfinite(x).all() for x in o):
@@ -101,7 +106,7 @@ if __name__ == "__main__":
     if EXP:  # the same calls through the shipped library, in a fresh process
         path = "/tmp/scratch_guard_release.npz"
         subprocess.run([sys.executable, os.path.abspath(__file__), "--release", "--save=" + path] +
-                       [a for a in sys.argv[1:] if a == "quick"], check=True)
+                       [a for a in sys.argv[1:] if a in ("quick", "big")], check=True)
         ref = np.load(path)
         worst = 0.0
         for k, v in results.items():

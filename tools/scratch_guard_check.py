@@ -25,7 +25,7 @@ SHAPES = [(5, 3, 37), (7, 3, 85), (7, 4, 163), (9, 4, 321), (9, 4, 700), (11, 4,
 if "quick" not in sys.argv:
     SHAPES += [(16, 4, 3001)]  # N = 3876: the long-K default plan
 if "big" in sys.argv:  # configs 3 and 4 alone, default plan, Adam (what bench.py times)
-    SHAPES = [(12, 6, 12376), (17, 5, 20349)]
+    SHAPES = [(12, 6, 12376), (17, 5, 20349), (21, 5, 96)]  # the last: N = 53130, segmented-s32 backward
 VARIANTS = [dict(), dict(tiny=True), dict(tiny=False, split=True), dict(tiny=False, split=False),
             dict(tiny=False, split=False, narrow_tiles=False, rmax_direct=False),
             dict(tiny=False, split=False, vtq_in_aux=False, vtq_from_update=False, r_headroom=False),

@@ -95,3 +95,8 @@ def test_experiment_build_compiles_and_exports():
     missing = [n for n in declared_functions() if not hasattr(exp, n)]
     assert not missing, missing
     assert b"SOS_GEMM_PROBE" in open(path, "rb").read()
+    # the guarded-allocation check (tools/scratch_guard_check.py) exists only there
+    from paper_2410_19844_b200.binding import LIB_PATH
+    rel = ctypes.CDLL(LIB_PATH)
+    for name in ("sos_exp_check_guards", "sos_exp_poke_guard"):
+        assert hasattr(exp, name) and not hasattr(rel, name), name

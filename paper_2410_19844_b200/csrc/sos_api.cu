@@ -424,6 +424,8 @@ int sos_plan_destroy(sos_plan* pl) {
     dfree(P.d_hp);
     dfree(P.d_hl);
     if (P.gexec) cudaGraphExecDestroy(P.gexec);
+    for (cudaGraphExec_t& g : P.gexec_long)
+        if (g) cudaGraphExecDestroy(g);
     dfree(P.d_coef);
     dfree(P.d_res);
     dfree(P.d_m);
@@ -540,6 +542,10 @@ int sos_opt_init(sos_plan* pl, const sos_opt_params* prm, void* stream) {
     if (P.gexec) {  // the captured steps bake in the optimiser kind and moment buffers
         cudaGraphExecDestroy(P.gexec);
         P.gexec = nullptr;
+    }
+    for (cudaGraphExec_t& g : P.gexec_long) {
+        if (g) cudaGraphExecDestroy(g);
+        g = nullptr;
     }
     if (prm->kind == SOS_OPT_ADAM) {
         if (!(prm->beta1 >= 0.f && prm->beta1 < 1.f && prm->beta2 >= 0.f && prm->beta2 < 1.f))
@@ -701,6 +707,8 @@ static int descend_step(Plan& P, const DescendPtrs& d, int b, float* V, const fl
     return check_launch("descend step");
 }
 
+constexpr int kLongGraphPairs[2] = {16, 4};  // pairs of steps per replay of a split plan's long graphs
+
 // K descent steps; with sig_last the final step runs outside the graph with the
 // row-chunk release of V on (P.d_rowsig zeroed, then P.sig_ev recorded, on st)
 static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps, double* losses_dev, cudaStream_t st,
@@ -743,32 +751,52 @@ static int descend_impl(Plan& P, float* V_dev, const float* p_dev, int64_t steps
     const bool timing = P.timing && P.timing->on;  // per-kernel events need plain launches
     const int64_t keep_plain = sig_last ? 1 : 0;      // the signalling step is never replayed
     if (left >= 2 + keep_plain && !timing) {
-        // steps 1, 2 (parities 1, 0) captured once as a graph, replayed for every pair
+        // steps 1, 2 (parities 1, 0) captured once as a graph, replayed for every pair;
+        // split plans (a step of 4 short kernels chained by programmatic dependent
+        // launch, which does not reach across graph launches) also keep a graph of
+        // graphs of 16 and 4 pairs, so that a graph boundary (~3 us) falls on every 32nd
+        // or 8th step instead of every 2nd
         const void* key[3] = {V_dev, p_dev, nullptr};  // the loss array is read from DevOpt
-        if (!P.gexec || memcmp(key, P.gkey, sizeof(key)) != 0) {
-            if (P.gexec) {
-                cudaGraphExecDestroy(P.gexec);
-                P.gexec = nullptr;
+        if (memcmp(key, P.gkey, sizeof(key)) != 0) {
+            if (P.gexec) cudaGraphExecDestroy(P.gexec);
+            for (cudaGraphExec_t& g : P.gexec_long) {
+                if (g) cudaGraphExecDestroy(g);
+                g = nullptr;
             }
+            P.gexec = nullptr;
+            memcpy(P.gkey, key, sizeof(key));
+        }
+        auto capture = [&](cudaGraphExec_t* exec, int pairs) -> int {
+            if (*exec) return SOS_OK;
             cudaStream_t cs;
             CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
             const int64_t l0 = P.launches;
             cudaGraph_t graph = nullptr;
             cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-            int rc1 = e == cudaSuccess ? descend_step(P, d, 1, V_dev, p_dev, losses_dev, cs) : SOS_ERR_CUDA;
-            int rc2 = e == cudaSuccess && !rc1 ? descend_step(P, d, 0, V_dev, p_dev, losses_dev, cs) : SOS_ERR_CUDA;
+            int rcs = e == cudaSuccess ? SOS_OK : SOS_ERR_CUDA;
+            for (int k = 0; k < 2 * pairs && !rcs; ++k)
+                rcs = descend_step(P, d, (k + 1) & 1, V_dev, p_dev, losses_dev, cs);
             cudaError_t e2 = cudaStreamEndCapture(cs, &graph);
-            P.glaunches = P.launches - l0;
+            P.glaunches = (P.launches - l0) / pairs;
             P.launches = l0;
             cudaStreamDestroy(cs);
-            if (e != cudaSuccess || rc1 || rc2 || e2 != cudaSuccess ||
-                cudaGraphInstantiate(&P.gexec, graph, 0) != cudaSuccess) {
+            if (e != cudaSuccess || rcs || e2 != cudaSuccess || cudaGraphInstantiate(exec, graph, 0) != cudaSuccess) {
                 if (graph) cudaGraphDestroy(graph);
-                P.gexec = nullptr;
+                *exec = nullptr;
                 return fail(SOS_ERR_CUDA, "descend graph capture failed: %s", cudaGetErrorString(cudaGetLastError()));
             }
             cudaGraphDestroy(graph);
-            memcpy(P.gkey, key, sizeof(key));
+            return SOS_OK;
+        };
+        if ((rc = capture(&P.gexec, 1))) return rc;
+        for (int g = 0; g < 2 && P.split; ++g) {
+            const int pairs = kLongGraphPairs[g];
+            if (left < 2 * pairs + keep_plain) continue;
+            if ((rc = capture(&P.gexec_long[g], pairs))) return rc;
+            for (; left >= 2 * pairs + keep_plain; left -= 2 * pairs) {
+                CK(cudaGraphLaunch(P.gexec_long[g], st));
+                P.launches += P.glaunches * pairs;
+            }
         }
         for (; left >= 2 + keep_plain; left -= 2) {
             CK(cudaGraphLaunch(P.gexec, st));

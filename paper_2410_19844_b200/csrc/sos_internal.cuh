@@ -212,9 +212,10 @@ struct Plan {
     DevOpt* d_opt;    // device copy of the optimiser parameters + step counter
     // sos_descend: a captured pair of steps, replayed with cudaGraphLaunch
     cudaGraphExec_t gexec;
-    const void* gkey[3];   // (V, p, -) the graph was captured for
+    cudaGraphExec_t gexec_long[2];  // split plans: kLongGraphPairs[i] pairs per replay (fewer graph boundaries)
+    const void* gkey[3];   // (V, p, -) the graphs were captured for
     double* h_losses;      // host copy of the current sos_descend call's loss array pointer
-    int64_t glaunches;     // kernels per replay (launch accounting)
+    int64_t glaunches;     // kernels per replay of the pair graph (launch accounting)
     // sos_solve_host: device staging of the caller's host buffers (lazy)
     float* d_hV;
     float* d_hp;

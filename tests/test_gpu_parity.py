@@ -629,6 +629,33 @@ def test_descend_matches_steps(sos, kind, lr, r, variant):
     assert lo < ld[0].item()
 
 
+@pytest.mark.parametrize("kind,lr", [("gd", 5e-3), ("adam", 1e-3)])
+@pytest.mark.parametrize("steps", [9, 47, 100])
+def test_descend_split_graph_cascade_vs_oracle(sos, steps, kind, lr):
+    """A split plan's sos_descend replays graphs of 16, 4 and 1 pairs of steps
+    (47 = 1 plain + 32 + 8 + 3 x 2; 100 = 1 + 3 x 32 + 2 + 1 plain; 9 = 1 + 8):
+    V_t and every loss against the oracle's descent at config 1."""
+    c = si.CONFIGS["c1_n8_2d8"]
+    o = oracle(c.n, c.d)
+    ix = sos.SosIndex(c.n, c.d)
+    plan = sos.SosPlan(ix, c.r, split=True, tiny=False)
+    p = o.forward(si.planted_w(o.N, c.r_star, 0)).astype(np.float32)
+    V0 = si.v0(o.N, c.r, 3)
+    plan.opt_init(kind, lr)
+    Vd = torch.from_numpy(V0.copy()).cuda()
+    ld = plan.descend(Vd, torch.from_numpy(p).cuda(), steps).cpu().numpy()
+    Vo, Lo = o.descent(V0, p, kind, steps, lr)
+    # loss bar along a trajectory: 1e-4.  The 1e-5 bar holds for L at a given V (tested
+    # above); here V_t itself carries the accumulated ~2e-6 and the residual shrinks, so
+    # the relative loss error grows with t (GD: ~5e-6 at step 9, 1.2e-5 .. 1.9e-5 at step
+    # 100, varying with the order of the forward's atomics; Adam ~7e-7)
+    L = Lo[:steps]
+    err, lerr = rel_l2(Vd.cpu().numpy() - V0, Vo - V0), np.max(np.abs(ld - L) / L)
+    print(f"graph cascade {kind} {steps} steps: dV rel err {err:.2e}, worst loss rel err {lerr:.2e}")
+    assert err <= 1e-4
+    assert lerr <= 1e-4
+
+
 def test_descend_reaches_1e8_config2_and_stops(sos):
     """Config 2 through sos_descend with the device-side stopping rule: the
     iteration freezes at the first V with eps_rel <= 0.5e-8, checked by the
